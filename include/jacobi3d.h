@@ -1,0 +1,192 @@
+/*
+ * jacobi3d.h -- C ABI of the B200-native overdecomposed Jacobi3D library
+ * (libjacobi3d.so, built from paper_2605_12734_b200/csrc/).
+ *
+ * The operation (§5 "jacobi2d": "applies the Jacobi iterative method
+ * on a 2D grid. The grid is divided among charm++ chares/MPI ranks, which
+ * communicate by halo exchanges. The application is run for 100 iterations without
+ * convergence checks"), lifted to 3D: a global fp64 grid of
+ * nx*ny*nz updated points plus a fixed 1-cell Dirichlet shell (R6, R7) is swept
+ *     u'(p) = ((((((u(p) + u(x-)) + u(x+)) + u(y-)) + u(y+)) + u(z-)) + u(z+)) * fl(1/7)
+ * (R2-R4).  The grid is overdecomposed into bx*by*bz blocks ("chares"), ODF =
+ * blocks / GPUs (§3.1 "putting 8-16 chares per GPU device"),
+ * each block with its own ghosted storage; every iteration exchanges faces between
+ * blocks on the same GPU and on other GPUs (§4) and sweeps
+ * every block.  Results are bit-identical to the undecomposed iteration for every
+ * ODF and GPU count.
+ *
+ * Conventions for every function:
+ *   - returns JAC_OK (0) or a negative jac_status; on error jac_last_error()
+ *     returns a thread-local message naming the offending argument.
+ *   - host pointers are borrowed for the duration of the call only; the context
+ *     owns every device allocation, stream, event and CUDA graph it creates.
+ *   - one context is driven by one host thread at a time (no internal locking).
+ *   - padded host arrays are (nz+2)*(ny+2)*(nx+2) doubles, x fastest:
+ *     p(i,j,k) = (k*(ny+2) + j)*(nx+2) + i, 0 <= i <= nx+1 etc.; interior is
+ *     1..nx, 1..ny, 1..nz.
+ *   - block (ix,iy,iz) covers interior points [ix*ex,(ix+1)*ex) x [iy*ey,..) x
+ *     [iz*ez,..) (0-based), ex = nx/bx etc.; GPU partitions are contiguous
+ *     sub-boxes of the block grid (SPEC.md:259-265 contiguous block_map),
+ *     partition id g = (pz*gy + py)*gx + px.
+ */
+#ifndef JACOBI3D_H
+#define JACOBI3D_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+#if defined(__GNUC__)
+#pragma GCC visibility push(default) /* the library is built with -fvisibility=hidden */
+#endif
+
+typedef struct jac_ctx jac_ctx; /* opaque */
+
+enum jac_status {
+    JAC_OK = 0,
+    JAC_EINVAL = -1,  /* null pointer, extent < 1, n_gpus < 1, n_iters < 0, bad index */
+    JAC_EDECOMP = -2, /* nx % bx, bx % gx (likewise y, z), gx*gy*gz != n_gpus, or
+                         (bx*by*bz) % n_gpus != 0 (non-integral ODF): SPEC.md:254-258,
+                         "tiling mismatch -> configuration error" SPEC.md:475 */
+    JAC_EDEVICE = -3, /* no CUDA device, device not sm_100, too few devices */
+    JAC_ENOMEM = -4,  /* device or pinned-host allocation failed */
+    JAC_ECUDA = -5,   /* any other CUDA runtime / driver error (message has the name) */
+    JAC_ENCCL = -6,   /* reserved for the NCCL transport (JAC_F_NCCL) */
+    JAC_ESTATE = -7   /* call out of order: jac_step before init, import twice, ... */
+};
+
+enum jac_flags {
+    JAC_F_DEFAULT = 0,
+    JAC_F_FMA = 1u << 0,          /* accepted, no effect: the update has no a*b+c (R5) */
+    JAC_F_NO_GRAPH = 1u << 1,     /* launch every kernel from the host each iteration
+                                     (ablation of the CUDA-Graph iteration) */
+    JAC_F_NCCL = 1u << 2,         /* reserved: NCCL send/recv transport (not built yet) */
+    JAC_F_UNFUSED_PACK = 1u << 4, /* north-star layout: the sweep packs faces into an
+                                     outbox and a separate batched ghost-copy kernel
+                                     fills the ghosts (PAPER.md:90 pack/unpack kernels) */
+    JAC_F_NO_TMA = 1u << 5,       /* plain per-point global-load sweep (no TMA staging) */
+    JAC_F_VIRTUAL_GPUS = 1u << 6, /* test-only: all n_gpus partitions live on device 0 and
+                                     are swept by ONE kernel (no cross-partition waits);
+                                     exercises the partition / REMOTE-face logic */
+    JAC_F_SKIP_EXCHANGE = 1u << 7 /* timing-only ablation: no face writes. WRONG results */
+};
+
+/* Face kinds of the block-descriptor table (the analog of the paper's pre-filled
+ * location table, "requires a runtime option that pre-fills the
+ * location table", and its three transports). */
+enum jac_face_kind { JAC_FACE_BOUNDARY = 0, JAC_FACE_LOCAL = 1, JAC_FACE_REMOTE = 2 };
+
+/* ---------------------------------------------------------------- planning (host only)
+ * Pure host computation, no device needed.  Validates a decomposition and returns
+ * the GPU grid (given, or by the minimum-inter-GPU-face-area rule R10 when
+ * gpu_grid_in is NULL; ties prefer splitting z, then y, then x) and the uniform
+ * block extent.  gpu_grid_out[3] and block_extent_out[3] are caller-owned. */
+int jac_plan(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, int32_t bz,
+             int32_t n_gpus, const int32_t *gpu_grid_in, int32_t *gpu_grid_out,
+             int64_t *block_extent_out);
+
+/* Face kind and neighbour of face f (0..5 = x-,x+,y-,y+,z-,z+) of block (ix,iy,iz)
+ * under the plan above.  *owner = partition owning the neighbour (or -1 at the
+ * global boundary).  Host only. */
+int jac_plan_face(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, int32_t bz,
+                  int32_t n_gpus, const int32_t *gpu_grid_in, int32_t ix, int32_t iy,
+                  int32_t iz, int32_t f, int32_t *kind, int32_t *owner);
+
+/* ---------------------------------------------------------------- lifecycle
+ * jac_create: one process drives all n_gpus partitions.  Partition g runs on CUDA
+ * device g, or on device 0 for every g under JAC_F_VIRTUAL_GPUS.  Multi-device
+ * single-process contexts are not supported this round (use jac_create_rank, one
+ * process per GPU); n_gpus > 1 without JAC_F_VIRTUAL_GPUS returns JAC_EINVAL.
+ * Allocates everything (two ghosted arrays per block, descriptor table, control
+ * words, streams, events); nothing is allocated inside jac_step (PAPER.md:190-194
+ * "persistent Views ... preallocated buffers"). *out receives the context. */
+int jac_create(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, int32_t bz,
+               int32_t n_gpus, const int32_t *gpu_grid, uint32_t flags, jac_ctx **out);
+
+/* jac_create_rank: the calling process owns partition `rank` of n_gpus on CUDA
+ * device `device` (one process per GPU).  Before jac_set_init the ranks exchange
+ * their IPC handles (jac_export_ipc on every rank, all-gather, jac_import_ipc on
+ * every rank); faces to other ranks are then stored directly into the peer's
+ * ghost cells over NVLink by the sweep kernel (the single-copy replacement of the
+ * paper's two-copy IPC staging).  All ranks must call jac_set_init*,
+ * jac_step and jac_destroy collectively with the same arguments. */
+int jac_create_rank(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, int32_t bz,
+                    int32_t n_gpus, const int32_t *gpu_grid, int32_t rank, int32_t device,
+                    uint32_t flags, jac_ctx **out);
+
+/* Bytes of one rank's exported handle record (a cudaIpcMemHandle plus layout
+ * fingerprint). */
+size_t jac_ipc_handle_bytes(void);
+/* Writes this rank's record into out[jac_ipc_handle_bytes()]. */
+int jac_export_ipc(jac_ctx *c, void *out);
+/* all = n_gpus records in rank order (all-gathered by the caller).  Opens the
+ * neighbours' memory, fills REMOTE face pointers of the device table. */
+int jac_import_ipc(jac_ctx *c, const void *all);
+
+/* Copies the padded initial field (host, see conventions) into BOTH ghosted
+ * buffers of every local block, ghosts included, so the shell is Dirichlet data in
+ * both ("outer halo = initial boundary values") and the first sweep's
+ * ghosts are the neighbours' initial values.  Resets iterations_done to 0.  A
+ * pinned host array is copied by DMA; a pageable one is staged by the driver. */
+int jac_set_init(jac_ctx *c, const double *padded);
+/* Device-side synthetic init: every padded cell p gets R11's splitmix64 hash value
+ * of key (seed << 40) + p, scaled to [0,1). */
+int jac_set_init_hash(jac_ctx *c, uint64_t seed);
+
+/* Runs exactly n_iters >= 0 Jacobi sweeps (R12; 0 = identity; accumulates across
+ * calls).  Blocking: returns after this context's GPUs finish. */
+int jac_step(jac_ctx *c, int32_t n_iters);
+
+/* Interior of block (ix,iy,iz) after the sweeps so far, ex*ey*ez doubles, x fastest,
+ * into caller-owned host `out`.  The block must be local to this context. */
+int jac_get_block(jac_ctx *c, int32_t ix, int32_t iy, int32_t iz, double *out);
+/* Debug (pin P11): the whole ghosted block of the current buffer,
+ * (ex+2)*(ey+2)*(ez+2) doubles, x fastest. */
+int jac_get_block_padded(jac_ctx *c, int32_t ix, int32_t iy, int32_t iz, double *out);
+/* Interiors of all local blocks written into the padded host array (shell and
+ * non-local blocks untouched). */
+int jac_get_field(jac_ctx *c, double *padded);
+
+int jac_get_layout(const jac_ctx *c, int32_t *gpu_grid, int64_t *block_extent,
+                   int64_t *iterations_done);
+/* Partition (GPU) owning block (ix,iy,iz). */
+int jac_block_owner(const jac_ctx *c, int32_t ix, int32_t iy, int32_t iz, int32_t *gpu);
+
+/* Device time of the last jac_step (CUDA events recorded on the launching
+ * stream(s) around its launches; max over this context's devices), in ms. */
+int jac_last_step_ms(const jac_ctx *c, double *ms);
+/* Runs n_iters sweeps launched one by one without a graph, with CUDA events
+ * around every sweep-kernel launch; returns the average sweep-kernel duration in
+ * ms (for the roofline's per-launch figure).  Advances the state like jac_step. */
+int jac_profile_sweep(jac_ctx *c, int32_t n_iters, double *avg_sweep_ms);
+
+enum jac_stat {
+    JAC_STAT_KERNEL_LAUNCHES = 0, /* our kernels launched so far (graph nodes counted) */
+    JAC_STAT_GRAPH_LAUNCHES = 1,
+    JAC_STAT_KERNELS_PER_ITER = 2,
+    JAC_STAT_LOCAL_BLOCKS = 3,
+    JAC_STAT_LOCAL_FACES = 4,     /* exchanged LOCAL faces per iteration */
+    JAC_STAT_REMOTE_FACES = 5,    /* exchanged REMOTE faces per iteration */
+    JAC_STAT_REMOTE_BYTES = 6,    /* bytes stored to peers per iteration */
+    JAC_STAT_ARENA_BYTES = 7,     /* device bytes of the ghosted block arena */
+    JAC_STAT_SWEEP_VARIANT = 8,   /* 0 = TMA z-march, 1 = plain loads */
+    JAC_STAT_N = 9
+};
+int jac_get_stats(const jac_ctx *c, int64_t *stats /* [JAC_STAT_N] */);
+
+/* NULL-safe.  Rank contexts: every rank must have finished its last jac_step
+ * (caller barrier) before any rank destroys. */
+int jac_destroy(jac_ctx *c);
+
+const char *jac_last_error(void);
+int jac_version(void); /* 10000*major + 100*minor + patch */
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+#ifdef __cplusplus
+}
+#endif
+#endif /* JACOBI3D_H */

@@ -1,0 +1,66 @@
+// device.hpp -- data shared by the host engine and the sm_100a kernels:
+// the device-resident block-descriptor table (north-star subsystem 1) and the
+// launch arguments.  No method arithmetic lives here.
+//
+// HBM layout.  Every block ("chare") owns two ghosted arrays (ping,
+// pong) of (ez+2) planes x (ey+2) rows x P doubles.  Element (i,j,k) of a block,
+// i in [-1,ex], j in [-1,ey], k in [-1,ez] (-1 and e* are ghosts), lives at
+//     base + (k+1)*Q + (j+1)*P + A + i,      Q = P*(ey+2)
+// with A = 4 so the interior row starts on a 32-byte sector (and 16-byte aligned
+// double2 accesses), P = round_up(A+ex+2, 4).  All slots of one GPU sit in one
+// arena: slot s of buffer b starts at arena + (b*nslots + s)*bstride, which lets ONE
+// 4-D TMA tensor map {P, ey+2, ez+2, 2*nslots} cover every block of the GPU.
+#pragma once
+#include <cstdint>
+
+namespace jac {
+
+enum Face { XM = 0, XP = 1, YM = 2, YP = 3, ZM = 4, ZP = 5 };
+inline constexpr int opposite(int f) { return f ^ 1; }
+
+constexpr int kA = 4;        // x offset of interior column 0 inside a row
+constexpr int kMaxParts = 1024;
+
+struct DevBlock {
+    int32_t slot;            // own slot in this GPU's arena
+    int32_t org[3];          // global interior origin of the block (x, y, z)
+    double *nb[6][2];        // neighbour block array base for buffer 0/1, local or
+                             // peer-mapped (IPC); nullptr = global boundary face
+    const double *nb_out[6]; // neighbour's outbox region for the face opposite to f
+                             // (JAC_F_UNFUSED_PACK only)
+};
+
+struct Geom {
+    int32_t ex, ey, ez;      // block interior extents
+    int32_t A;               // = kA
+    int64_t P, Q;            // row / plane pitch in doubles
+    int64_t bstride;         // doubles between consecutive slots (256-byte multiple)
+    int32_t nslots;          // slots per buffer in the arena
+    int32_t pad_;
+    int64_t ostride;         // outbox doubles per slot
+    int64_t ooff[6];         // outbox face offsets inside a slot
+};
+
+enum SweepMode { MODE_FUSED = 0, MODE_PACK = 1, MODE_NOEXCHANGE = 2 };
+
+struct SweepArgs {
+    Geom g;
+    const DevBlock *blocks;  // [nslots]
+    double *arena;
+    double *outbox;
+    int32_t src;             // buffer read (0/1); the sweep writes 1-src
+    int32_t mode;            // SweepMode
+    int32_t ntx, nty, ntz;   // tiles per block in x, y, z
+    int32_t zc;              // planes per z-chunk
+};
+
+// Neighbour barrier between ranks (one process per GPU): one flag word per sender
+// in the receiver's control block, monotonically increasing epochs.
+struct BarrierArgs {
+    uint64_t *ctrl;          // own control block: [0] = epoch, [1 + sender] = flags
+    uint64_t *peer_slot[6];  // for each face-adjacent rank (<= 6): &peer_ctrl[1 + my_rank]
+    int32_t peer_id[6];      // neighbour rank ids
+    int32_t npeers;
+};
+
+}  // namespace jac

@@ -1,0 +1,766 @@
+// engine.cu -- host engine + C ABI (include/jacobi3d.h).
+//
+// Owns, per context (one CUDA device; one process per GPU for multi-GPU runs):
+//   * the block-descriptor table (north-star subsystem 1), built once from the
+//     planner and copied to the device; REMOTE faces carry IPC-mapped peer pointers
+//     (the paper's pre-filled location table + transport selection, PAPER.md:230,
+//     266-275, resolved once instead of per message);
+//   * one arena holding both ghosted buffers of every local block, one 4-D TMA
+//     tensor map over it, optional outbox (JAC_F_UNFUSED_PACK), control words;
+//   * one stream, CUDA graphs of the iteration (north-star subsystem 5; PAPER.md:86
+//     "CUDA Graphs to amortize kernel launch overhead"), timing events.
+// Nothing is allocated inside jac_step (persistent views and
+// preallocated scratch instead of allocations that imply fences).
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/jacobi3d.h"
+#include "device.hpp"
+#include "kernels.hpp"
+#include "plan.hpp"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char *fmt, ...)
+{
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define CK(call)                                                                             \
+    do {                                                                                     \
+        cudaError_t e_ = (call);                                                             \
+        if (e_ != cudaSuccess)                                                               \
+            return fail(e_ == cudaErrorMemoryAllocation ? JAC_ENOMEM : JAC_ECUDA, "%s: %s (%s:%d)", \
+                        #call, cudaGetErrorString(e_), __FILE__, __LINE__);                  \
+    } while (0)
+
+constexpr uint32_t kIpcMagic = 0x4A414333u;  // "JAC3"
+
+struct IpcRecord {
+    uint32_t magic;
+    int32_t rank;
+    uint64_t fingerprint;
+    uint64_t arena_off, outbox_off, ctrl_off;
+    cudaIpcMemHandle_t handle;
+    unsigned char pad_[256 - 40 - sizeof(cudaIpcMemHandle_t)];
+};
+static_assert(sizeof(IpcRecord) == 256, "IPC record size");
+
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
+                                    const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
+                                    const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                    CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+}  // namespace
+
+struct jac_ctx {
+    jac::Plan plan{};
+    uint32_t flags = 0;
+    bool rank_mode = false;
+    int32_t rank = 0;         // partition owned in rank mode
+    int device = 0;
+    std::vector<int32_t> parts;  // partitions hosted by this context
+    int32_t nslots = 0;
+    std::vector<int32_t> slot_part, slot_local;  // partition / local slot of each slot
+
+    jac::Geom geom{};
+    char *alloc = nullptr;    // single allocation: [ctrl][arena][outbox]
+    size_t alloc_bytes = 0, ctrl_off = 0, arena_off = 0, outbox_off = 0;
+    uint64_t *ctrl = nullptr;
+    double *arena = nullptr, *outbox = nullptr;
+    std::vector<jac::DevBlock> hblocks;
+    jac::DevBlock *dblocks = nullptr;
+
+    int variant = 0;          // 0 TMA wide, 1 TMA narrow, 2 plain
+    CUtensorMap tmap{};
+    int ntx = 1, nty = 1, ntz = 1, zc = 1;
+
+    // cross-rank exchange
+    std::vector<int32_t> peer_ranks;     // face-adjacent ranks
+    std::vector<void *> ipc_opened;
+    bool ipc_done = false;
+    jac::BarrierArgs bar{};
+
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    cudaGraphExec_t g1[2] = {nullptr, nullptr}, gU[2] = {nullptr, nullptr};
+    int unroll = 10;
+
+    bool inited = false;
+    int64_t iters = 0;
+    double last_ms = 0.0;
+    int64_t kernel_launches = 0, graph_launches = 0;
+    int64_t local_faces = 0, remote_faces = 0, remote_bytes = 0;
+
+    bool has_remote() const { return !peer_ranks.empty(); }
+    int kernels_per_iter() const
+    {
+        int k = 1;
+        if (flags & JAC_F_UNFUSED_PACK) k += 1 + (has_remote() ? 2 : 0);
+        else if (has_remote()) k += 1;
+        return k;
+    }
+    double *slot_ptr(int buf, int slot) const
+    {
+        return arena + (int64_t)(buf * nslots + slot) * geom.bstride;
+    }
+};
+
+namespace {
+
+int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
+
+uint64_t fingerprint(const jac_ctx *c)
+{
+    uint64_t h = 1469598103934665603ull;
+    auto mix = [&](uint64_t v) { h = (h ^ v) * 1099511628211ull; };
+    for (int d = 0; d < 3; ++d) { mix(c->plan.n[d]); mix(c->plan.b[d]); mix(c->plan.g[d]); }
+    mix(c->plan.n_gpus); mix(c->flags & (JAC_F_UNFUSED_PACK)); mix(c->geom.bstride); mix(c->geom.ostride);
+    return h;
+}
+
+jac::SweepArgs sweep_args(const jac_ctx *c, int src, int mode)
+{
+    jac::SweepArgs a{};
+    a.g = c->geom;
+    a.blocks = c->dblocks;
+    a.arena = c->arena;
+    a.outbox = c->outbox;
+    a.src = src;
+    a.mode = mode;
+    a.ntx = c->ntx; a.nty = c->nty; a.ntz = c->ntz; a.zc = c->zc;
+    return a;
+}
+
+int sweep_mode(const jac_ctx *c)
+{
+    if (c->flags & JAC_F_SKIP_EXCHANGE) return jac::MODE_NOEXCHANGE;
+    if (c->flags & JAC_F_UNFUSED_PACK) return jac::MODE_PACK;
+    return jac::MODE_FUSED;
+}
+
+int enqueue_sweep(jac_ctx *c, int src)
+{
+    const jac::SweepArgs a = sweep_args(c, src, sweep_mode(c));
+    if (c->variant == 2) CK(jac::launch_sweep_plain(a, c->stream));
+    else CK(jac::launch_sweep_tma(c->tmap, a, c->variant, c->stream));
+    return JAC_OK;
+}
+
+int enqueue_barrier(jac_ctx *c)
+{
+    if (!c->has_remote()) return JAC_OK;
+    CK(jac::launch_barrier(c->bar, c->stream));
+    return JAC_OK;
+}
+
+// One Jacobi iteration reading buffer `src` (all kernels on c->stream).
+int enqueue_iteration(jac_ctx *c, int src, cudaEvent_t evs = nullptr, cudaEvent_t eve = nullptr)
+{
+    int rc;
+    if (evs) CK(cudaEventRecord(evs, c->stream));
+    if ((rc = enqueue_sweep(c, src))) return rc;
+    if (eve) CK(cudaEventRecord(eve, c->stream));
+    if ((rc = enqueue_barrier(c))) return rc;
+    if ((c->flags & JAC_F_UNFUSED_PACK) && !(c->flags & JAC_F_SKIP_EXCHANGE)) {
+        CK(jac::launch_ghost_fill(sweep_args(c, src, jac::MODE_PACK), 1 - src, c->stream));
+        if ((rc = enqueue_barrier(c))) return rc;
+    }
+    return JAC_OK;
+}
+
+int build_graph(jac_ctx *c, int src, int n, cudaGraphExec_t *out)
+{
+    cudaGraph_t g = nullptr;
+    CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    int rc = JAC_OK;
+    for (int u = 0; u < n && rc == JAC_OK; ++u) rc = enqueue_iteration(c, src ^ (u & 1));
+    cudaError_t e = cudaStreamEndCapture(c->stream, &g);
+    if (rc) { if (g) cudaGraphDestroy(g); return rc; }
+    if (e != cudaSuccess) return fail(JAC_ECUDA, "graph capture: %s", cudaGetErrorString(e));
+    e = cudaGraphInstantiate(out, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return fail(JAC_ECUDA, "graph instantiate: %s", cudaGetErrorString(e));
+    return JAC_OK;
+}
+
+int encode_tmap(jac_ctx *c)
+{
+    static PFN_encodeTiled encode = nullptr;
+    if (!encode) {
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+        if (!fn || q != cudaDriverEntryPointSuccess)
+            return fail(JAC_ECUDA, "cuTensorMapEncodeTiled unavailable");
+        encode = (PFN_encodeTiled)fn;
+    }
+    const jac::Geom &g = c->geom;
+    const jac::TileShape ts = jac::tma_tile_shape(c->variant);
+    const cuuint64_t dims[4] = {(cuuint64_t)g.P, (cuuint64_t)(g.ey + 2), (cuuint64_t)(g.ez + 2),
+                                (cuuint64_t)(2 * c->nslots)};
+    const cuuint64_t strides[3] = {(cuuint64_t)g.P * 8, (cuuint64_t)g.Q * 8, (cuuint64_t)g.bstride * 8};
+    const cuuint32_t box[4] = {(cuuint32_t)(ts.bx + 4), (cuuint32_t)(ts.by + 2), 1, 1};
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = encode(&c->tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, c->arena, dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(JAC_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return JAC_OK;
+}
+
+// Pointer of block (global coords nb) in buffer `buf` as seen from this context.
+double *block_ptr_local(const jac_ctx *c, const int32_t nb[3], int buf)
+{
+    const jac::Plan &p = c->plan;
+    const int32_t part = p.owner(nb[0], nb[1], nb[2]);
+    const int32_t ls = p.local_slot(nb[0], nb[1], nb[2]);
+    for (size_t h = 0; h < c->parts.size(); ++h)
+        if (c->parts[h] == part) return c->slot_ptr(buf, (int)h * p.blocks_per_part() + ls);
+    return nullptr;
+}
+
+int create_common(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, int32_t bz,
+                  int32_t n_gpus, const int32_t *gpu_grid, bool rank_mode, int32_t rank,
+                  int32_t device, uint32_t flags, jac_ctx **out)
+{
+    if (!out) return fail(JAC_EINVAL, "out is NULL");
+    *out = nullptr;
+    jac::Plan plan;
+    std::string err;
+    int rc = jac::make_plan(nx, ny, nz, bx, by, bz, n_gpus, gpu_grid, &plan, &err);
+    if (rc) return fail(rc, "%s", err.c_str());
+    if (flags & JAC_F_NCCL) return fail(JAC_EINVAL, "flags: JAC_F_NCCL transport is not built in this version");
+    if (rank_mode) {
+        if (rank < 0 || rank >= n_gpus) return fail(JAC_EINVAL, "rank %d out of [0,%d)", rank, n_gpus);
+        if (flags & JAC_F_VIRTUAL_GPUS) return fail(JAC_EINVAL, "flags: JAC_F_VIRTUAL_GPUS is not valid for rank contexts");
+    } else if (n_gpus > 1 && !(flags & JAC_F_VIRTUAL_GPUS)) {
+        return fail(JAC_EINVAL, "n_gpus > 1 in one process needs JAC_F_VIRTUAL_GPUS; use jac_create_rank (one process per GPU)");
+    }
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev < 1) return fail(JAC_EDEVICE, "no CUDA device (%s)", cudaGetErrorString(e));
+    if (device < 0 || device >= ndev) return fail(JAC_EDEVICE, "device %d not present (%d devices)", device, ndev);
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10) return fail(JAC_EDEVICE, "device %d is sm_%d%d, this library is built for sm_100a", device, prop.major, prop.minor);
+    CK(cudaSetDevice(device));
+
+    jac_ctx *c = new jac_ctx();
+    c->plan = plan;
+    c->flags = flags;
+    c->rank_mode = rank_mode;
+    c->rank = rank;
+    c->device = device;
+    if (rank_mode) c->parts = {rank};
+    else for (int32_t g = 0; g < n_gpus; ++g) c->parts.push_back(g);
+    const int32_t bpp = plan.blocks_per_part();
+    c->nslots = (int32_t)c->parts.size() * bpp;
+
+    // geometry (device.hpp layout)
+    jac::Geom &g = c->geom;
+    g.ex = (int32_t)plan.e[0]; g.ey = (int32_t)plan.e[1]; g.ez = (int32_t)plan.e[2];
+    g.A = jac::kA;
+    g.P = round_up(g.A + g.ex + 2, 4);
+    g.Q = g.P * (g.ey + 2);
+    g.bstride = round_up(g.Q * (g.ez + 2), 32);
+    g.nslots = c->nslots;
+    const int64_t fx = (int64_t)g.ey * g.ez, fy = (int64_t)g.ex * g.ez, fz = (int64_t)g.ex * g.ey;
+    int64_t o = 0;
+    const int64_t fsz[6] = {fx, fx, fy, fy, fz, fz};
+    for (int f = 0; f < 6; ++f) { g.ooff[f] = o; o += round_up(fsz[f], 4); }
+    g.ostride = (flags & JAC_F_UNFUSED_PACK) ? round_up(o, 32) : 0;
+
+    // tile shape / variant
+    if (flags & JAC_F_NO_TMA) c->variant = 2;
+    else c->variant = (g.ex <= 32) ? jac::TMA_NARROW : jac::TMA_WIDE;
+    const int tbx = (c->variant == 2) ? 64 : jac::tma_tile_shape(c->variant).bx;
+    const int tby = (c->variant == 2) ? 8 : jac::tma_tile_shape(c->variant).by;
+    c->ntx = (g.ex + tbx - 1) / tbx;
+    c->nty = (g.ey + tby - 1) / tby;
+    // z-chunk: enough CTAs for several waves on 148 SMs, chunks of >= 16 planes
+    int zc = g.ez;
+    const int64_t target = 148 * 4 * 4;
+    while ((int64_t)c->nslots * c->ntx * c->nty * ((g.ez + zc - 1) / zc) < target && zc > 16) zc = (zc + 1) / 2;
+    if (const char *s = getenv("JAC_ZC")) zc = std::max(1, std::min(g.ez, atoi(s)));
+    c->zc = zc;
+    c->ntz = (g.ez + zc - 1) / zc;
+    if (const char *s = getenv("JAC_UNROLL")) c->unroll = std::max(2, atoi(s) & ~1);
+    if ((int64_t)c->nslots * c->ntx * c->nty * c->ntz > 0x7fffffffLL) {
+        delete c;
+        return fail(JAC_EINVAL, "too many tiles for one launch");
+    }
+
+    // allocation: [ctrl 64 KiB][arena][outbox]
+    c->ctrl_off = 0;
+    c->arena_off = 65536;
+    const size_t arena_bytes = (size_t)2 * c->nslots * g.bstride * sizeof(double);
+    c->outbox_off = c->arena_off + arena_bytes;
+    const size_t outbox_bytes = (size_t)c->nslots * g.ostride * sizeof(double);
+    c->alloc_bytes = c->outbox_off + outbox_bytes;
+    e = cudaMalloc(&c->alloc, c->alloc_bytes);
+    if (e != cudaSuccess) {
+        delete c;
+        return fail(JAC_ENOMEM, "cudaMalloc(%zu bytes) for the block arena: %s", c->alloc_bytes, cudaGetErrorString(e));
+    }
+    c->ctrl = reinterpret_cast<uint64_t *>(c->alloc + c->ctrl_off);
+    c->arena = reinterpret_cast<double *>(c->alloc + c->arena_off);
+    c->outbox = outbox_bytes ? reinterpret_cast<double *>(c->alloc + c->outbox_off) : nullptr;
+    auto bail = [&](int code) { jac_destroy(c); return code; };
+    if (cudaMemset(c->alloc, 0, c->alloc_bytes) != cudaSuccess) return bail(fail(JAC_ECUDA, "cudaMemset arena"));
+
+    // descriptor table
+    c->hblocks.resize(c->nslots);
+    for (int32_t s = 0; s < c->nslots; ++s) {
+        const int32_t part = c->parts[s / bpp], ls = s % bpp;
+        int32_t blk[3];
+        plan.block_of(part, ls, blk);
+        jac::DevBlock &d = c->hblocks[s];
+        memset(&d, 0, sizeof d);
+        d.slot = s;
+        for (int k = 0; k < 3; ++k) d.org[k] = (int32_t)(blk[k] * plan.e[k]);
+        for (int f = 0; f < 6; ++f) {
+            int32_t nb[3];
+            if (!plan.neighbor(blk, f, nb)) continue;
+            const int32_t owner = plan.owner(nb[0], nb[1], nb[2]);
+            const bool local = std::find(c->parts.begin(), c->parts.end(), owner) != c->parts.end();
+            const bool same_part = owner == part;
+            if (same_part) c->local_faces++;
+            else c->remote_faces++;
+            if (!same_part) c->remote_bytes += 8 * ((f >> 1) == 0 ? fx : (f >> 1) == 1 ? fy : fz);
+            if (local) {
+                d.nb[f][0] = block_ptr_local(c, nb, 0);
+                d.nb[f][1] = block_ptr_local(c, nb, 1);
+                if (c->outbox) {
+                    int32_t h = (int32_t)(std::find(c->parts.begin(), c->parts.end(), owner) - c->parts.begin());
+                    const int32_t ns = h * bpp + plan.local_slot(nb[0], nb[1], nb[2]);
+                    d.nb_out[f] = c->outbox + (int64_t)ns * g.ostride + g.ooff[jac::opposite(f)];
+                }
+            } else if (std::find(c->peer_ranks.begin(), c->peer_ranks.end(), owner) == c->peer_ranks.end()) {
+                c->peer_ranks.push_back(owner);  // pointers filled by jac_import_ipc
+            }
+        }
+    }
+    if (c->peer_ranks.size() > 6) return bail(fail(JAC_EINVAL, "more than 6 neighbour ranks"));
+    if (cudaMalloc(&c->dblocks, sizeof(jac::DevBlock) * c->nslots) != cudaSuccess)
+        return bail(fail(JAC_ENOMEM, "cudaMalloc descriptor table"));
+    if (cudaMemcpy(c->dblocks, c->hblocks.data(), sizeof(jac::DevBlock) * c->nslots, cudaMemcpyHostToDevice) != cudaSuccess)
+        return bail(fail(JAC_ECUDA, "descriptor table upload"));
+    if (c->variant != 2) {
+        if ((rc = encode_tmap(c))) return bail(rc);
+        if (jac::prepare_sweep_tma(c->variant) != cudaSuccess) return bail(fail(JAC_ECUDA, "sweep kernel attribute"));
+    }
+    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess)
+        return bail(fail(JAC_ECUDA, "stream/event creation"));
+    // barrier args (peer slots filled at import)
+    c->bar.ctrl = c->ctrl;
+    c->bar.npeers = (int32_t)c->peer_ranks.size();
+    for (int n = 0; n < c->bar.npeers; ++n) c->bar.peer_id[n] = c->peer_ranks[n];
+    c->ipc_done = !c->has_remote() && !rank_mode;
+    *out = c;
+    return JAC_OK;
+}
+
+int require_ready(const jac_ctx *c)
+{
+    if (!c) return fail(JAC_EINVAL, "ctx is NULL");
+    if (c->rank_mode && !c->ipc_done) return fail(JAC_ESTATE, "rank context: call jac_import_ipc before init/step");
+    return JAC_OK;
+}
+
+int local_slot_of(const jac_ctx *c, int32_t ix, int32_t iy, int32_t iz, int32_t *slot)
+{
+    const jac::Plan &p = c->plan;
+    if (ix < 0 || iy < 0 || iz < 0 || ix >= p.b[0] || iy >= p.b[1] || iz >= p.b[2])
+        return fail(JAC_EINVAL, "block index (%d,%d,%d) outside (%d,%d,%d)", ix, iy, iz, p.b[0], p.b[1], p.b[2]);
+    const int32_t part = p.owner(ix, iy, iz);
+    for (size_t h = 0; h < c->parts.size(); ++h)
+        if (c->parts[h] == part) {
+            *slot = (int32_t)h * p.blocks_per_part() + p.local_slot(ix, iy, iz);
+            return JAC_OK;
+        }
+    return fail(JAC_EINVAL, "block (%d,%d,%d) is owned by partition %d, not by this context", ix, iy, iz, part);
+}
+
+int finish_init(jac_ctx *c)
+{
+    int rc;
+    if ((rc = enqueue_barrier(c))) return rc;  // neighbours may write our ghosts only after this
+    CK(cudaStreamSynchronize(c->stream));
+    c->inited = true;
+    c->iters = 0;
+    return JAC_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int jac_version(void) { return 100; }
+
+const char *jac_last_error(void) { return g_err.c_str(); }
+
+int jac_plan(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, int32_t bz, int32_t n_gpus,
+             const int32_t *gpu_grid_in, int32_t *gpu_grid_out, int64_t *block_extent_out)
+{
+    jac::Plan p;
+    std::string err;
+    int rc = jac::make_plan(nx, ny, nz, bx, by, bz, n_gpus, gpu_grid_in, &p, &err);
+    if (rc) return fail(rc, "%s", err.c_str());
+    for (int d = 0; d < 3; ++d) {
+        if (gpu_grid_out) gpu_grid_out[d] = p.g[d];
+        if (block_extent_out) block_extent_out[d] = p.e[d];
+    }
+    return JAC_OK;
+}
+
+int jac_plan_face(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, int32_t bz,
+                  int32_t n_gpus, const int32_t *gpu_grid_in, int32_t ix, int32_t iy, int32_t iz,
+                  int32_t f, int32_t *kind, int32_t *owner)
+{
+    jac::Plan p;
+    std::string err;
+    int rc = jac::make_plan(nx, ny, nz, bx, by, bz, n_gpus, gpu_grid_in, &p, &err);
+    if (rc) return fail(rc, "%s", err.c_str());
+    if (!kind || !owner) return fail(JAC_EINVAL, "kind/owner is NULL");
+    if (f < 0 || f > 5) return fail(JAC_EINVAL, "face %d not in 0..5", f);
+    if (ix < 0 || iy < 0 || iz < 0 || ix >= p.b[0] || iy >= p.b[1] || iz >= p.b[2])
+        return fail(JAC_EINVAL, "block index out of range");
+    const int32_t blk[3] = {ix, iy, iz};
+    int32_t nb[3];
+    if (!p.neighbor(blk, f, nb)) { *kind = JAC_FACE_BOUNDARY; *owner = -1; return JAC_OK; }
+    *owner = p.owner(nb[0], nb[1], nb[2]);
+    *kind = (*owner == p.owner(ix, iy, iz)) ? JAC_FACE_LOCAL : JAC_FACE_REMOTE;
+    return JAC_OK;
+}
+
+int jac_create(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, int32_t bz, int32_t n_gpus,
+               const int32_t *gpu_grid, uint32_t flags, jac_ctx **out)
+{
+    try {
+        return create_common(nx, ny, nz, bx, by, bz, n_gpus, gpu_grid, false, 0, 0, flags, out);
+    } catch (...) { return fail(JAC_ENOMEM, "host allocation failed"); }
+}
+
+int jac_create_rank(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, int32_t bz,
+                    int32_t n_gpus, const int32_t *gpu_grid, int32_t rank, int32_t device,
+                    uint32_t flags, jac_ctx **out)
+{
+    try {
+        return create_common(nx, ny, nz, bx, by, bz, n_gpus, gpu_grid, true, rank, device, flags, out);
+    } catch (...) { return fail(JAC_ENOMEM, "host allocation failed"); }
+}
+
+size_t jac_ipc_handle_bytes(void) { return sizeof(IpcRecord); }
+
+int jac_export_ipc(jac_ctx *c, void *out)
+{
+    if (!c || !out) return fail(JAC_EINVAL, "ctx/out is NULL");
+    if (!c->rank_mode) return fail(JAC_ESTATE, "jac_export_ipc needs a rank context");
+    CK(cudaSetDevice(c->device));
+    IpcRecord r;
+    memset(&r, 0, sizeof r);
+    r.magic = kIpcMagic;
+    r.rank = c->rank;
+    r.fingerprint = fingerprint(c);
+    r.arena_off = c->arena_off;
+    r.outbox_off = c->outbox_off;
+    r.ctrl_off = c->ctrl_off;
+    CK(cudaIpcGetMemHandle(&r.handle, c->alloc));
+    memcpy(out, &r, sizeof r);
+    return JAC_OK;
+}
+
+int jac_import_ipc(jac_ctx *c, const void *all)
+{
+    if (!c || !all) return fail(JAC_EINVAL, "ctx/all is NULL");
+    if (!c->rank_mode) return fail(JAC_ESTATE, "jac_import_ipc needs a rank context");
+    if (c->ipc_done) return fail(JAC_ESTATE, "jac_import_ipc called twice");
+    CK(cudaSetDevice(c->device));
+    const IpcRecord *recs = static_cast<const IpcRecord *>(all);
+    const jac::Plan &p = c->plan;
+    const uint64_t fp = fingerprint(c);
+    std::vector<char *> base(p.n_gpus, nullptr);
+    for (int32_t q : c->peer_ranks) {
+        const IpcRecord &r = recs[q];
+        if (r.magic != kIpcMagic || r.rank != q) return fail(JAC_EINVAL, "all: record %d is not a jacobi3d IPC record of rank %d", q, q);
+        if (r.fingerprint != fp) return fail(JAC_EINVAL, "all: rank %d was created with a different decomposition/flags", q);
+        void *ptr = nullptr;
+        CK(cudaIpcOpenMemHandle(&ptr, r.handle, cudaIpcMemLazyEnablePeerAccess));
+        c->ipc_opened.push_back(ptr);
+        base[q] = static_cast<char *>(ptr);
+    }
+    const int32_t bpp = p.blocks_per_part();
+    const jac::Geom &g = c->geom;
+    for (int32_t s = 0; s < c->nslots; ++s) {
+        int32_t blk[3];
+        p.block_of(c->rank, s, blk);
+        for (int f = 0; f < 6; ++f) {
+            int32_t nb[3];
+            if (!p.neighbor(blk, f, nb)) continue;
+            const int32_t q = p.owner(nb[0], nb[1], nb[2]);
+            if (q == c->rank) continue;
+            const int32_t ns = p.local_slot(nb[0], nb[1], nb[2]);
+            double *arena = reinterpret_cast<double *>(base[q] + recs[q].arena_off);
+            c->hblocks[s].nb[f][0] = arena + (int64_t)ns * g.bstride;
+            c->hblocks[s].nb[f][1] = arena + (int64_t)(bpp + ns) * g.bstride;
+            if (c->outbox) {
+                const double *ob = reinterpret_cast<const double *>(base[q] + recs[q].outbox_off);
+                c->hblocks[s].nb_out[f] = ob + (int64_t)ns * g.ostride + g.ooff[jac::opposite(f)];
+            }
+        }
+    }
+    for (int n = 0; n < c->bar.npeers; ++n) {
+        const int32_t q = c->bar.peer_id[n];
+        uint64_t *pc = reinterpret_cast<uint64_t *>(base[q] + recs[q].ctrl_off);
+        c->bar.peer_slot[n] = pc + 1 + c->rank;
+    }
+    CK(cudaMemcpy(c->dblocks, c->hblocks.data(), sizeof(jac::DevBlock) * c->nslots, cudaMemcpyHostToDevice));
+    c->ipc_done = true;
+    return JAC_OK;
+}
+
+int jac_set_init(jac_ctx *c, const double *padded)
+{
+    int rc;
+    if ((rc = require_ready(c))) return rc;
+    if (!padded) return fail(JAC_EINVAL, "padded is NULL");
+    CK(cudaSetDevice(c->device));
+    const jac::Plan &p = c->plan;
+    const jac::Geom &g = c->geom;
+    if ((rc = enqueue_barrier(c))) return rc;  // neighbours finished writing our ghosts
+    for (int32_t s = 0; s < c->nslots; ++s) {
+        const jac::DevBlock &d = c->hblocks[s];
+        cudaMemcpy3DParms m{};
+        m.srcPtr = make_cudaPitchedPtr(const_cast<double *>(padded), (size_t)(p.n[0] + 2) * 8,
+                                       (size_t)(p.n[0] + 2), (size_t)(p.n[1] + 2));
+        m.srcPos = make_cudaPos((size_t)d.org[0] * 8, (size_t)d.org[1], (size_t)d.org[2]);
+        m.dstPtr = make_cudaPitchedPtr(c->slot_ptr(0, s), (size_t)g.P * 8, (size_t)g.P, (size_t)(g.ey + 2));
+        m.dstPos = make_cudaPos((size_t)(g.A - 1) * 8, 0, 0);
+        m.extent = make_cudaExtent((size_t)(g.ex + 2) * 8, (size_t)(g.ey + 2), (size_t)(g.ez + 2));
+        m.kind = cudaMemcpyHostToDevice;
+        CK(cudaMemcpy3DAsync(&m, c->stream));
+    }
+    CK(cudaMemcpyAsync(c->slot_ptr(1, 0), c->slot_ptr(0, 0), (size_t)c->nslots * g.bstride * 8,
+                       cudaMemcpyDeviceToDevice, c->stream));
+    return finish_init(c);
+}
+
+int jac_set_init_hash(jac_ctx *c, uint64_t seed)
+{
+    int rc;
+    if ((rc = require_ready(c))) return rc;
+    CK(cudaSetDevice(c->device));
+    if ((rc = enqueue_barrier(c))) return rc;
+    CK(jac::launch_hash_init(sweep_args(c, 0, 0), c->plan.n[0], c->plan.n[1], seed, c->stream));
+    return finish_init(c);
+}
+
+int jac_step(jac_ctx *c, int32_t n)
+{
+    int rc;
+    if ((rc = require_ready(c))) return rc;
+    if (n < 0) return fail(JAC_EINVAL, "n_iters = %d < 0", n);
+    if (!c->inited) return fail(JAC_ESTATE, "jac_step before jac_set_init / jac_set_init_hash");
+    CK(cudaSetDevice(c->device));
+    const bool graphs = !(c->flags & JAC_F_NO_GRAPH);
+    if (graphs && !c->g1[0]) {
+        for (int s = 0; s < 2; ++s) {
+            if ((rc = build_graph(c, s, 1, &c->g1[s]))) return rc;
+            if ((rc = build_graph(c, s, c->unroll, &c->gU[s]))) return rc;
+        }
+    }
+    const int kpi = c->kernels_per_iter();
+    CK(cudaEventRecord(c->ev0, c->stream));
+    int src = (int)(c->iters & 1);
+    int left = n;
+    if (graphs) {
+        while (left >= c->unroll) {
+            CK(cudaGraphLaunch(c->gU[src], c->stream));
+            c->graph_launches++;
+            left -= c->unroll;  // unroll is even: parity unchanged
+        }
+        while (left > 0) {
+            CK(cudaGraphLaunch(c->g1[src], c->stream));
+            c->graph_launches++;
+            src ^= 1;
+            --left;
+        }
+    } else {
+        for (; left > 0; --left, src ^= 1)
+            if ((rc = enqueue_iteration(c, src))) return rc;
+    }
+    CK(cudaEventRecord(c->ev1, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+    c->last_ms = ms;
+    c->iters += n;
+    c->kernel_launches += (int64_t)n * kpi;
+    return JAC_OK;
+}
+
+int jac_profile_sweep(jac_ctx *c, int32_t n, double *avg_ms)
+{
+    int rc;
+    if ((rc = require_ready(c))) return rc;
+    if (n < 1 || !avg_ms) return fail(JAC_EINVAL, "n_iters must be >= 1 and avg_sweep_ms non-NULL");
+    if (!c->inited) return fail(JAC_ESTATE, "jac_profile_sweep before init");
+    CK(cudaSetDevice(c->device));
+    std::vector<cudaEvent_t> ev(2 * (size_t)n);
+    for (auto &e : ev) CK(cudaEventCreate(&e));
+    int src = (int)(c->iters & 1);
+    for (int it = 0; it < n; ++it, src ^= 1)
+        if ((rc = enqueue_iteration(c, src, ev[2 * it], ev[2 * it + 1]))) return rc;
+    CK(cudaStreamSynchronize(c->stream));
+    double tot = 0;
+    for (int it = 0; it < n; ++it) {
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, ev[2 * it], ev[2 * it + 1]));
+        tot += ms;
+    }
+    for (auto &e : ev) cudaEventDestroy(e);
+    c->iters += n;
+    c->kernel_launches += (int64_t)n * c->kernels_per_iter();
+    *avg_ms = tot / n;
+    return JAC_OK;
+}
+
+int jac_get_block_padded(jac_ctx *c, int32_t ix, int32_t iy, int32_t iz, double *out)
+{
+    if (!c || !out) return fail(JAC_EINVAL, "ctx/out is NULL");
+    int32_t s;
+    int rc;
+    if ((rc = local_slot_of(c, ix, iy, iz, &s))) return rc;
+    CK(cudaSetDevice(c->device));
+    const jac::Geom &g = c->geom;
+    cudaMemcpy3DParms m{};
+    m.srcPtr = make_cudaPitchedPtr(c->slot_ptr((int)(c->iters & 1), s), (size_t)g.P * 8, (size_t)g.P, (size_t)(g.ey + 2));
+    m.srcPos = make_cudaPos((size_t)(g.A - 1) * 8, 0, 0);
+    m.dstPtr = make_cudaPitchedPtr(out, (size_t)(g.ex + 2) * 8, (size_t)(g.ex + 2), (size_t)(g.ey + 2));
+    m.extent = make_cudaExtent((size_t)(g.ex + 2) * 8, (size_t)(g.ey + 2), (size_t)(g.ez + 2));
+    m.kind = cudaMemcpyDeviceToHost;
+    CK(cudaMemcpy3DAsync(&m, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return JAC_OK;
+}
+
+int jac_get_block(jac_ctx *c, int32_t ix, int32_t iy, int32_t iz, double *out)
+{
+    if (!c || !out) return fail(JAC_EINVAL, "ctx/out is NULL");
+    int32_t s;
+    int rc;
+    if ((rc = local_slot_of(c, ix, iy, iz, &s))) return rc;
+    CK(cudaSetDevice(c->device));
+    const jac::Geom &g = c->geom;
+    cudaMemcpy3DParms m{};
+    m.srcPtr = make_cudaPitchedPtr(c->slot_ptr((int)(c->iters & 1), s), (size_t)g.P * 8, (size_t)g.P, (size_t)(g.ey + 2));
+    m.srcPos = make_cudaPos((size_t)g.A * 8, 1, 1);
+    m.dstPtr = make_cudaPitchedPtr(out, (size_t)g.ex * 8, (size_t)g.ex, (size_t)g.ey);
+    m.extent = make_cudaExtent((size_t)g.ex * 8, (size_t)g.ey, (size_t)g.ez);
+    m.kind = cudaMemcpyDeviceToHost;
+    CK(cudaMemcpy3DAsync(&m, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return JAC_OK;
+}
+
+int jac_get_field(jac_ctx *c, double *padded)
+{
+    if (!c || !padded) return fail(JAC_EINVAL, "ctx/padded is NULL");
+    CK(cudaSetDevice(c->device));
+    const jac::Plan &p = c->plan;
+    const jac::Geom &g = c->geom;
+    for (int32_t s = 0; s < c->nslots; ++s) {
+        const jac::DevBlock &d = c->hblocks[s];
+        cudaMemcpy3DParms m{};
+        m.srcPtr = make_cudaPitchedPtr(c->slot_ptr((int)(c->iters & 1), s), (size_t)g.P * 8, (size_t)g.P, (size_t)(g.ey + 2));
+        m.srcPos = make_cudaPos((size_t)g.A * 8, 1, 1);
+        m.dstPtr = make_cudaPitchedPtr(padded, (size_t)(p.n[0] + 2) * 8, (size_t)(p.n[0] + 2), (size_t)(p.n[1] + 2));
+        m.dstPos = make_cudaPos((size_t)(d.org[0] + 1) * 8, (size_t)(d.org[1] + 1), (size_t)(d.org[2] + 1));
+        m.extent = make_cudaExtent((size_t)g.ex * 8, (size_t)g.ey, (size_t)g.ez);
+        m.kind = cudaMemcpyDeviceToHost;
+        CK(cudaMemcpy3DAsync(&m, c->stream));
+    }
+    CK(cudaStreamSynchronize(c->stream));
+    return JAC_OK;
+}
+
+int jac_get_layout(const jac_ctx *c, int32_t *gpu_grid, int64_t *block_extent, int64_t *iterations_done)
+{
+    if (!c) return fail(JAC_EINVAL, "ctx is NULL");
+    for (int d = 0; d < 3; ++d) {
+        if (gpu_grid) gpu_grid[d] = c->plan.g[d];
+        if (block_extent) block_extent[d] = c->plan.e[d];
+    }
+    if (iterations_done) *iterations_done = c->iters;
+    return JAC_OK;
+}
+
+int jac_block_owner(const jac_ctx *c, int32_t ix, int32_t iy, int32_t iz, int32_t *gpu)
+{
+    if (!c || !gpu) return fail(JAC_EINVAL, "ctx/gpu is NULL");
+    const jac::Plan &p = c->plan;
+    if (ix < 0 || iy < 0 || iz < 0 || ix >= p.b[0] || iy >= p.b[1] || iz >= p.b[2])
+        return fail(JAC_EINVAL, "block index out of range");
+    *gpu = p.owner(ix, iy, iz);
+    return JAC_OK;
+}
+
+int jac_last_step_ms(const jac_ctx *c, double *ms)
+{
+    if (!c || !ms) return fail(JAC_EINVAL, "ctx/ms is NULL");
+    *ms = c->last_ms;
+    return JAC_OK;
+}
+
+int jac_get_stats(const jac_ctx *c, int64_t *st)
+{
+    if (!c || !st) return fail(JAC_EINVAL, "ctx/stats is NULL");
+    st[JAC_STAT_KERNEL_LAUNCHES] = c->kernel_launches;
+    st[JAC_STAT_GRAPH_LAUNCHES] = c->graph_launches;
+    st[JAC_STAT_KERNELS_PER_ITER] = c->kernels_per_iter();
+    st[JAC_STAT_LOCAL_BLOCKS] = c->nslots;
+    st[JAC_STAT_LOCAL_FACES] = c->local_faces;
+    st[JAC_STAT_REMOTE_FACES] = c->remote_faces;
+    st[JAC_STAT_REMOTE_BYTES] = c->remote_bytes;
+    st[JAC_STAT_ARENA_BYTES] = (int64_t)(2 * (size_t)c->nslots * c->geom.bstride * 8);
+    st[JAC_STAT_SWEEP_VARIANT] = c->variant == 2 ? 1 : 0;
+    return JAC_OK;
+}
+
+int jac_destroy(jac_ctx *c)
+{
+    if (!c) return JAC_OK;
+    cudaSetDevice(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    for (int s = 0; s < 2; ++s) {
+        if (c->g1[s]) cudaGraphExecDestroy(c->g1[s]);
+        if (c->gU[s]) cudaGraphExecDestroy(c->gU[s]);
+    }
+    for (void *p : c->ipc_opened) cudaIpcCloseMemHandle(p);
+    if (c->ev0) cudaEventDestroy(c->ev0);
+    if (c->ev1) cudaEventDestroy(c->ev1);
+    if (c->stream) cudaStreamDestroy(c->stream);
+    if (c->dblocks) cudaFree(c->dblocks);
+    if (c->alloc) cudaFree(c->alloc);
+    delete c;
+    return JAC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,310 @@
+"""Thin ctypes binding of libjacobi3d.so (include/jacobi3d.h) -- argument
+marshalling only.  Every step of the hot path runs in the library's sm_100a kernels;
+there is no Python or CPU fallback: if the shared library cannot be built or loaded
+the import of this module's functions raises.
+
+Function names mirror the C ABI (``jac_create``, ``jac_set_init``, ``jac_step``,
+``jac_get_block``, ``jac_destroy``, ...).  ``Jacobi3D`` is a small convenience
+wrapper around one context.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import build as _build
+
+JAC_OK, JAC_EINVAL, JAC_EDECOMP, JAC_EDEVICE, JAC_ENOMEM, JAC_ECUDA, JAC_ENCCL, JAC_ESTATE = (
+    0, -1, -2, -3, -4, -5, -6, -7)
+JAC_F_DEFAULT = 0
+JAC_F_FMA = 1 << 0
+JAC_F_NO_GRAPH = 1 << 1
+JAC_F_NCCL = 1 << 2
+JAC_F_UNFUSED_PACK = 1 << 4
+JAC_F_NO_TMA = 1 << 5
+JAC_F_VIRTUAL_GPUS = 1 << 6
+JAC_F_SKIP_EXCHANGE = 1 << 7
+JAC_FACE_BOUNDARY, JAC_FACE_LOCAL, JAC_FACE_REMOTE = 0, 1, 2
+STAT_NAMES = ["kernel_launches", "graph_launches", "kernels_per_iter", "local_blocks",
+              "local_faces", "remote_faces", "remote_bytes", "arena_bytes", "sweep_variant"]
+EXPORTED = ["jac_plan", "jac_plan_face", "jac_create", "jac_create_rank", "jac_ipc_handle_bytes",
+            "jac_export_ipc", "jac_import_ipc", "jac_set_init", "jac_set_init_hash", "jac_step",
+            "jac_get_block", "jac_get_block_padded", "jac_get_field", "jac_get_layout",
+            "jac_block_owner", "jac_last_step_ms", "jac_profile_sweep", "jac_get_stats",
+            "jac_destroy", "jac_last_error", "jac_version"]
+
+_ERRNAMES = {-1: "JAC_EINVAL", -2: "JAC_EDECOMP", -3: "JAC_EDEVICE", -4: "JAC_ENOMEM",
+             -5: "JAC_ECUDA", -6: "JAC_ENCCL", -7: "JAC_ESTATE"}
+
+
+class JacError(RuntimeError):
+    def __init__(self, code: int, fn: str, msg: str):
+        super().__init__(f"{fn}: {_ERRNAMES.get(code, code)}: {msg}")
+        self.code = code
+
+
+_lib: Optional[ctypes.CDLL] = None
+
+
+def lib_path() -> str:
+    return _build.LIB
+
+
+def load() -> ctypes.CDLL:
+    """Loads (building first if missing or stale) the in-tree libjacobi3d.so."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    path = _build.build()
+    if not os.path.exists(path):
+        raise ImportError(f"libjacobi3d.so missing at {path}; run __graft_entry__.build()")
+    L = ctypes.CDLL(path)
+    i64, i32, u32, u64 = ctypes.c_int64, ctypes.c_int32, ctypes.c_uint32, ctypes.c_uint64
+    P = ctypes.POINTER
+    vp, dp = ctypes.c_void_p, P(ctypes.c_double)
+    sig = {
+        "jac_plan": [i64, i64, i64, i32, i32, i32, i32, P(i32), P(i32), P(i64)],
+        "jac_plan_face": [i64, i64, i64, i32, i32, i32, i32, P(i32), i32, i32, i32, i32, P(i32), P(i32)],
+        "jac_create": [i64, i64, i64, i32, i32, i32, i32, P(i32), u32, P(vp)],
+        "jac_create_rank": [i64, i64, i64, i32, i32, i32, i32, P(i32), i32, i32, u32, P(vp)],
+        "jac_export_ipc": [vp, vp],
+        "jac_import_ipc": [vp, vp],
+        "jac_set_init": [vp, dp],
+        "jac_set_init_hash": [vp, u64],
+        "jac_step": [vp, i32],
+        "jac_get_block": [vp, i32, i32, i32, dp],
+        "jac_get_block_padded": [vp, i32, i32, i32, dp],
+        "jac_get_field": [vp, dp],
+        "jac_get_layout": [vp, P(i32), P(i64), P(i64)],
+        "jac_block_owner": [vp, i32, i32, i32, P(i32)],
+        "jac_last_step_ms": [vp, P(ctypes.c_double)],
+        "jac_profile_sweep": [vp, i32, P(ctypes.c_double)],
+        "jac_get_stats": [vp, P(i64)],
+        "jac_destroy": [vp],
+    }
+    for name, args in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = ctypes.c_int
+    L.jac_ipc_handle_bytes.argtypes = []
+    L.jac_ipc_handle_bytes.restype = ctypes.c_size_t
+    L.jac_last_error.argtypes = []
+    L.jac_last_error.restype = ctypes.c_char_p
+    L.jac_version.argtypes = []
+    L.jac_version.restype = ctypes.c_int
+    _lib = L
+    return L
+
+
+def _check(rc: int, fn: str) -> None:
+    if rc != JAC_OK:
+        raise JacError(rc, fn, (load().jac_last_error() or b"").decode())
+
+
+def _grid(g: Optional[Sequence[int]]):
+    if g is None:
+        return None
+    return (ctypes.c_int32 * 3)(*[int(v) for v in g])
+
+
+def _dptr(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+# ------------------------------------------------------------------ C-ABI mirrors
+def jac_plan(nx, ny, nz, bx, by, bz, n_gpus, gpu_grid=None):
+    g = (ctypes.c_int32 * 3)()
+    e = (ctypes.c_int64 * 3)()
+    _check(load().jac_plan(nx, ny, nz, bx, by, bz, n_gpus, _grid(gpu_grid), g, e), "jac_plan")
+    return tuple(g), tuple(e)
+
+
+def jac_plan_face(nx, ny, nz, bx, by, bz, n_gpus, gpu_grid, ix, iy, iz, f):
+    kind, owner = ctypes.c_int32(), ctypes.c_int32()
+    _check(load().jac_plan_face(nx, ny, nz, bx, by, bz, n_gpus, _grid(gpu_grid), ix, iy, iz, f,
+                                ctypes.byref(kind), ctypes.byref(owner)), "jac_plan_face")
+    return kind.value, owner.value
+
+
+def jac_create(nx, ny, nz, bx, by, bz, n_gpus=1, gpu_grid=None, flags=0) -> int:
+    out = ctypes.c_void_p()
+    _check(load().jac_create(nx, ny, nz, bx, by, bz, n_gpus, _grid(gpu_grid), flags,
+                             ctypes.byref(out)), "jac_create")
+    return out.value
+
+
+def jac_create_rank(nx, ny, nz, bx, by, bz, n_gpus, gpu_grid, rank, device, flags=0) -> int:
+    out = ctypes.c_void_p()
+    _check(load().jac_create_rank(nx, ny, nz, bx, by, bz, n_gpus, _grid(gpu_grid), rank, device,
+                                  flags, ctypes.byref(out)), "jac_create_rank")
+    return out.value
+
+
+def jac_ipc_handle_bytes() -> int:
+    return int(load().jac_ipc_handle_bytes())
+
+
+def jac_export_ipc(ctx) -> bytes:
+    buf = ctypes.create_string_buffer(jac_ipc_handle_bytes())
+    _check(load().jac_export_ipc(ctx, buf), "jac_export_ipc")
+    return buf.raw
+
+
+def jac_import_ipc(ctx, records: Sequence[bytes]) -> None:
+    blob = b"".join(records)
+    buf = ctypes.create_string_buffer(blob, len(blob))
+    _check(load().jac_import_ipc(ctx, buf), "jac_import_ipc")
+
+
+def jac_set_init(ctx, padded: np.ndarray) -> None:
+    if padded.dtype != np.float64 or not padded.flags.c_contiguous:
+        raise ValueError("padded must be C-contiguous float64")
+    _check(load().jac_set_init(ctx, _dptr(padded)), "jac_set_init")
+
+
+def jac_set_init_hash(ctx, seed: int) -> None:
+    _check(load().jac_set_init_hash(ctx, seed), "jac_set_init_hash")
+
+
+def jac_step(ctx, n_iters: int) -> None:
+    _check(load().jac_step(ctx, n_iters), "jac_step")
+
+
+def jac_get_block(ctx, ix, iy, iz, out: np.ndarray) -> np.ndarray:
+    _check(load().jac_get_block(ctx, ix, iy, iz, _dptr(out)), "jac_get_block")
+    return out
+
+
+def jac_get_block_padded(ctx, ix, iy, iz, out: np.ndarray) -> np.ndarray:
+    _check(load().jac_get_block_padded(ctx, ix, iy, iz, _dptr(out)), "jac_get_block_padded")
+    return out
+
+
+def jac_get_field(ctx, padded: np.ndarray) -> np.ndarray:
+    _check(load().jac_get_field(ctx, _dptr(padded)), "jac_get_field")
+    return padded
+
+
+def jac_get_layout(ctx):
+    g = (ctypes.c_int32 * 3)()
+    e = (ctypes.c_int64 * 3)()
+    it = ctypes.c_int64()
+    _check(load().jac_get_layout(ctx, g, e, ctypes.byref(it)), "jac_get_layout")
+    return tuple(g), tuple(e), it.value
+
+
+def jac_block_owner(ctx, ix, iy, iz) -> int:
+    g = ctypes.c_int32()
+    _check(load().jac_block_owner(ctx, ix, iy, iz, ctypes.byref(g)), "jac_block_owner")
+    return g.value
+
+
+def jac_last_step_ms(ctx) -> float:
+    v = ctypes.c_double()
+    _check(load().jac_last_step_ms(ctx, ctypes.byref(v)), "jac_last_step_ms")
+    return v.value
+
+
+def jac_profile_sweep(ctx, n_iters: int) -> float:
+    v = ctypes.c_double()
+    _check(load().jac_profile_sweep(ctx, n_iters, ctypes.byref(v)), "jac_profile_sweep")
+    return v.value
+
+
+def jac_get_stats(ctx) -> dict:
+    st = (ctypes.c_int64 * len(STAT_NAMES))()
+    _check(load().jac_get_stats(ctx, st), "jac_get_stats")
+    return dict(zip(STAT_NAMES, list(st)))
+
+
+def jac_destroy(ctx) -> None:
+    _check(load().jac_destroy(ctx), "jac_destroy")
+
+
+def jac_last_error() -> str:
+    return (load().jac_last_error() or b"").decode()
+
+
+def jac_version() -> int:
+    return int(load().jac_version())
+
+
+# ------------------------------------------------------------------ convenience
+class Jacobi3D:
+    """One context.  ``dims`` = (nx, ny, nz) interior points, ``blocks`` = (bx, by, bz)
+    global blocks per dim.  ``rank``/``device`` select a rank context (one process
+    per GPU; see ``paper_2605_12734_b200.dist``)."""
+
+    def __init__(self, dims, blocks, n_gpus=1, gpu_grid=None, flags=0, rank=None, device=0):
+        self.dims = tuple(int(v) for v in dims)
+        self.blocks = tuple(int(v) for v in blocks)
+        self.n_gpus = int(n_gpus)
+        if rank is None:
+            self.ctx = jac_create(*self.dims, *self.blocks, self.n_gpus, gpu_grid, flags)
+        else:
+            self.ctx = jac_create_rank(*self.dims, *self.blocks, self.n_gpus, gpu_grid, rank, device, flags)
+        self.rank = rank
+        self.gpu_grid, self.block_extent, _ = jac_get_layout(self.ctx)
+
+    @property
+    def odf(self) -> int:
+        return self.blocks[0] * self.blocks[1] * self.blocks[2] // self.n_gpus
+
+    def set_init(self, padded: np.ndarray) -> None:
+        jac_set_init(self.ctx, padded)
+
+    def set_init_hash(self, seed: int) -> None:
+        jac_set_init_hash(self.ctx, seed)
+
+    def step(self, n: int) -> None:
+        jac_step(self.ctx, n)
+
+    def block(self, ix, iy, iz) -> np.ndarray:
+        ex, ey, ez = self.block_extent
+        return jac_get_block(self.ctx, ix, iy, iz, np.empty((ez, ey, ex), dtype=np.float64))
+
+    def block_padded(self, ix, iy, iz) -> np.ndarray:
+        ex, ey, ez = self.block_extent
+        return jac_get_block_padded(self.ctx, ix, iy, iz, np.empty((ez + 2, ey + 2, ex + 2), dtype=np.float64))
+
+    def field(self, like: np.ndarray) -> np.ndarray:
+        """Padded array: shell/non-local cells copied from ``like``, local interiors
+        from the device."""
+        out = np.array(like, dtype=np.float64, copy=True)
+        return jac_get_field(self.ctx, out)
+
+    @property
+    def iterations(self) -> int:
+        return jac_get_layout(self.ctx)[2]
+
+    def last_step_ms(self) -> float:
+        return jac_last_step_ms(self.ctx)
+
+    def profile_sweep(self, n: int) -> float:
+        return jac_profile_sweep(self.ctx, n)
+
+    def stats(self) -> dict:
+        return jac_get_stats(self.ctx)
+
+    def owner(self, ix, iy, iz) -> int:
+        return jac_block_owner(self.ctx, ix, iy, iz)
+
+    def close(self) -> None:
+        if self.ctx:
+            jac_destroy(self.ctx)
+            self.ctx = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,201 @@
+"""GPU parity: the CUDA path through the C ABI against the CPU oracle, element by
+element, bit-exact (north star: "GPU results must be bit-exact to the oracle ...
+the same across all ODFs"; the result is unique to the bit).
+
+All inputs come from jac_inputs (seeded, synthetic, shaped like the paper's
+Jacobi runs: uniform dense grid, fixed iteration count).
+"""
+from __future__ import annotations
+
+import os
+
+import numpy as np
+import pytest
+
+import jac_inputs as JI
+import oracle
+import paper_2605_12734_b200 as jb
+from paper_2605_12734_b200 import jacobi3d as J
+
+pytestmark = pytest.mark.gpu
+
+F = J
+
+
+def ref(u0, n):
+    out, _ = oracle.jacobi3d_omp(u0, n)
+    return out
+
+
+def run(u0, blocks, n, flags=0, n_gpus=1, steps=None):
+    nz2, ny2, nx2 = u0.shape
+    with jb.Jacobi3D((nx2 - 2, ny2 - 2, nz2 - 2), blocks, n_gpus=n_gpus, flags=flags) as s:
+        s.set_init(u0)
+        for k in (steps or [n]):
+            s.step(k)
+        assert s.iterations == n
+        return s.field(u0)
+
+
+def assert_bits(a, b):
+    assert a.shape == b.shape
+    bad = np.flatnonzero(a.view(np.uint64) != b.view(np.uint64))
+    assert bad.size == 0, f"{bad.size} mismatches, first at {np.unravel_index(bad[0], a.shape)}: {a.flat[bad[0]]!r} vs {b.flat[bad[0]]!r}"
+
+
+def test_native_library_loaded():
+    jb.load()
+    maps = open("/proc/self/maps").read()
+    assert J.lib_path() in maps
+
+
+def test_c1_config_bit_exact_and_regression_constants():
+    """BASELINE.json configs[0]: 64^3, 2x2x2 blocks (ODF 8), 1 GPU, 10 iterations."""
+    u0 = JI.hash_field(64, 64, 64, seed=1)
+    got = run(u0, (2, 2, 2), 10)
+    assert_bits(got, ref(u0, 10))
+    assert oracle.bithash(got) == 0x77818AA80EA02999  # tests/golden/c1_regression.txt
+
+
+def test_device_hash_init_matches_generator():
+    nx, ny, nz = 40, 24, 16
+    u0 = JI.hash_field(nx, ny, nz, seed=3)
+    with jb.Jacobi3D((nx, ny, nz), (2, 1, 2)) as s:
+        s.set_init_hash(3)
+        for iz in range(2):
+            for ix in range(2):
+                ex, ey, ez = s.block_extent
+                blk = s.block_padded(ix, 0, iz)
+                want = u0[iz * ez:iz * ez + ez + 2, 0:ey + 2, ix * ex:ix * ex + ex + 2]
+                assert_bits(blk, want)
+        s.step(4)
+        assert_bits(s.field(u0), ref(u0, 4))
+
+
+@pytest.mark.parametrize("blocks", [(1, 1, 1), (1, 1, 2), (1, 2, 2), (2, 2, 2), (2, 2, 4),
+                                    (2, 4, 4), (4, 4, 4), (4, 8, 8)])
+def test_odf_sweep_128(blocks):
+    """ODF 1..256 at 128^3 (the C2 sweep's shapes, scaled down) all equal the oracle."""
+    u0 = JI.hash_field(128, 128, 128, seed=2)
+    want = ref(u0, 7)
+    assert_bits(run(u0, blocks, 7), want)
+
+
+@pytest.mark.parametrize("dims,blocks", [
+    ((70, 37, 23), (2, 1, 1)),    # odd x extent 35, ragged tiles in x and y
+    ((70, 37, 23), (5, 1, 1)),    # ex = 14: narrow tile variant
+    ((33, 5, 9), (1, 1, 3)),      # odd everything, ez = 3
+    ((130, 18, 6), (2, 2, 6)),    # ez = 1: every plane is a z-face
+    ((1, 1, 1), (1, 1, 1)),
+    ((2, 3, 4), (2, 3, 4)),       # 1^3 blocks: every point is a face point of 6 faces
+    ((96, 66, 40), (3, 3, 5)),    # ex = 32 boundary of the narrow variant
+])
+def test_ragged_and_degenerate(dims, blocks):
+    u0 = JI.hash_field(*dims, seed=1)
+    assert_bits(run(u0, blocks, 5), ref(u0, 5))
+
+
+@pytest.mark.parametrize("flags", [J.JAC_F_NO_TMA, J.JAC_F_UNFUSED_PACK, J.JAC_F_NO_GRAPH,
+                                   J.JAC_F_UNFUSED_PACK | J.JAC_F_NO_TMA, J.JAC_F_FMA])
+@pytest.mark.parametrize("dims,blocks", [((64, 48, 40), (2, 3, 2)), ((37, 21, 19), (1, 1, 1))])
+def test_variants_bit_exact(flags, dims, blocks):
+    u0 = JI.hash_field(*dims, seed=2)
+    assert_bits(run(u0, blocks, 6, flags=flags), ref(u0, 6))
+
+
+@pytest.mark.parametrize("n_gpus,blocks", [(2, (2, 2, 2)), (4, (2, 2, 4)), (8, (4, 4, 4)), (8, (2, 2, 2))])
+def test_virtual_partitions(n_gpus, blocks):
+    """Partition/REMOTE-face logic with all partitions on one device, one kernel."""
+    u0 = JI.hash_field(64, 64, 64, seed=1)
+    assert_bits(run(u0, blocks, 9, n_gpus=n_gpus, flags=J.JAC_F_VIRTUAL_GPUS), ref(u0, 9))
+
+
+def test_step_accumulation_and_graph_unroll_boundaries():
+    u0 = JI.hash_field(48, 40, 36, seed=3)
+    want = ref(u0, 23)
+    assert_bits(run(u0, (2, 2, 2), 23, steps=[0, 3, 10, 1, 9]), want)
+    assert_bits(run(u0, (2, 2, 2), 23, steps=[23]), want)
+    assert_bits(run(u0, (1, 1, 1), 0, steps=[0]), u0)
+
+
+def test_restart_from_field_equals_continuous_run():
+    """P9: step(5), get the field, set_init (same shell), step(6) == step(11)."""
+    u0 = JI.hash_field(40, 40, 40, seed=2)
+    with jb.Jacobi3D((40, 40, 40), (2, 2, 2)) as s:
+        s.set_init(u0)
+        s.step(5)
+        mid = s.field(u0)
+        s.set_init(mid)
+        s.step(6)
+        assert_bits(s.field(u0), ref(u0, 11))
+
+
+def test_structured_fields_on_gpu():
+    """P1 constant and P2 linear fields stay bit-identical on the GPU too."""
+    for u0 in (JI.constant_field(30, 20, 10, 3.25), JI.linear_field(30, 20, 10)):
+        assert_bits(run(u0, (3, 2, 2), 8), u0)
+
+
+def test_ghost_conservation_p11():
+    """After the exchange, every LOCAL ghost face equals the neighbour's boundary layer."""
+    dims, blocks = (32, 24, 16), (2, 2, 2)
+    u0 = JI.hash_field(*dims, seed=1)
+    with jb.Jacobi3D(dims, blocks) as s:
+        s.set_init(u0)
+        s.step(3)
+        ex, ey, ez = s.block_extent
+        pads = {(x, y, z): s.block_padded(x, y, z) for x in range(2) for y in range(2) for z in range(2)}
+        for (x, y, z), b in pads.items():
+            if x == 0:
+                assert_bits(b[1:-1, 1:-1, ex + 1], pads[(1, y, z)][1:-1, 1:-1, 1])
+            if y == 0:
+                assert_bits(b[1:-1, ey + 1, 1:-1], pads[(x, 1, z)][1:-1, 1, 1:-1])
+            if z == 0:
+                assert_bits(b[ez + 1, 1:-1, 1:-1], pads[(x, y, 1)][1, 1:-1, 1:-1])
+
+
+def test_skip_exchange_is_wrong_and_flagged():
+    """JAC_F_SKIP_EXCHANGE is timing-only: with ODF > 1 it must NOT match."""
+    u0 = JI.hash_field(32, 32, 32, seed=1)
+    got = run(u0, (2, 1, 1), 4, flags=J.JAC_F_SKIP_EXCHANGE)
+    assert not np.array_equal(got, ref(u0, 4))
+
+
+def test_c5_fine_grain_scaled():
+    """C5's shape (32^3 blocks, 8 partitions) at 256^3: 512 blocks, 64 per partition."""
+    u0 = JI.hash_field(256, 256, 256, seed=1)
+    want = ref(u0, 12)
+    assert_bits(run(u0, (8, 8, 8), 12, n_gpus=8, flags=J.JAC_F_VIRTUAL_GPUS), want)
+
+
+def _lightcone_check(got, u0, n, corners, s=8):
+    nz, ny, nx = (d - 2 for d in u0.shape)
+    for (x0, y0, z0) in corners:
+        lo = [max(0, c - n) for c in (z0, y0, x0)]
+        hi = [min(N, c + s + n) for c, N in ((z0, nz), (y0, ny), (x0, nx))]
+        sub = np.ascontiguousarray(u0[lo[0]:hi[0] + 2, lo[1]:hi[1] + 2, lo[2]:hi[2] + 2])
+        res = ref(sub, n)
+        a = res[z0 - lo[0] + 1:z0 - lo[0] + 1 + s, y0 - lo[1] + 1:y0 - lo[1] + 1 + s,
+                x0 - lo[2] + 1:x0 - lo[2] + 1 + s]
+        assert_bits(got[z0 + 1:z0 + 1 + s, y0 + 1:y0 + 1 + s, x0 + 1:x0 + 1 + s], a)
+
+
+def test_c2_full_size_bench_config():
+    """BASELINE.json configs[1] at full size in the bench's launch configuration
+    (512^3, device hash init, 100 iterations): bit-hash identical across ODF 1, 8, 64,
+    and light-cone sub-cubes at block seams / corners / centre equal the oracle."""
+    nx = 512
+    n = 100
+    u0 = JI.hash_field(nx, nx, nx, seed=1)
+    hashes = []
+    got = None
+    for blocks in [(2, 2, 2), (1, 1, 1), (4, 4, 4)]:
+        with jb.Jacobi3D((nx, nx, nx), blocks) as s:
+            s.set_init_hash(1)
+            s.step(n)
+            f = s.field(u0)
+        hashes.append(oracle.bithash(f))
+        if got is None:
+            got = f
+    assert len(set(hashes)) == 1
+    _lightcone_check(got, u0, n, [(0, 0, 0), (252, 252, 252), (504, 100, 255), (127, 383, 504)])
