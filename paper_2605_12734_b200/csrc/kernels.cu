@@ -141,19 +141,37 @@ __device__ __forceinline__ void mbar_fence_init()
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
 
+// Watchdog: a wait that cannot complete (a TMA that never lands, a peer rank that
+// never signals) traps after ~kSpinLimitNs instead of hanging the GPU.
+constexpr uint64_t kSpinLimitNs = 20ull * 1000 * 1000 * 1000;
+
+__device__ __forceinline__ uint64_t globaltimer_ns()
+{
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+__device__ __forceinline__ bool mbar_try(uint32_t b, uint32_t parity)
+{
+    uint32_t done;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(b), "r"(parity)
+        : "memory");
+    return done != 0;
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
 {
     const uint32_t b = smem_u32(bar);
-    uint32_t done;
-    do {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-            "selp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(done)
-            : "r"(b), "r"(parity)
-            : "memory");
-    } while (!done);
+    if (mbar_try(b, parity)) return;
+    const uint64_t t0 = globaltimer_ns();
+    while (!mbar_try(b, parity))
+        if (globaltimer_ns() - t0 > kSpinLimitNs) __trap();
 }
 
 __device__ __forceinline__ void tma_plane(const CUtensorMap *tm, double *dst, uint64_t *bar,
@@ -170,6 +188,11 @@ __device__ __forceinline__ void tma_plane(const CUtensorMap *tm, double *dst, ui
         : "memory");
 }
 
+constexpr size_t tma_smem_bytes(int BX, int BY, int NS)
+{
+    return (size_t)NS * (((BX + 4) * (BY + 2) + 15) / 16 * 16) * sizeof(double) + NS * sizeof(uint64_t);
+}
+
 // BX x BY tile per CTA, NT threads, NS-deep plane ring.  Each thread owns a pair of
 // x-points (double2) in RY rows.
 template <int BX, int BY, int NT, int NS>
@@ -182,13 +205,13 @@ __global__ void __launch_bounds__(NT) sweep_tma_kernel(const __grid_constant__ C
     static_assert(RY >= 1 && RY * NRG == BY, "tile shape");
     constexpr int W = BX + 4;      // staged width: x0-2 .. x0+BX+1
     constexpr int H = BY + 2;      // staged height: y0-1 .. y0+BY
-    constexpr int STAGE = W * H;
-    constexpr uint32_t STAGE_BYTES = STAGE * sizeof(double);
+    constexpr uint32_t STAGE_BYTES = W * H * sizeof(double);  // TMA transaction bytes
+    constexpr int STAGE = (W * H + 15) / 16 * 16;  // ring stride: TMA needs 128-byte aligned smem
     static_assert(NS >= 3, "ring must hold planes k, k+1 and prefetch");
 
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double *stage = reinterpret_cast<double *>(smem_raw);
-    uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + NS * STAGE_BYTES);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + NS * STAGE * sizeof(double));
 
     const Geom &g = a.g;
     int t = blockIdx.x;
@@ -224,6 +247,9 @@ __global__ void __launch_bounds__(NT) sweep_tma_kernel(const __grid_constant__ C
 #pragma unroll
     for (int r = 0; r < RY; ++r)
         zm[r] = *reinterpret_cast<const double2 *>(stage + (rg * RY + r + 1) * W + col);
+    __syncthreads();  // plane q = 0 only feeds zm: its stage is free for q = NS
+    if (threadIdx.x == 0 && NS < nq)
+        tma_plane(&tmap, stage, &bars[0], STAGE_BYTES, c0, y0, z0 + NS, c3);
     mbar_wait(&bars[1 % NS], (1 / NS) & 1);
 #pragma unroll
     for (int r = 0; r < RY; ++r)
@@ -339,9 +365,13 @@ __global__ void barrier_kernel(const BarrierArgs ba)
     for (int n = 0; n < ba.npeers; ++n) {
         const uint64_t *f = ba.ctrl + 1 + ba.peer_id[n];
         uint64_t v;
-        do {
+        const uint64_t t0 = globaltimer_ns();
+        for (;;) {
             asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(f) : "memory");
-        } while (v < e);
+            if (v >= e) break;
+            if (globaltimer_ns() - t0 > kSpinLimitNs) __trap();
+            __nanosleep(64);
+        }
     }
     __threadfence_system();
 }
@@ -381,7 +411,7 @@ __global__ void hash_init_kernel(const SweepArgs a, int64_t nx, int64_t ny, uint
 template <int BX, int BY, int NT, int NS>
 static cudaError_t launch_tma_t(const CUtensorMap &tm, const SweepArgs &a, cudaStream_t s)
 {
-    constexpr size_t smem = (size_t)NS * (BX + 4) * (BY + 2) * sizeof(double) + NS * sizeof(uint64_t);
+    constexpr size_t smem = tma_smem_bytes(BX, BY, NS);
     const int64_t grid = (int64_t)a.g.nslots * a.ntx * a.nty * a.ntz;
     sweep_tma_kernel<BX, BY, NT, NS><<<(unsigned)grid, NT, smem, s>>>(tm, a);
     return cudaGetLastError();
@@ -390,7 +420,7 @@ static cudaError_t launch_tma_t(const CUtensorMap &tm, const SweepArgs &a, cudaS
 template <int BX, int BY, int NT, int NS>
 static cudaError_t prepare_tma_t()
 {
-    constexpr size_t smem = (size_t)NS * (BX + 4) * (BY + 2) * sizeof(double) + NS * sizeof(uint64_t);
+    constexpr size_t smem = tma_smem_bytes(BX, BY, NS);
     return cudaFuncSetAttribute(sweep_tma_kernel<BX, BY, NT, NS>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 }
