@@ -1,0 +1,440 @@
+#!/usr/bin/env python
+"""bench.py -- the driver's benchmark contract for the overdecomposed Jacobi3D path.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config c2|c3|c4|c5] [--odf 8] [--no-sweep]
+
+A *step* is one Jacobi iteration of the whole hot path over the whole grid: every
+block's fused sweep + face exchange (a0/a1 -- planning
+and init -- are the cold path run before timing).  Metric: GLUP/s (10^9 lattice
+updates per second, whole job, all GPUs), BASELINE.json "Jacobi3D GLUP/s & ms/iter
+vs ODF (1 GPU) and at 2/4/8 B200; % HBM roofline".
+
+Workloads (synthetic, R11 hash init seed 1, shaped like the paper's Jacobi runs:
+uniform dense fp64 grid, fixed iteration count, no convergence check):
+  c2 (default)  BASELINE configs[1]: 512^3 per GPU, ODF 8 headline + the ODF sweep
+                1..64 at N=1; at N>1 weak scaling (global grid doubles z, y, x).
+  c3            configs[2]: 768^3 per GPU, ODF 8, weak scaling.
+  c4            configs[3]: 1536^3 global, ODF --odf (1 or 16), strong scaling.
+  c5            configs[4]: 1024^3 global, 32^3 blocks, strong scaling.
+Inputs are larger than L2 (>= 2 x 1.07 GB per GPU), so no L2 flush is needed.
+
+N > 1: launched by torchrun, one process per GPU; ranks exchange IPC records once
+(torch.distributed, plumbing only) and faces move by peer stores inside the sweep
+kernel; the timed region is bracketed by barrier + cuda synchronize, the device
+time (CUDA events on the launching stream) is max-reduced over ranks.
+
+--impl reference: the CPU oracle (oracle/, OpenMP over z on all host cores) timed
+on a bounded sample of the same workload -- the per-GPU 512^3 box, one iteration
+per step; rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+BYTES_PER_LUP = 16  # algorithmic HBM bytes per lattice update: 8 B read + 8 B write
+FLOPS_PER_LUP = 7
+
+
+# ------------------------------------------------------------------ geometry
+def blocks_for_odf(box, odf):
+    """Reading R9: from the per-GPU box, repeatedly halve the largest block extent;
+    ties go to z, then y, then x.  Returns blocks per GPU (bx, by, bz)."""
+    b = [1, 1, 1]
+    e = list(box)
+    left = odf
+    while left > 1:
+        if left % 2:
+            raise ValueError(f"ODF {odf} is not a power of two")
+        m = max(e)
+        d = next(k for k in (2, 1, 0) if e[k] == m)  # ties: z, then y, then x
+        if e[d] % 2:
+            raise ValueError(f"cannot halve extent {e[d]}")
+        e[d] //= 2
+        b[d] *= 2
+        left //= 2
+    return tuple(b)
+
+
+def weak_gpu_grid(n):
+    """Weak scaling: the global grid doubles z, then y, then x (PAPER.md:285
+    'grid dimensions are alternately increased'; matches reading R10)."""
+    g = [1, 1, 1]
+    d = 2
+    m = n
+    while m > 1:
+        if m % 2:
+            raise ValueError("n_gpus must be a power of two")
+        g[d] *= 2
+        d = (d - 1) % 3
+        m //= 2
+    return tuple(g)
+
+
+def workload(cfg, n, odf):
+    """(global dims, global blocks, gpu grid, label, scaling)."""
+    if cfg in ("c2", "c3"):
+        box = (512, 512, 512) if cfg == "c2" else (768, 768, 768)
+        g = weak_gpu_grid(n)
+        lb = blocks_for_odf(box, odf)
+        dims = tuple(box[d] * g[d] for d in range(3))
+        blocks = tuple(lb[d] * g[d] for d in range(3))
+        return dims, blocks, g, f"jacobi3d_{box[0]}^3_per_gpu_odf{odf}", "weak"
+    if cfg == "c4":
+        dims = (1536, 1536, 1536)
+        g = weak_gpu_grid(n)
+        box = tuple(dims[d] // g[d] for d in range(3))
+        lb = blocks_for_odf(box, odf)
+        return dims, tuple(lb[d] * g[d] for d in range(3)), g, f"jacobi3d_1536^3_global_odf{odf}", "strong"
+    if cfg == "c5":
+        dims = (1024, 1024, 1024)
+        g = weak_gpu_grid(n)
+        return dims, (32, 32, 32), g, "jacobi3d_1024^3_32^3_blocks", "strong"
+    raise ValueError(cfg)
+
+
+# ------------------------------------------------------------------ clocks (NVML)
+class ClockSampler:
+    """Samples SM clock and clock-event reasons of one GPU every ~2 ms (NVML)."""
+
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x2: "applications_clocks_setting",
+               0x10: "sync_boost", 0x100: "display_clock_setting"}
+
+    def __init__(self, cuda_index):
+        self.ok = False
+        self.samples, self.reasons = [], 0
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            idx = int(vis.split(",")[cuda_index]) if vis else cuda_index
+            self.N, self.h = N, N.nvmlDeviceGetHandleByIndex(idx)
+            self.max_mhz = N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # noqa: BLE001
+            self.err = str(e)
+
+    def _run(self):
+        N, h = self.N, self.h
+        while not self._stop.is_set():
+            try:
+                self.samples.append(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM))
+                try:
+                    r = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+                except AttributeError:
+                    r = N.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                self.reasons |= int(r)
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.ok:
+            self._stop = threading.Event()
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self._t.join()
+
+    def summary(self):
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "error": getattr(self, "err", "")}
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "samples": len(self.samples),
+                "reasons": [n for b, n in self.REASONS.items() if self.reasons & b]}
+
+
+def hbm_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        v = float(json.load(open(p))["hbm_gbs"])
+        return v, "measured"
+    except Exception:  # noqa: BLE001
+        return 6650.0, "fallback"
+
+
+def ncu_traffic(label):
+    """dram read+write bytes per sweep launch from the committed ncu summary."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        return json.load(open(p)).get(label)
+    except Exception:  # noqa: BLE001
+        return None
+
+
+# ------------------------------------------------------------------ distributed helpers
+class Dist:
+    def __init__(self):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.dist = None
+
+    def init(self, need_gpu=True):
+        if self.world > 1:
+            import torch
+            import torch.distributed as dist
+            if need_gpu:
+                torch.cuda.set_device(self.local)
+            dist.init_process_group("nccl" if need_gpu else "gloo")
+            self.dist = dist
+
+    def barrier(self):
+        if self.dist:
+            self.dist.barrier()
+
+    def max(self, v):
+        if not self.dist:
+            return v
+        import torch
+        t = torch.tensor([float(v)], device="cuda")
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum(self, v):
+        if not self.dist:
+            return v
+        import torch
+        t = torch.tensor([float(v)], device="cuda")
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM)
+        return float(t.item())
+
+    def finish(self):
+        if self.dist:
+            self.dist.barrier()
+            self.dist.destroy_process_group()
+
+
+# ------------------------------------------------------------------ CPU oracle timing
+def cpu_oracle(box=(512, 512, 512), n_target=None, budget_s=15.0, steps=None, warmup=0):
+    """Times the oracle as it stands (OpenMP over z, all host cores, iteration loop only)."""
+    import jac_inputs as JI
+    import oracle
+
+    nx, ny, nz = box
+    u0 = JI.hash_field(nx, ny, nz, seed=1)
+    if steps is None:
+        _, _, t1 = oracle.jacobi3d_omp_timed(u0, 1)
+        n = max(2, min(n_target or 100, int(budget_s / max(t1, 1e-6))))
+    else:
+        if warmup:
+            oracle.jacobi3d_omp_timed(u0, warmup)
+        n = steps
+    _, threads, secs = oracle.jacobi3d_omp_timed(u0, n)
+    glups = nx * ny * nz * n / secs / 1e9
+    return {"value": glups, "unit": "GLUP/s", "cores": threads, "kind": "oracle",
+            "sample": f"{nx}x{ny}x{nz} grid (the per-GPU C2 box), {n} iterations, OpenMP over z on {threads} "
+                      f"threads, iteration loop only", "ms_per_iter": 1e3 * secs / n, "nproc": os.cpu_count()}
+
+
+def run_reference(args, D):
+    D.init(need_gpu=False)
+    if D.rank != 0:
+        D.finish()
+        return
+    dims, blocks, g, label, scaling = workload(args.config, args.gpus, args.odf)
+    box = tuple(dims[d] // g[d] for d in range(3))
+    if args.config in ("c4", "c5"):
+        box = (512, 512, 512)  # bounded sample of a strong-scaling grid
+    cb = cpu_oracle(box=box, steps=args.steps, warmup=args.warmup)
+    line = {"impl": "reference", "metric": "Jacobi3D GLUP/s (whole job)", "value": cb["value"],
+            "unit": "GLUP/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": cb["ms_per_iter"], "higher_is_better": True, "scaling": scaling,
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (R11 splitmix64 hash, seed 1)",
+            "config": {"workload": label, "global_dims": dims, "sample_dims": box},
+            "cpu_baseline": {"kind": "oracle", "cores": cb["cores"], "sample": cb["sample"], "value": cb["value"],
+                             "unit": "GLUP/s"},
+            "e2e": {"value": cb["value"], "unit": "GLUP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    D.finish()
+
+
+# ------------------------------------------------------------------ our arm
+def time_ctx(J, K, W, D, sampler=None):
+    """W warm-up steps, then exactly K timed steps.  Returns device ms (max over ranks)."""
+    import torch
+    J.step(W)
+    st0 = J.stats()["kernel_launches"]
+    D.barrier()
+    torch.cuda.synchronize()
+    if sampler:
+        with sampler:
+            J.step(K)
+    else:
+        J.step(K)
+    torch.cuda.synchronize()
+    D.barrier()
+    dev_ms = D.max(J.last_step_ms())
+    launches = J.stats()["kernel_launches"] - st0
+    return dev_ms, launches
+
+
+def make_ctx(dims, blocks, g, D, flags=0):
+    import paper_2605_12734_b200 as jb
+    if D.world > 1:
+        from paper_2605_12734_b200.dist import create_rank_context
+        return create_rank_context(dims, blocks, gpu_grid=g, flags=flags, device=D.local)
+    return jb.Jacobi3D(dims, blocks, n_gpus=1, gpu_grid=g, flags=flags)
+
+
+def close_ctx(J, D):
+    if D.world > 1:
+        from paper_2605_12734_b200.dist import destroy_rank_context
+        destroy_rank_context(J)
+    else:
+        J.close()
+
+
+def run_ours(args, D):
+    import numpy as np
+    import torch
+
+    D.init(need_gpu=True)
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py: no CUDA device (the product path has no CPU fallback)")
+    from paper_2605_12734_b200 import jacobi3d as JB
+
+    K, W = args.steps, max(3, args.warmup)
+    dims, blocks, g, label, scaling = workload(args.config, args.gpus, args.odf)
+    pts = dims[0] * dims[1] * dims[2]
+    pts_gpu = pts // args.gpus
+    peak, peak_src = hbm_peak()
+
+    # ---- headline: timed region
+    J = make_ctx(dims, blocks, g, D)
+    J.set_init_hash(1)
+    sampler = ClockSampler(D.local)
+    dev_ms, launches = time_ctx(J, K, W, D, sampler)
+    value = pts * K / (dev_ms * 1e-3) / 1e9
+    ms_iter = dev_ms / K
+    st = J.stats()
+    # per-launch sweep duration (CUDA events around each sweep launch, same stream)
+    sweep_ms = D.max(J.profile_sweep(min(max(K, 10), 50)))
+    achieved = BYTES_PER_LUP * pts_gpu / (sweep_ms * 1e-3) / 1e9
+    traffic = ncu_traffic(label)
+
+    # ---- e2e through the public API with pinned host buffers
+    import jac_inputs as JI
+    origin, extent = J.local_box()
+    host_in = torch.empty((extent[2], extent[1], extent[0]), dtype=torch.float64, pin_memory=True).numpy()
+    host_in[...] = JI.hash_box(*dims, origin, extent, seed=1)
+    host_out = torch.empty_like(torch.from_numpy(host_in), pin_memory=True).numpy()
+    D.barrier()
+    t0 = time.perf_counter()
+    J.set_init_box(host_in, origin)
+    J.step(K)
+    J.field_box(host_out, origin)
+    e2e_s = D.max(time.perf_counter() - t0)
+    e2e_val = pts * K / e2e_s / 1e9
+    h2d = host_in.nbytes
+    d2h = pts_gpu * 8
+    close_ctx(J, D)
+
+    # ---- ODF sweep + ablations (N = 1, c2)
+    sweep = None
+    ablations = None
+    if args.gpus == 1 and args.config == "c2" and not args.no_sweep:
+        sweep = {}
+        for odf in (1, 2, 4, 8, 16, 32, 64):
+            d2, b2, g2, _, _ = workload("c2", 1, odf)
+            Jo = make_ctx(d2, b2, g2, D)
+            Jo.set_init_hash(1)
+            ms, _ = time_ctx(Jo, K, W, D)
+            sw = Jo.profile_sweep(20)
+            sweep[str(odf)] = {"blocks": b2, "ms_per_iter": ms / K, "glups": pts * K / (ms * 1e-3) / 1e9,
+                               "hbm_frac": BYTES_PER_LUP * pts / (ms / K * 1e-3) / 1e9 / peak,
+                               "sweep_kernel_us": 1e3 * sw}
+            close_ctx(Jo, D)
+        base = sweep["1"]["ms_per_iter"]
+        for v in sweep.values():
+            v["overhead_vs_odf1"] = v["ms_per_iter"] / base - 1.0
+        ablations = {}
+        d2, b2, g2, _, _ = workload("c2", 1, 16)
+        for name, fl in [("unfused_pack_ghost_kernel", JB.JAC_F_UNFUSED_PACK), ("no_tma", JB.JAC_F_NO_TMA),
+                         ("no_graph", JB.JAC_F_NO_GRAPH), ("skip_exchange_WRONG", JB.JAC_F_SKIP_EXCHANGE)]:
+            Ja = make_ctx(d2, b2, g2, D, flags=fl)
+            Ja.set_init_hash(1)
+            ms, _ = time_ctx(Ja, K, W, D)
+            ablations[name] = {"odf": 16, "ms_per_iter": ms / K, "glups": pts * K / (ms * 1e-3) / 1e9,
+                               "vs_default": ms / K / sweep["16"]["ms_per_iter"]}
+            close_ctx(Ja, D)
+
+    cpu = None
+    if args.gpus == 1 and D.rank == 0 and not args.no_cpu:
+        cpu = cpu_oracle(box=(512, 512, 512), budget_s=args.cpu_budget)
+
+    if D.rank == 0:
+        line = {
+            "metric": "Jacobi3D GLUP/s (whole job)", "value": value, "unit": "GLUP/s", "n_gpus": args.gpus,
+            "steps": K, "warmup": W, "ms_per_step": ms_iter, "higher_is_better": True, "scaling": scaling,
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (R11 splitmix64 hash, seed 1)",
+            "config": {"workload": label, "global_dims": dims, "blocks": blocks, "gpu_grid": g,
+                       "odf": blocks[0] * blocks[1] * blocks[2] // args.gpus, "step": "one Jacobi iteration",
+                       "l2": "inputs larger than L2 (2 ghosted fp64 arrays, >= 2.1 GB per GPU); no flush",
+                       "timing": "CUDA events on the launching stream around K graph-replayed iterations, max over ranks"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "kernel": "sweep_tma_kernel", "algorithmic_bytes_per_launch": BYTES_PER_LUP * pts_gpu,
+                         "avg_launch_us": 1e3 * sweep_ms,
+                         "sweep_share_of_step": sweep_ms / ms_iter},
+            "hbm_frac_step": BYTES_PER_LUP * pts_gpu / (ms_iter * 1e-3) / 1e9 / peak,
+            "hbm_frac_step_vs_8TBs": BYTES_PER_LUP * pts_gpu / (ms_iter * 1e-3) / 1e9 / 8000.0,
+            "e2e": {"value": e2e_val, "unit": "GLUP/s", "h2d_bytes_per_step": h2d / K, "d2h_bytes_per_step": d2h / K,
+                    "note": f"one job = jac_set_init_box (pinned H2D {h2d} B) + jac_step({K}) + "
+                            f"jac_get_field_box (pinned D2H {d2h} B); bytes amortised per iteration"},
+            "gpu_launches": launches,
+            "kernels_per_iter": st["kernels_per_iter"],
+            "clocks": sampler.summary(),
+            "cpu_baseline": cpu,
+            "exchange": {"remote_faces_per_gpu": st["remote_faces"], "remote_bytes_per_iter": st["remote_bytes"],
+                         "nvlink_ideal_us": st["remote_bytes"] / 900e9 * 1e6,
+                         "nvlink_share_ideal": st["remote_bytes"] / 900e9 / (ms_iter * 1e-3)},
+        }
+        if sweep is not None:
+            line["odf_sweep"] = sweep
+            line["ablations_odf16"] = ablations
+        print(json.dumps(line), flush=True)
+    D.finish()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=["c2", "c3", "c4", "c5"])
+    ap.add_argument("--odf", type=int, default=8)
+    ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    args = ap.parse_args()
+    D = Dist()
+    if D.world != args.gpus:
+        if D.world > 1:
+            raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={D.world}")
+        if args.gpus > 1 and args.impl == "ours":
+            raise SystemExit("--gpus N>1 must be launched with torchrun (one process per GPU)")
+    if args.impl == "reference":
+        run_reference(args, D)
+    else:
+        run_ours(args, D)
+
+
+if __name__ == "__main__":
+    main()

@@ -131,6 +131,16 @@ int jac_import_ipc(jac_ctx *c, const void *all);
  * ghosts are the neighbours' initial values.  Resets iterations_done to 0.  A
  * pinned host array is copied by DMA; a pageable one is staged by the driver. */
 int jac_set_init(jac_ctx *c, const double *padded);
+/* Same as jac_set_init for a sub-box of the padded global array: `box` holds
+ * extent[2] x extent[1] x extent[0] doubles (x fastest) whose element (0,0,0) is
+ * padded global cell (origin[0], origin[1], origin[2]).  It must cover the ghosted
+ * region of every local block (jac_local_box returns the smallest such box), else
+ * JAC_EINVAL.  This is how one rank of a multi-GPU run initialises its partition
+ * without holding the whole grid. */
+int jac_set_init_box(jac_ctx *c, const double *box, const int64_t *origin, const int64_t *extent);
+/* Padded-coordinate bounding box (origin[3], extent[3]) of this context's local
+ * blocks, ghost layers included. */
+int jac_local_box(const jac_ctx *c, int64_t *origin, int64_t *extent);
 /* Device-side synthetic init: every padded cell p gets R11's splitmix64 hash value
  * of key (seed << 40) + p, scaled to [0,1). */
 int jac_set_init_hash(jac_ctx *c, uint64_t seed);
@@ -148,6 +158,9 @@ int jac_get_block_padded(jac_ctx *c, int32_t ix, int32_t iy, int32_t iz, double 
 /* Interiors of all local blocks written into the padded host array (shell and
  * non-local blocks untouched). */
 int jac_get_field(jac_ctx *c, double *padded);
+/* Interiors of all local blocks written into a padded sub-box laid out as for
+ * jac_set_init_box (cells outside local interiors untouched). */
+int jac_get_field_box(jac_ctx *c, double *box, const int64_t *origin, const int64_t *extent);
 
 int jac_get_layout(const jac_ctx *c, int32_t *gpu_grid, int64_t *block_extent,
                    int64_t *iterations_done);

@@ -53,6 +53,20 @@ def hash_field(nx: int, ny: int, nz: int, seed: int = 1, chunk_planes: int = 64)
     return u
 
 
+def hash_box(nx: int, ny: int, nz: int, origin, extent, seed: int = 1) -> np.ndarray:
+    """Sub-box [extent z, y, x] of the padded R11 hash field starting at padded cell
+    origin = (ox, oy, oz) -- what one rank of a multi-GPU run holds."""
+    ox, oy, oz = (int(v) for v in origin)
+    sx, sy, sz = (int(v) for v in extent)
+    u = np.empty((sz, sy, sx), dtype=np.float64)
+    xs = np.arange(ox, ox + sx, dtype=np.uint64)
+    for k in range(sz):
+        rows = (np.uint64(oz + k) * np.uint64(ny + 2) + np.arange(oy, oy + sy, dtype=np.uint64))
+        p = rows[:, None] * np.uint64(nx + 2) + xs[None, :]
+        u[k] = hash_values(seed, p)
+    return u
+
+
 def constant_field(nx: int, ny: int, nz: int, c: float) -> np.ndarray:
     """P1: every padded cell = c."""
     return np.full((nz + 2, ny + 2, nx + 2), c, dtype=np.float64)

@@ -51,6 +51,9 @@ def lib() -> ctypes.CDLL:
         L.oracle_jacobi3d.restype = ctypes.c_int
         L.oracle_jacobi3d_omp.argtypes = [i64, i64, i64, dp, i64, dp, ctypes.c_int]
         L.oracle_jacobi3d_omp.restype = ctypes.c_int
+        L.oracle_jacobi3d_omp_timed.argtypes = [i64, i64, i64, dp, i64, dp, ctypes.c_int,
+                                                 ctypes.POINTER(ctypes.c_double)]
+        L.oracle_jacobi3d_omp_timed.restype = ctypes.c_int
         L.oracle_checksum.argtypes = [i64, i64, i64, dp]
         L.oracle_checksum.restype = ctypes.c_double
         L.oracle_bithash.argtypes = [i64, i64, i64, dp]
@@ -89,6 +92,18 @@ def jacobi3d_omp(u0: np.ndarray, n: int, nthreads: int = 0):
     if rc < 1:
         raise RuntimeError(f"oracle_jacobi3d_omp failed rc={rc}")
     return out, rc
+
+
+def jacobi3d_omp_timed(u0: np.ndarray, n: int, nthreads: int = 0):
+    """Returns (field, threads_used, seconds of the iteration loop alone)."""
+    nx, ny, nz = _dims(u0)
+    out = np.empty_like(u0)
+    secs = ctypes.c_double()
+    rc = lib().oracle_jacobi3d_omp_timed(nx, ny, nz, _ptr(u0), int(n), _ptr(out), int(nthreads),
+                                         ctypes.byref(secs))
+    if rc < 1:
+        raise RuntimeError(f"oracle_jacobi3d_omp_timed failed rc={rc}")
+    return out, rc, secs.value
 
 
 def checksum(u: np.ndarray) -> float:

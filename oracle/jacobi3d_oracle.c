@@ -93,8 +93,27 @@ int oracle_jacobi3d(int64_t nx, int64_t ny, int64_t nz, const double *u0, int64_
  * Per-point arithmetic is unchanged, so the result is bit-identical to the serial
  * oracle.  nthreads <= 0 means the OpenMP default.  Returns the thread count used
  * (>=1) or a negative error as above. */
+#include <time.h>
+static double now_s(void)
+{
+    struct timespec ts;
+    clock_gettime(CLOCK_MONOTONIC, &ts);
+    return (double)ts.tv_sec + 1e-9 * (double)ts.tv_nsec;
+}
+
+int oracle_jacobi3d_omp_timed(int64_t nx, int64_t ny, int64_t nz, const double *u0, int64_t n,
+                              double *out, int nthreads, double *loop_seconds);
+
 int oracle_jacobi3d_omp(int64_t nx, int64_t ny, int64_t nz, const double *u0, int64_t n,
                         double *out, int nthreads)
+{
+    return oracle_jacobi3d_omp_timed(nx, ny, nz, u0, n, out, nthreads, 0);
+}
+
+/* As oracle_jacobi3d_omp; *loop_seconds (if non-NULL) receives the wall time of the
+ * iteration loop alone (monotonic clock), for the bench's CPU baseline. */
+int oracle_jacobi3d_omp_timed(int64_t nx, int64_t ny, int64_t nz, const double *u0, int64_t n,
+                              double *out, int nthreads, double *loop_seconds)
 {
     if (nx < 1 || ny < 1 || nz < 1 || n < 0 || !u0 || !out) return -1;
     const size_t cells = (size_t)(nx + 2) * (size_t)(ny + 2) * (size_t)(nz + 2);
@@ -112,6 +131,7 @@ int oracle_jacobi3d_omp(int64_t nx, int64_t ny, int64_t nz, const double *u0, in
 #endif
     memcpy(A, u0, cells * sizeof(double));
     memcpy(B, u0, cells * sizeof(double));
+    const double t0 = now_s();
     for (int64_t it = 0; it < n; ++it) {
 #ifdef _OPENMP
 #pragma omp parallel for schedule(static)
@@ -119,6 +139,7 @@ int oracle_jacobi3d_omp(int64_t nx, int64_t ny, int64_t nz, const double *u0, in
         for (int64_t k = 1; k <= nz; ++k) sweep(nx, ny, nz, A, B, k, k);
         double *t = A; A = B; B = t;
     }
+    if (loop_seconds) *loop_seconds = now_s() - t0;
     memcpy(out, A, cells * sizeof(double));
     free(A); free(B);
     return used;

@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <climits>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -536,21 +537,50 @@ int jac_import_ipc(jac_ctx *c, const void *all)
     return JAC_OK;
 }
 
-int jac_set_init(jac_ctx *c, const double *padded)
+int jac_local_box(const jac_ctx *c, int64_t *origin, int64_t *extent)
+{
+    if (!c || !origin || !extent) return fail(JAC_EINVAL, "ctx/origin/extent is NULL");
+    const jac::Plan &p = c->plan;
+    int64_t lo[3] = {INT64_MAX, INT64_MAX, INT64_MAX}, hi[3] = {0, 0, 0};
+    for (const jac::DevBlock &d : c->hblocks)
+        for (int k = 0; k < 3; ++k) {
+            lo[k] = std::min<int64_t>(lo[k], d.org[k]);
+            hi[k] = std::max<int64_t>(hi[k], d.org[k] + p.e[k] + 2);
+        }
+    for (int k = 0; k < 3; ++k) { origin[k] = lo[k]; extent[k] = hi[k] - lo[k]; }
+    return JAC_OK;
+}
+
+namespace {
+int check_box(const jac_ctx *c, const void *box, const int64_t *origin, const int64_t *extent)
+{
+    if (!box || !origin || !extent) return fail(JAC_EINVAL, "box/origin/extent is NULL");
+    int64_t lo[3], ex[3];
+    jac_local_box(c, lo, ex);
+    for (int k = 0; k < 3; ++k)
+        if (origin[k] < 0 || extent[k] < 1 || origin[k] > lo[k] || origin[k] + extent[k] < lo[k] + ex[k] ||
+            origin[k] + extent[k] > c->plan.n[k] + 2)
+            return fail(JAC_EINVAL, "box origin/extent (dim %d: %lld+%lld) does not cover the local blocks (%lld+%lld)",
+                        k, (long long)origin[k], (long long)extent[k], (long long)lo[k], (long long)ex[k]);
+    return JAC_OK;
+}
+}  // namespace
+
+int jac_set_init_box(jac_ctx *c, const double *box, const int64_t *origin, const int64_t *extent)
 {
     int rc;
     if ((rc = require_ready(c))) return rc;
-    if (!padded) return fail(JAC_EINVAL, "padded is NULL");
+    if ((rc = check_box(c, box, origin, extent))) return rc;
     CK(cudaSetDevice(c->device));
-    const jac::Plan &p = c->plan;
     const jac::Geom &g = c->geom;
     if ((rc = enqueue_barrier(c))) return rc;  // neighbours finished writing our ghosts
     for (int32_t s = 0; s < c->nslots; ++s) {
         const jac::DevBlock &d = c->hblocks[s];
         cudaMemcpy3DParms m{};
-        m.srcPtr = make_cudaPitchedPtr(const_cast<double *>(padded), (size_t)(p.n[0] + 2) * 8,
-                                       (size_t)(p.n[0] + 2), (size_t)(p.n[1] + 2));
-        m.srcPos = make_cudaPos((size_t)d.org[0] * 8, (size_t)d.org[1], (size_t)d.org[2]);
+        m.srcPtr = make_cudaPitchedPtr(const_cast<double *>(box), (size_t)extent[0] * 8, (size_t)extent[0],
+                                       (size_t)extent[1]);
+        m.srcPos = make_cudaPos((size_t)(d.org[0] - origin[0]) * 8, (size_t)(d.org[1] - origin[1]),
+                                (size_t)(d.org[2] - origin[2]));
         m.dstPtr = make_cudaPitchedPtr(c->slot_ptr(0, s), (size_t)g.P * 8, (size_t)g.P, (size_t)(g.ey + 2));
         m.dstPos = make_cudaPos((size_t)(g.A - 1) * 8, 0, 0);
         m.extent = make_cudaExtent((size_t)(g.ex + 2) * 8, (size_t)(g.ey + 2), (size_t)(g.ez + 2));
@@ -560,6 +590,15 @@ int jac_set_init(jac_ctx *c, const double *padded)
     CK(cudaMemcpyAsync(c->slot_ptr(1, 0), c->slot_ptr(0, 0), (size_t)c->nslots * g.bstride * 8,
                        cudaMemcpyDeviceToDevice, c->stream));
     return finish_init(c);
+}
+
+int jac_set_init(jac_ctx *c, const double *padded)
+{
+    if (!c) return fail(JAC_EINVAL, "ctx is NULL");
+    if (!padded) return fail(JAC_EINVAL, "padded is NULL");
+    const int64_t o[3] = {0, 0, 0};
+    const int64_t e[3] = {c->plan.n[0] + 2, c->plan.n[1] + 2, c->plan.n[2] + 2};
+    return jac_set_init_box(c, padded, o, e);
 }
 
 int jac_set_init_hash(jac_ctx *c, uint64_t seed)
@@ -680,25 +719,36 @@ int jac_get_block(jac_ctx *c, int32_t ix, int32_t iy, int32_t iz, double *out)
     return JAC_OK;
 }
 
-int jac_get_field(jac_ctx *c, double *padded)
+int jac_get_field_box(jac_ctx *c, double *box, const int64_t *origin, const int64_t *extent)
 {
-    if (!c || !padded) return fail(JAC_EINVAL, "ctx/padded is NULL");
+    if (!c) return fail(JAC_EINVAL, "ctx is NULL");
+    int rc;
+    if ((rc = check_box(c, box, origin, extent))) return rc;
     CK(cudaSetDevice(c->device));
-    const jac::Plan &p = c->plan;
     const jac::Geom &g = c->geom;
     for (int32_t s = 0; s < c->nslots; ++s) {
         const jac::DevBlock &d = c->hblocks[s];
         cudaMemcpy3DParms m{};
         m.srcPtr = make_cudaPitchedPtr(c->slot_ptr((int)(c->iters & 1), s), (size_t)g.P * 8, (size_t)g.P, (size_t)(g.ey + 2));
         m.srcPos = make_cudaPos((size_t)g.A * 8, 1, 1);
-        m.dstPtr = make_cudaPitchedPtr(padded, (size_t)(p.n[0] + 2) * 8, (size_t)(p.n[0] + 2), (size_t)(p.n[1] + 2));
-        m.dstPos = make_cudaPos((size_t)(d.org[0] + 1) * 8, (size_t)(d.org[1] + 1), (size_t)(d.org[2] + 1));
+        m.dstPtr = make_cudaPitchedPtr(box, (size_t)extent[0] * 8, (size_t)extent[0], (size_t)extent[1]);
+        m.dstPos = make_cudaPos((size_t)(d.org[0] + 1 - origin[0]) * 8, (size_t)(d.org[1] + 1 - origin[1]),
+                                (size_t)(d.org[2] + 1 - origin[2]));
         m.extent = make_cudaExtent((size_t)g.ex * 8, (size_t)g.ey, (size_t)g.ez);
         m.kind = cudaMemcpyDeviceToHost;
         CK(cudaMemcpy3DAsync(&m, c->stream));
     }
     CK(cudaStreamSynchronize(c->stream));
     return JAC_OK;
+}
+
+int jac_get_field(jac_ctx *c, double *padded)
+{
+    if (!c) return fail(JAC_EINVAL, "ctx is NULL");
+    if (!padded) return fail(JAC_EINVAL, "padded is NULL");
+    const int64_t o[3] = {0, 0, 0};
+    const int64_t e[3] = {c->plan.n[0] + 2, c->plan.n[1] + 2, c->plan.n[2] + 2};
+    return jac_get_field_box(c, padded, o, e);
 }
 
 int jac_get_layout(const jac_ctx *c, int32_t *gpu_grid, int64_t *block_extent, int64_t *iterations_done)

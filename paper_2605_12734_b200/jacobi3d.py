@@ -33,7 +33,7 @@ STAT_NAMES = ["kernel_launches", "graph_launches", "kernels_per_iter", "local_bl
 EXPORTED = ["jac_plan", "jac_plan_face", "jac_create", "jac_create_rank", "jac_ipc_handle_bytes",
             "jac_export_ipc", "jac_import_ipc", "jac_set_init", "jac_set_init_hash", "jac_step",
             "jac_get_block", "jac_get_block_padded", "jac_get_field", "jac_get_layout",
-            "jac_block_owner", "jac_last_step_ms", "jac_profile_sweep", "jac_get_stats",
+            "jac_block_owner", "jac_last_step_ms", "jac_set_init_box", "jac_get_field_box", "jac_local_box", "jac_profile_sweep", "jac_get_stats",
             "jac_destroy", "jac_last_error", "jac_version"]
 
 _ERRNAMES = {-1: "JAC_EINVAL", -2: "JAC_EDECOMP", -3: "JAC_EDEVICE", -4: "JAC_ENOMEM",
@@ -78,6 +78,9 @@ def load() -> ctypes.CDLL:
         "jac_get_block": [vp, i32, i32, i32, dp],
         "jac_get_block_padded": [vp, i32, i32, i32, dp],
         "jac_get_field": [vp, dp],
+        "jac_set_init_box": [vp, dp, P(i64), P(i64)],
+        "jac_get_field_box": [vp, dp, P(i64), P(i64)],
+        "jac_local_box": [vp, P(i64), P(i64)],
         "jac_get_layout": [vp, P(i32), P(i64), P(i64)],
         "jac_block_owner": [vp, i32, i32, i32, P(i32)],
         "jac_last_step_ms": [vp, P(ctypes.c_double)],
@@ -188,6 +191,32 @@ def jac_get_field(ctx, padded: np.ndarray) -> np.ndarray:
     return padded
 
 
+def _i64x3(v):
+    return (ctypes.c_int64 * 3)(*[int(x) for x in v])
+
+
+def jac_set_init_box(ctx, box: np.ndarray, origin) -> None:
+    """``box`` is a [sz, sy, sx] float64 sub-array of the padded grid starting at
+    padded cell ``origin`` = (ox, oy, oz)."""
+    if box.dtype != np.float64 or not box.flags.c_contiguous or box.ndim != 3:
+        raise ValueError("box must be a C-contiguous float64 3-D array")
+    ext = (box.shape[2], box.shape[1], box.shape[0])
+    _check(load().jac_set_init_box(ctx, _dptr(box), _i64x3(origin), _i64x3(ext)), "jac_set_init_box")
+
+
+def jac_get_field_box(ctx, box: np.ndarray, origin) -> np.ndarray:
+    ext = (box.shape[2], box.shape[1], box.shape[0])
+    _check(load().jac_get_field_box(ctx, _dptr(box), _i64x3(origin), _i64x3(ext)), "jac_get_field_box")
+    return box
+
+
+def jac_local_box(ctx):
+    o = (ctypes.c_int64 * 3)()
+    e = (ctypes.c_int64 * 3)()
+    _check(load().jac_local_box(ctx, o, e), "jac_local_box")
+    return tuple(o), tuple(e)
+
+
 def jac_get_layout(ctx):
     g = (ctypes.c_int32 * 3)()
     e = (ctypes.c_int64 * 3)()
@@ -275,6 +304,16 @@ class Jacobi3D:
         from the device."""
         out = np.array(like, dtype=np.float64, copy=True)
         return jac_get_field(self.ctx, out)
+
+    def local_box(self):
+        """(origin, extent) of this context's ghosted bounding box, padded coords (x, y, z)."""
+        return jac_local_box(self.ctx)
+
+    def set_init_box(self, box: np.ndarray, origin) -> None:
+        jac_set_init_box(self.ctx, box, origin)
+
+    def field_box(self, box: np.ndarray, origin) -> np.ndarray:
+        return jac_get_field_box(self.ctx, box, origin)
 
     @property
     def iterations(self) -> int:
