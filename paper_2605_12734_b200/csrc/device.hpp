@@ -50,8 +50,12 @@ struct SweepArgs {
     double *outbox;
     int32_t src;             // buffer read (0/1); the sweep writes 1-src
     int32_t mode;            // SweepMode
-    int32_t ntx, nty, ntz;   // tiles per block in x, y, z
-    int32_t zc;              // planes per z-chunk
+    int32_t ntx, nty, ntz;   // tiles per block in x, y, z (ntz: plain kernel only)
+    int32_t zc;              // planes per z-chunk (plain kernel only)
+    // TMA kernel work list: item = zchunk * ncols + column, column = (b*nty + ty)*ntx + tx;
+    // persistent CTA c takes items c, c + gridDim.x, ...; z-chunk zi of a column covers
+    // planes [zi*ez/nzc, (zi+1)*ez/nzc).
+    int32_t nzc, ncols, nitems;
 };
 
 // Neighbour barrier between ranks (one process per GPU): one flag word per sender

@@ -90,6 +90,7 @@ struct jac_ctx {
     int variant = 0;          // 0 TMA wide, 1 TMA narrow, 2 plain
     CUtensorMap tmap{};
     int ntx = 1, nty = 1, ntz = 1, zc = 1;
+    int nzc = 1, ncols = 1, nitems = 1;
 
     // cross-rank exchange
     std::vector<int32_t> peer_ranks;     // face-adjacent ranks
@@ -145,6 +146,7 @@ jac::SweepArgs sweep_args(const jac_ctx *c, int src, int mode)
     a.src = src;
     a.mode = mode;
     a.ntx = c->ntx; a.nty = c->nty; a.ntz = c->ntz; a.zc = c->zc;
+    a.nzc = c->nzc; a.ncols = c->ncols; a.nitems = c->nitems;
     return a;
 }
 
@@ -277,7 +279,8 @@ int create_common(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, in
     jac::Geom &g = c->geom;
     g.ex = (int32_t)plan.e[0]; g.ey = (int32_t)plan.e[1]; g.ez = (int32_t)plan.e[2];
     g.A = jac::kA;
-    g.P = round_up(g.A + g.ex + 2, 4);
+    if (const char *s = getenv("JAC_A")) g.A = std::max(2, atoi(s) & ~1);  // layout experiment knob
+    g.P = round_up(g.A + g.ex + 4, 4);  // room for the 32-byte +x ghost sector (A % 4 == 0)
     g.Q = g.P * (g.ey + 2);
     g.bstride = round_up(g.Q * (g.ez + 2), 32);
     g.nslots = c->nslots;
@@ -290,6 +293,7 @@ int create_common(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, in
     // tile shape / variant
     if (flags & JAC_F_NO_TMA) c->variant = 2;
     else c->variant = (g.ex <= 32) ? jac::TMA_NARROW : jac::TMA_WIDE;
+    if (const char *s = getenv("JAC_VARIANT"); s && c->variant != 2) c->variant = atoi(s) ? jac::TMA_NARROW : jac::TMA_WIDE;
     const int tbx = (c->variant == 2) ? 64 : jac::tma_tile_shape(c->variant).bx;
     const int tby = (c->variant == 2) ? 8 : jac::tma_tile_shape(c->variant).by;
     c->ntx = (g.ex + tbx - 1) / tbx;
@@ -301,6 +305,18 @@ int create_common(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, in
     if (const char *s = getenv("JAC_ZC")) zc = std::max(1, std::min(g.ez, atoi(s)));
     c->zc = zc;
     c->ntz = (g.ez + zc - 1) / zc;
+    // TMA kernel work list: columns cut into z-chunks of ~32 planes.  Short
+    // chunks keep concurrently running CTAs at nearby z, so the x/y halo rows one
+    // CTA stages are L2 hits for its neighbours (long marches drift apart and turn
+    // the halos into DRAM re-reads: measured +19.6% reads at 256-plane chunks);
+    // the price is 2 extra planes per chunk.
+    c->ncols = c->nslots * c->ntx * c->nty;
+    {
+        int zchunk = 32;
+        if (const char *s = getenv("JAC_ZCHUNK")) zchunk = std::max(1, atoi(s));
+        c->nzc = std::max(1, (g.ez + zchunk - 1) / zchunk);
+        c->nitems = c->ncols * c->nzc;
+    }
     if (const char *s = getenv("JAC_UNROLL")) c->unroll = std::max(2, atoi(s) & ~1);
     if ((int64_t)c->nslots * c->ntx * c->nty * c->ntz > 0x7fffffffLL) {
         delete c;

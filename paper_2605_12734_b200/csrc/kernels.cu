@@ -29,6 +29,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstdint>
 
 #include "device.hpp"
@@ -88,16 +89,34 @@ __device__ __forceinline__ void emit_pair(const SweepArgs &a, const DevBlock &bl
             double *p = blk.nb[YP][dst];
             if (p) st_pair(p + (int64_t)(k + 1) * g.Q + g.A + i, v, both);
         }
+        // x-faces: the ghost column is strided (one value per row).  Write the
+        // whole 32-byte sector holding it (the rest is row padding) so L2 never
+        // has to fetch a partially written sector from DRAM.
         if (i == 0) {
             double *p = blk.nb[XM][dst];
-            if (p) p[off - i + g.ex] = v.x;  // neighbour's ghost column i = ex
+            if (p) {
+                double *q = p + (off - i + g.ex);  // neighbour's ghost column i = ex (col A+ex)
+                if (((g.A + g.ex) & 3) == 0) {  // ghost alone in its sector
+                    *reinterpret_cast<double2 *>(q) = make_double2(v.x, 0.0);
+                    *reinterpret_cast<double2 *>(q + 2) = make_double2(0.0, 0.0);
+                } else {
+                    *q = v.x;
+                }
+            }
         }
-        if (i == g.ex - 1) {
+        const bool last_x = (i == g.ex - 1) || (both && i + 1 == g.ex - 1);
+        if (last_x) {
             double *p = blk.nb[XP][dst];
-            if (p) p[off - i - 1] = v.x;     // neighbour's ghost column i = -1
-        } else if (both && i + 1 == g.ex - 1) {
-            double *p = blk.nb[XP][dst];
-            if (p) p[off - i - 1] = v.y;
+            if (p) {
+                const double val = (i == g.ex - 1) ? v.x : v.y;
+                double *q = p + (off - i - 1);     // neighbour's ghost column i = -1 (col A-1)
+                if ((g.A & 3) == 0) {                // ghost is the last word of its sector
+                    *reinterpret_cast<double2 *>(q - 3) = make_double2(0.0, 0.0);
+                    *reinterpret_cast<double2 *>(q - 1) = make_double2(0.0, val);
+                } else {
+                    *q = val;
+                }
+            }
         }
     } else {  // MODE_PACK: contiguous outbox faces, layouts x:[k][j] y:[k][i] z:[j][i]
         double *ob = a.outbox + (int64_t)blk.slot * g.ostride;
@@ -193,10 +212,70 @@ constexpr size_t tma_smem_bytes(int BX, int BY, int NS)
     return (size_t)NS * (((BX + 4) * (BY + 2) + 15) / 16 * 16) * sizeof(double) + NS * sizeof(uint64_t);
 }
 
-// BX x BY tile per CTA, NT threads, NS-deep plane ring.  Each thread owns a pair of
-// x-points (double2) in RY rows.
+struct TileItem {
+    int b, x0, y0, zs, ze;
+};
+
+template <int BX, int BY>
+__device__ __forceinline__ TileItem decode_item(const SweepArgs &a, int item)
+{
+    TileItem t;
+    const int zi = item / a.ncols;
+    int col = item - zi * a.ncols;
+    const int tx = col % a.ntx; col /= a.ntx;
+    const int ty = col % a.nty;
+    t.b = col / a.nty;
+    t.x0 = tx * BX;
+    t.y0 = ty * BY;
+    t.zs = (int)(((int64_t)zi * a.g.ez) / a.nzc);
+    t.ze = (int)(((int64_t)(zi + 1) * a.g.ez) / a.nzc);
+    return t;
+}
+
+// Producer state (thread 0 only): walks this CTA's items and their planes in order,
+// keeping up to NS plane loads in flight across item boundaries.
+template <int BX, int BY, int NS>
+struct Producer {
+    int item;    // current item index (global)
+    int p;       // plane offset within the item's load sequence (0 .. ze-zs+1)
+    uint32_t l;  // loads issued so far
+    TileItem t;
+    int c3;
+
+    __device__ __forceinline__ void start(const SweepArgs &a)
+    {
+        item = blockIdx.x;
+        p = 0;
+        l = 0;
+        if (item < a.nitems) {
+            t = decode_item<BX, BY>(a, item);
+            c3 = a.src * a.g.nslots + a.blocks[t.b].slot;
+        }
+    }
+    __device__ __forceinline__ void issue(const SweepArgs &a, const CUtensorMap *tm, double *stage,
+                                          uint64_t *bars, int stage_doubles, uint32_t bytes)
+    {
+        if (item >= a.nitems) return;
+        const int s = (int)(l % NS);
+        // plane k = zs - 1 + p  ->  tensor z index k + 1 = zs + p
+        tma_plane(tm, stage + s * stage_doubles, &bars[s], bytes, a.g.A - 2 + t.x0, t.y0, t.zs + p, c3);
+        ++l;
+        if (++p == t.ze - t.zs + 2) {
+            p = 0;
+            item += gridDim.x;
+            if (item < a.nitems) {
+                t = decode_item<BX, BY>(a, item);
+                c3 = a.src * a.g.nslots + a.blocks[t.b].slot;
+            }
+        }
+    }
+};
+
+// Persistent TMA z-march.  BX x BY column tile per work item, NT threads, NS-deep
+// plane ring.  Each thread owns a pair of x-points (double2) in RY rows; the
+// z-neighbours ride in registers, x/y neighbours come from the staged plane.
 template <int BX, int BY, int NT, int NS>
-__global__ void __launch_bounds__(NT) sweep_tma_kernel(const __grid_constant__ CUtensorMap tmap,
+__global__ void __launch_bounds__(NT, 4) sweep_tma_kernel(const __grid_constant__ CUtensorMap tmap,
                                                        const SweepArgs a)
 {
     constexpr int TXL = BX / 2;    // threads along x
@@ -214,78 +293,73 @@ __global__ void __launch_bounds__(NT) sweep_tma_kernel(const __grid_constant__ C
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + NS * STAGE * sizeof(double));
 
     const Geom &g = a.g;
-    int t = blockIdx.x;
-    const int tx = t % a.ntx; t /= a.ntx;
-    const int ty = t % a.nty; t /= a.nty;
-    const int tz = t % a.ntz;
-    const int b = t / a.ntz;
-    const int x0 = tx * BX, y0 = ty * BY, z0 = tz * a.zc;
-    const int z1 = min(g.ez, z0 + a.zc);
-    const int nq = (z1 - z0) + 2;  // planes z0-1 .. z1 (interior k = z0-1+q)
-    const DevBlock &blk = a.blocks[b];
-    const int c3 = a.src * g.nslots + blk.slot;
-    const int c0 = g.A - 2 + x0;
-    const int dst = 1 - a.src;
-
+    __shared__ Producer<BX, BY, NS> prod;  // touched by thread 0 only; kept out of registers
     if (threadIdx.x == 0) {
         for (int s = 0; s < NS; ++s) mbar_init(&bars[s], 1);
         mbar_fence_init();
+        prod.start(a);
+        for (int s = 0; s < NS; ++s) prod.issue(a, &tmap, stage, bars, STAGE, STAGE_BYTES);
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        for (int q = 0; q < NS && q < nq; ++q)
-            tma_plane(&tmap, stage + q * STAGE, &bars[q], STAGE_BYTES, c0, y0, z0 + q, c3);
-    }
 
     const int lane = threadIdx.x % TXL;
     const int rg = threadIdx.x / TXL;
     const int col = 2 * lane + 2;  // staged column of point i = x0 + 2*lane
-    const int i = x0 + 2 * lane;
+    const int dst = 1 - a.src;
+    uint32_t l = 0;                // loads consumed
 
-    double2 zm[RY], c[RY], zp[RY];
-    mbar_wait(&bars[0], 0);
-#pragma unroll
-    for (int r = 0; r < RY; ++r)
-        zm[r] = *reinterpret_cast<const double2 *>(stage + (rg * RY + r + 1) * W + col);
-    __syncthreads();  // plane q = 0 only feeds zm: its stage is free for q = NS
-    if (threadIdx.x == 0 && NS < nq)
-        tma_plane(&tmap, stage, &bars[0], STAGE_BYTES, c0, y0, z0 + NS, c3);
-    mbar_wait(&bars[1 % NS], (1 / NS) & 1);
-#pragma unroll
-    for (int r = 0; r < RY; ++r)
-        c[r] = *reinterpret_cast<const double2 *>(stage + (1 % NS) * STAGE + (rg * RY + r + 1) * W + col);
+    // release(): every thread is done with the oldest unreleased stage -> refill it
+    auto release = [&]() {
+        __syncthreads();
+        if (threadIdx.x == 0) prod.issue(a, &tmap, stage, bars, STAGE, STAGE_BYTES);
+    };
+    auto plane = [&](uint32_t li) { return stage + (li % NS) * STAGE; };
+    auto wait = [&](uint32_t li) { mbar_wait(&bars[li % NS], (li / NS) & 1); };
 
-    for (int m = 0; m < nq - 2; ++m) {
-        const int qn = m + 2;
-        const double *Sn = stage + (qn % NS) * STAGE;
-        mbar_wait(&bars[qn % NS], (qn / NS) & 1);
+    for (int item = blockIdx.x; item < a.nitems; item += gridDim.x) {
+        const TileItem t = decode_item<BX, BY>(a, item);
+        const DevBlock &blk = a.blocks[t.b];
+        const int i = t.x0 + 2 * lane;
+        double2 zm[RY], c[RY], zp[RY];
+        wait(l);
 #pragma unroll
         for (int r = 0; r < RY; ++r)
-            zp[r] = *reinterpret_cast<const double2 *>(Sn + (rg * RY + r + 1) * W + col);
+            zm[r] = *reinterpret_cast<const double2 *>(plane(l) + (rg * RY + r + 1) * W + col);
+        release();  // plane zs-1 only feeds zm
+        ++l;
+        wait(l);
+#pragma unroll
+        for (int r = 0; r < RY; ++r)
+            c[r] = *reinterpret_cast<const double2 *>(plane(l) + (rg * RY + r + 1) * W + col);
 
-        const double *S = stage + ((m + 1) % NS) * STAGE;
-        const int k = z0 + m;
+        for (int k = t.zs; k < t.ze; ++k) {
+            const double *Sn = plane(l + 1);
+            wait(l + 1);
 #pragma unroll
-        for (int r = 0; r < RY; ++r) {
-            const int jl = rg * RY + r;
-            const double *row = S + (jl + 1) * W + col;
-            const double xm = row[-1];
-            const double xp = row[2];
-            const double2 ym = (r == 0) ? *reinterpret_cast<const double2 *>(row - W) : c[r - 1];
-            const double2 yp = (r == RY - 1) ? *reinterpret_cast<const double2 *>(row + W) : c[r + 1];
-            double2 v;
-            v.x = stencil7(c[r].x, xm, c[r].y, ym.x, yp.x, zm[r].x, zp[r].x);
-            v.y = stencil7(c[r].y, c[r].x, xp, ym.y, yp.y, zm[r].y, zp[r].y);
-            const int j = y0 + jl;
-            if (j < g.ey) emit_pair(a, blk, dst, i, j, k, v);
-        }
-        __syncthreads();  // every thread is done with stage (m+1) % NS
-        if (threadIdx.x == 0 && m + 1 + NS < nq) {
-            const int q = m + 1 + NS;
-            tma_plane(&tmap, stage + (q % NS) * STAGE, &bars[q % NS], STAGE_BYTES, c0, y0, z0 + q, c3);
-        }
+            for (int r = 0; r < RY; ++r)
+                zp[r] = *reinterpret_cast<const double2 *>(Sn + (rg * RY + r + 1) * W + col);
+            const double *S = plane(l);
 #pragma unroll
-        for (int r = 0; r < RY; ++r) { zm[r] = c[r]; c[r] = zp[r]; }
+            for (int r = 0; r < RY; ++r) {
+                const int jl = rg * RY + r;
+                const double *row = S + (jl + 1) * W + col;
+                const double xm = row[-1];
+                const double xp = row[2];
+                const double2 ym = (r == 0) ? *reinterpret_cast<const double2 *>(row - W) : c[r - 1];
+                const double2 yp = (r == RY - 1) ? *reinterpret_cast<const double2 *>(row + W) : c[r + 1];
+                double2 v;
+                v.x = stencil7(c[r].x, xm, c[r].y, ym.x, yp.x, zm[r].x, zp[r].x);
+                v.y = stencil7(c[r].y, c[r].x, xp, ym.y, yp.y, zm[r].y, zp[r].y);
+                const int j = t.y0 + jl;
+                if (j < g.ey) emit_pair(a, blk, dst, i, j, k, v);
+            }
+            release();  // centre plane k is done
+            ++l;
+#pragma unroll
+            for (int r = 0; r < RY; ++r) { zm[r] = c[r]; c[r] = zp[r]; }
+        }
+        release();  // plane ze only fed zp
+        ++l;
     }
 }
 
@@ -409,10 +483,35 @@ __global__ void hash_init_kernel(const SweepArgs a, int64_t nx, int64_t ny, uint
 
 // ------------------------------------------------------------------ host launchers
 template <int BX, int BY, int NT, int NS>
+static int resident_tma_t()
+{
+    static int resident = 0;  // SMs x CTAs per SM (per process; one device per process)
+    if (!resident) {
+        constexpr size_t smem = tma_smem_bytes(BX, BY, NS);
+        int dev = 0, sms = 0, per_sm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_tma_kernel<BX, BY, NT, NS>, NT, smem);
+        resident = std::max(1, sms * std::max(1, per_sm));
+    }
+    return resident;
+}
+
+template <int BX, int BY, int NT, int NS>
 static cudaError_t launch_tma_t(const CUtensorMap &tm, const SweepArgs &a, cudaStream_t s)
 {
     constexpr size_t smem = tma_smem_bytes(BX, BY, NS);
-    const int64_t grid = (int64_t)a.g.nslots * a.ntx * a.nty * a.ntz;
+    // One CTA per item by default: the hardware launches CTAs in index order as slots
+    // free up, which keeps x/y-adjacent tiles (and successive z-chunks of a column)
+    // temporally close, so their shared halo planes are L2 hits.  A persistent grid
+    // with static striding lets CTAs drift apart and turns halos into DRAM re-reads
+    // (measured 359 -> 454 us per 512^3 sweep).  JAC_GRID=<n> caps the grid (tuning).
+    static int grid_cap = -1;
+    if (grid_cap < 0) {
+        const char *e = getenv("JAC_GRID");
+        grid_cap = e ? std::max(0, atoi(e)) : 0;
+    }
+    const int grid = grid_cap > 0 ? std::min(a.nitems, grid_cap) : a.nitems;
     sweep_tma_kernel<BX, BY, NT, NS><<<(unsigned)grid, NT, smem, s>>>(tm, a);
     return cudaGetLastError();
 }
@@ -429,6 +528,12 @@ cudaError_t prepare_sweep_tma(int variant)
 {
     if (variant == TMA_NARROW) return prepare_tma_t<32, 16, 256, 4>();
     return prepare_tma_t<64, 16, 256, 4>();
+}
+
+int sweep_resident_ctas(int variant)
+{
+    if (variant == TMA_NARROW) return resident_tma_t<32, 16, 256, 4>();
+    return resident_tma_t<64, 16, 256, 4>();
 }
 
 TileShape tma_tile_shape(int variant)

@@ -11,7 +11,8 @@ enum TmaVariant { TMA_WIDE = 0 /* 64 x 16 tiles */, TMA_NARROW = 1 /* 32 x 16 ti
 struct TileShape { int bx, by; };
 
 TileShape tma_tile_shape(int variant);
-cudaError_t prepare_sweep_tma(int variant);  // sets the dynamic-smem attribute (current device)
+cudaError_t prepare_sweep_tma(int variant);
+int sweep_resident_ctas(int variant);         // SMs x resident CTAs of the TMA sweep (current device)  // sets the dynamic-smem attribute (current device)
 cudaError_t launch_sweep_tma(const CUtensorMap &tm, const SweepArgs &a, int variant, cudaStream_t s);
 cudaError_t launch_sweep_plain(const SweepArgs &a, cudaStream_t s);  // 64 x 8 tiles
 cudaError_t launch_ghost_fill(const SweepArgs &a, int dst, cudaStream_t s);
