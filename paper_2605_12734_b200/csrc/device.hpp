@@ -52,10 +52,11 @@ struct SweepArgs {
     int32_t mode;            // SweepMode
     int32_t ntx, nty, ntz;   // tiles per block in x, y, z (ntz: plain kernel only)
     int32_t zc;              // planes per z-chunk (plain kernel only)
-    // TMA kernel work list: item = zchunk * ncols + column, column = (b*nty + ty)*ntx + tx;
-    // persistent CTA c takes items c, c + gridDim.x, ...; z-chunk zi of a column covers
-    // planes [zi*ez/nzc, (zi+1)*ez/nzc).
-    int32_t nzc, ncols, nitems;
+    // TMA kernel work list.  column = (b*nty + ty)*ntx + tx; columns are cut into
+    // groups of gcols (about the number of resident CTAs), and items run group by
+    // group, z-chunk-major inside a group: item = g*gcols*nzc + zi*gsize + (col - g*gcols).
+    // z-chunk zi of a column covers planes [zi*ez/nzc, (zi+1)*ez/nzc).
+    int32_t nzc, ncols, nitems, gcols;
 };
 
 // Neighbour barrier between ranks (one process per GPU): one flag word per sender

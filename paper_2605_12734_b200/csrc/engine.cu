@@ -90,7 +90,7 @@ struct jac_ctx {
     int variant = 0;          // 0 TMA wide, 1 TMA narrow, 2 plain
     CUtensorMap tmap{};
     int ntx = 1, nty = 1, ntz = 1, zc = 1;
-    int nzc = 1, ncols = 1, nitems = 1;
+    int nzc = 1, ncols = 1, nitems = 1, gcols = 1;
 
     // cross-rank exchange
     std::vector<int32_t> peer_ranks;     // face-adjacent ranks
@@ -146,7 +146,7 @@ jac::SweepArgs sweep_args(const jac_ctx *c, int src, int mode)
     a.src = src;
     a.mode = mode;
     a.ntx = c->ntx; a.nty = c->nty; a.ntz = c->ntz; a.zc = c->zc;
-    a.nzc = c->nzc; a.ncols = c->ncols; a.nitems = c->nitems;
+    a.nzc = c->nzc; a.ncols = c->ncols; a.nitems = c->nitems; a.gcols = c->gcols;
     return a;
 }
 
@@ -316,6 +316,12 @@ int create_common(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, in
         if (const char *s = getenv("JAC_ZCHUNK")) zchunk = std::max(1, atoi(s));
         c->nzc = std::max(1, (g.ez + zchunk - 1) / zchunk);
         c->nitems = c->ncols * c->nzc;
+        // Column groups of ~one resident wave: inside a group the chunk k+1 item of a
+        // column launches about when its chunk k item retires, so the two planes they
+        // share are still in L2.
+        int gcols = c->variant == 2 ? c->ncols : jac::sweep_resident_ctas(c->variant);
+        if (const char *s = getenv("JAC_GCOLS")) gcols = atoi(s);
+        c->gcols = std::max(1, std::min(c->ncols, gcols > 0 ? gcols : c->ncols));
     }
     if (const char *s = getenv("JAC_UNROLL")) c->unroll = std::max(2, atoi(s) & ~1);
     if ((int64_t)c->nslots * c->ntx * c->nty * c->ntz > 0x7fffffffLL) {

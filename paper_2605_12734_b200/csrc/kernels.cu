@@ -220,8 +220,11 @@ template <int BX, int BY>
 __device__ __forceinline__ TileItem decode_item(const SweepArgs &a, int item)
 {
     TileItem t;
-    const int zi = item / a.ncols;
-    int col = item - zi * a.ncols;
+    const int grp = item / (a.gcols * a.nzc);
+    const int r = item - grp * a.gcols * a.nzc;
+    const int gsize = min(a.gcols, a.ncols - grp * a.gcols);
+    const int zi = r / gsize;
+    int col = grp * a.gcols + (r - zi * gsize);
     const int tx = col % a.ntx; col /= a.ntx;
     const int ty = col % a.nty;
     t.b = col / a.nty;

@@ -1,1 +1,2 @@
-for v in 0 1; do for zc in 24 32 48 64 128; do echo "== VARIANT=$v ZCHUNK=$zc"; JAC_VARIANT=$v JAC_ZCHUNK=$zc ITERS=40 ODFS=1,8,16,64 timeout 200 python tools/quick_perf.py 2>&1; done; done > gpurun_out/qp_matrix3.log
+timeout 300 python -m pytest tests/test_parity_gpu.py -q -x > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$? >> gpurun_out/pytest_gpu.log
+for gc in 0 100000 444 296 592; do echo "== GCOLS=$gc"; if [ $gc = 0 ]; then ITERS=40 timeout 200 python tools/quick_perf.py 2>&1; else JAC_GCOLS=$gc ITERS=40 timeout 200 python tools/quick_perf.py 2>&1; fi; done > gpurun_out/qp_gcols.log
