@@ -137,3 +137,14 @@ def test_null_safety():
     out = ctypes.c_void_p()
     assert L.jac_create(8, 8, 8, 1, 1, 1, 1, None, 0, None) == J.JAC_EINVAL
     assert L.jac_create(8, 8, 8, 1, 1, 1, 1, None, J.JAC_F_NCCL, ctypes.byref(out)) == J.JAC_EINVAL
+
+
+def test_sass_no_fma_and_tma_present():
+    """R5: the update has no a*b+c and the build uses -fmad=false, so the SASS must
+    hold no DFMA; the TMA sweep must issue UTMALDG (cp.async.bulk.tensor)."""
+    import subprocess
+    sass = subprocess.run(["cuobjdump", "-sass", J.lib_path()], capture_output=True, text=True).stdout
+    assert "DFMA" not in sass
+    funcs = sass.split("Function : ")
+    tma = [f for f in funcs if f.startswith("_ZN3jac16sweep_tma_kernel")]
+    assert len(tma) == 2 and all("UTMALDG" in f for f in tma)
