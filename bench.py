@@ -228,14 +228,15 @@ def cpu_oracle(box=(512, 512, 512), n_target=None, budget_s=15.0, steps=None, wa
 
     nx, ny, nz = box
     u0 = JI.hash_field(nx, ny, nz, seed=1)
+    cores = os.cpu_count() or 1  # torchrun exports OMP_NUM_THREADS=1; the baseline uses every core
     if steps is None:
-        _, _, t1 = oracle.jacobi3d_omp_timed(u0, 1)
+        _, _, t1 = oracle.jacobi3d_omp_timed(u0, 1, cores)
         n = max(2, min(n_target or 100, int(budget_s / max(t1, 1e-6))))
     else:
         if warmup:
-            oracle.jacobi3d_omp_timed(u0, warmup)
+            oracle.jacobi3d_omp_timed(u0, warmup, cores)
         n = steps
-    _, threads, secs = oracle.jacobi3d_omp_timed(u0, n)
+    _, threads, secs = oracle.jacobi3d_omp_timed(u0, n, cores)
     glups = nx * ny * nz * n / secs / 1e9
     return {"value": glups, "unit": "GLUP/s", "cores": threads, "kind": "oracle",
             "sample": f"{nx}x{ny}x{nz} grid (the per-GPU C2 box), {n} iterations, OpenMP over z on {threads} "

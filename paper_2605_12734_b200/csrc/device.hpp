@@ -7,11 +7,26 @@
 // i in [-1,ex], j in [-1,ey], k in [-1,ez] (-1 and e* are ghosts), lives at
 //     base + (k+1)*Q + (j+1)*P + A + i,      Q = P*(ey+2)
 // with A = 4 so the interior row starts on a 32-byte sector (and 16-byte aligned
-// double2 accesses), P = round_up(A+ex+2, 4).  All slots of one GPU sit in one
-// arena: slot s of buffer b starts at arena + (b*nslots + s)*bstride, which lets ONE
-// 4-D TMA tensor map {P, ey+2, ez+2, 2*nslots} cover every block of the GPU.
+// double2 accesses).  All slots of one GPU sit in one arena: slot s of buffer b
+// starts at arena + (b*nslots + s)*bstride, which lets ONE 4-D TMA tensor map
+// {P, ey+2, ez+2, 2*nslots} cover every block of the GPU.
+//
+// x-face ghosts do NOT live in the rows (one strided double per row would cost a
+// whole 32-byte sector per row on both the write and the read side).  Each block
+// owns, per buffer, two contiguous x-ghost arrays XG[side] of ez x eyp doubles,
+// element (j, k) at xg + k*eyp + j: side 0 = the ghost column i = -1, side 1 =
+// i = ex.  Senders store them as 128-byte runs (16 rows of a tile), receivers stage
+// them with one bulk copy per plane.  XG(buf, slot, side) =
+//     xg + ((buf*nslots + slot)*2 + side)*xgstride.
+// The y- and z-face ghosts stay in place (whole rows / planes, coalesced).
 #pragma once
 #include <cstdint>
+
+#ifdef __CUDACC__
+#define JAC_HD __host__ __device__
+#else
+#define JAC_HD
+#endif
 
 namespace jac {
 
@@ -19,13 +34,16 @@ enum Face { XM = 0, XP = 1, YM = 2, YP = 3, ZM = 4, ZP = 5 };
 inline constexpr int opposite(int f) { return f ^ 1; }
 
 constexpr int kA = 4;        // x offset of interior column 0 inside a row
-constexpr int kMaxParts = 1024;
+constexpr int kXgPad = 32;   // doubles of slack after each x-ghost array (bulk-copy overrun)
 
 struct DevBlock {
     int32_t slot;            // own slot in this GPU's arena
     int32_t org[3];          // global interior origin of the block (x, y, z)
-    double *nb[6][2];        // neighbour block array base for buffer 0/1, local or
-                             // peer-mapped (IPC); nullptr = global boundary face
+    double *nb[6][2];        // per face and buffer, where this block's boundary layer
+                             // goes: y/z faces -> the neighbour block's array base;
+                             // x faces -> the neighbour's x-ghost array (side
+                             // opposite to f).  Local or peer-mapped (IPC); nullptr =
+                             // global boundary face.
     const double *nb_out[6]; // neighbour's outbox region for the face opposite to f
                              // (JAC_F_UNFUSED_PACK only)
 };
@@ -36,7 +54,8 @@ struct Geom {
     int64_t P, Q;            // row / plane pitch in doubles
     int64_t bstride;         // doubles between consecutive slots (256-byte multiple)
     int32_t nslots;          // slots per buffer in the arena
-    int32_t pad_;
+    int32_t eyp;             // x-ghost array row pitch (ey rounded up to 4)
+    int64_t xgstride;        // doubles per x-ghost array (incl. kXgPad, 256-byte multiple)
     int64_t ostride;         // outbox doubles per slot
     int64_t ooff[6];         // outbox face offsets inside a slot
 };
@@ -47,6 +66,7 @@ struct SweepArgs {
     Geom g;
     const DevBlock *blocks;  // [nslots]
     double *arena;
+    double *xg;              // x-ghost arrays
     double *outbox;
     int32_t src;             // buffer read (0/1); the sweep writes 1-src
     int32_t mode;            // SweepMode
@@ -58,6 +78,11 @@ struct SweepArgs {
     // z-chunk zi of a column covers planes [zi*ez/nzc, (zi+1)*ez/nzc).
     int32_t nzc, ncols, nitems, gcols;
 };
+
+JAC_HD inline double *xg_array(double *xg, const Geom &g, int buf, int slot, int side)
+{
+    return xg + ((int64_t)(buf * g.nslots + slot) * 2 + side) * g.xgstride;
+}
 
 // Neighbour barrier between ranks (one process per GPU): one flag word per sender
 // in the receiver's control block, monotonically increasing epochs.

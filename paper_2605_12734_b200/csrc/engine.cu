@@ -50,15 +50,16 @@ int fail(int code, const char *fmt, ...)
                         #call, cudaGetErrorString(e_), __FILE__, __LINE__);                  \
     } while (0)
 
-constexpr uint32_t kIpcMagic = 0x4A414333u;  // "JAC3"
+constexpr uint32_t kIpcMagic = 0x4A414334u;  // "JAC4"
+constexpr int kPlain = 2;  // variant id of the JAC_F_NO_TMA sweep
 
 struct IpcRecord {
     uint32_t magic;
     int32_t rank;
     uint64_t fingerprint;
-    uint64_t arena_off, outbox_off, ctrl_off;
+    uint64_t arena_off, outbox_off, ctrl_off, xg_off;
     cudaIpcMemHandle_t handle;
-    unsigned char pad_[256 - 40 - sizeof(cudaIpcMemHandle_t)];
+    unsigned char pad_[256 - 48 - sizeof(cudaIpcMemHandle_t)];
 };
 static_assert(sizeof(IpcRecord) == 256, "IPC record size");
 
@@ -81,13 +82,13 @@ struct jac_ctx {
 
     jac::Geom geom{};
     char *alloc = nullptr;    // single allocation: [ctrl][arena][outbox]
-    size_t alloc_bytes = 0, ctrl_off = 0, arena_off = 0, outbox_off = 0;
+    size_t alloc_bytes = 0, ctrl_off = 0, arena_off = 0, xg_off = 0, outbox_off = 0;
     uint64_t *ctrl = nullptr;
-    double *arena = nullptr, *outbox = nullptr;
+    double *arena = nullptr, *xg = nullptr, *outbox = nullptr;
     std::vector<jac::DevBlock> hblocks;
     jac::DevBlock *dblocks = nullptr;
 
-    int variant = 0;          // 0 TMA wide, 1 TMA narrow, 2 plain
+    int variant = 0;          // jac::TmaVariant, or kPlain
     CUtensorMap tmap{};
     int ntx = 1, nty = 1, ntz = 1, zc = 1;
     int nzc = 1, ncols = 1, nitems = 1, gcols = 1;
@@ -133,6 +134,7 @@ uint64_t fingerprint(const jac_ctx *c)
     auto mix = [&](uint64_t v) { h = (h ^ v) * 1099511628211ull; };
     for (int d = 0; d < 3; ++d) { mix(c->plan.n[d]); mix(c->plan.b[d]); mix(c->plan.g[d]); }
     mix(c->plan.n_gpus); mix(c->flags & (JAC_F_UNFUSED_PACK)); mix(c->geom.bstride); mix(c->geom.ostride);
+    mix(c->geom.xgstride);
     return h;
 }
 
@@ -142,6 +144,7 @@ jac::SweepArgs sweep_args(const jac_ctx *c, int src, int mode)
     a.g = c->geom;
     a.blocks = c->dblocks;
     a.arena = c->arena;
+    a.xg = c->xg;
     a.outbox = c->outbox;
     a.src = src;
     a.mode = mode;
@@ -160,7 +163,7 @@ int sweep_mode(const jac_ctx *c)
 int enqueue_sweep(jac_ctx *c, int src)
 {
     const jac::SweepArgs a = sweep_args(c, src, sweep_mode(c));
-    if (c->variant == 2) CK(jac::launch_sweep_plain(a, c->stream));
+    if (c->variant == kPlain) CK(jac::launch_sweep_plain(a, c->stream));
     else CK(jac::launch_sweep_tma(c->tmap, a, c->variant, c->stream));
     return JAC_OK;
 }
@@ -176,9 +179,10 @@ int enqueue_barrier(jac_ctx *c)
 int enqueue_iteration(jac_ctx *c, int src, cudaEvent_t evs = nullptr, cudaEvent_t eve = nullptr)
 {
     int rc;
-    if (evs) CK(cudaEventRecord(evs, c->stream));
+    // external event-record nodes when captured (jac_profile_sweep), so they time
+    if (evs) CK(cudaEventRecordWithFlags(evs, c->stream, cudaEventRecordExternal));
     if ((rc = enqueue_sweep(c, src))) return rc;
-    if (eve) CK(cudaEventRecord(eve, c->stream));
+    if (eve) CK(cudaEventRecordWithFlags(eve, c->stream, cudaEventRecordExternal));
     if ((rc = enqueue_barrier(c))) return rc;
     if ((c->flags & JAC_F_UNFUSED_PACK) && !(c->flags & JAC_F_SKIP_EXCHANGE)) {
         CK(jac::launch_ghost_fill(sweep_args(c, src, jac::MODE_PACK), 1 - src, c->stream));
@@ -218,7 +222,7 @@ int encode_tmap(jac_ctx *c)
     const cuuint64_t dims[4] = {(cuuint64_t)g.P, (cuuint64_t)(g.ey + 2), (cuuint64_t)(g.ez + 2),
                                 (cuuint64_t)(2 * c->nslots)};
     const cuuint64_t strides[3] = {(cuuint64_t)g.P * 8, (cuuint64_t)g.Q * 8, (cuuint64_t)g.bstride * 8};
-    const cuuint32_t box[4] = {(cuuint32_t)(ts.bx + 4), (cuuint32_t)(ts.by + 2), 1, 1};
+    const cuuint32_t box[4] = {(cuuint32_t)ts.w, (cuuint32_t)(ts.by + 2), 1, 1};
     const cuuint32_t estr[4] = {1, 1, 1, 1};
     CUresult r = encode(&c->tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, c->arena, dims, strides, box, estr,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -227,14 +231,20 @@ int encode_tmap(jac_ctx *c)
     return JAC_OK;
 }
 
-// Pointer of block (global coords nb) in buffer `buf` as seen from this context.
-double *block_ptr_local(const jac_ctx *c, const int32_t nb[3], int buf)
+// Where the boundary layer of face f goes, for a neighbour block (global coords nb)
+// hosted by this context, in buffer `buf`: its array base (y/z faces) or its x-ghost
+// array on the side facing us (x faces).
+double *block_ptr_local(const jac_ctx *c, const int32_t nb[3], int buf, int f)
 {
     const jac::Plan &p = c->plan;
     const int32_t part = p.owner(nb[0], nb[1], nb[2]);
     const int32_t ls = p.local_slot(nb[0], nb[1], nb[2]);
     for (size_t h = 0; h < c->parts.size(); ++h)
-        if (c->parts[h] == part) return c->slot_ptr(buf, (int)h * p.blocks_per_part() + ls);
+        if (c->parts[h] == part) {
+            const int slot = (int)h * p.blocks_per_part() + ls;
+            if ((f >> 1) == 0) return jac::xg_array(c->xg, c->geom, buf, slot, jac::opposite(f) & 1);
+            return c->slot_ptr(buf, slot);
+        }
     return nullptr;
 }
 
@@ -284,6 +294,8 @@ int create_common(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, in
     g.Q = g.P * (g.ey + 2);
     g.bstride = round_up(g.Q * (g.ez + 2), 32);
     g.nslots = c->nslots;
+    g.eyp = (int32_t)round_up(g.ey, 4);
+    g.xgstride = round_up((int64_t)g.eyp * g.ez + jac::kXgPad, 32);
     const int64_t fx = (int64_t)g.ey * g.ez, fy = (int64_t)g.ex * g.ez, fz = (int64_t)g.ex * g.ey;
     int64_t o = 0;
     const int64_t fsz[6] = {fx, fx, fy, fy, fz, fz};
@@ -291,11 +303,16 @@ int create_common(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, in
     g.ostride = (flags & JAC_F_UNFUSED_PACK) ? round_up(o, 32) : 0;
 
     // tile shape / variant
-    if (flags & JAC_F_NO_TMA) c->variant = 2;
-    else c->variant = (g.ex <= 32) ? jac::TMA_NARROW : jac::TMA_WIDE;
-    if (const char *s = getenv("JAC_VARIANT"); s && c->variant != 2) c->variant = atoi(s) ? jac::TMA_NARROW : jac::TMA_WIDE;
-    const int tbx = (c->variant == 2) ? 64 : jac::tma_tile_shape(c->variant).bx;
-    const int tby = (c->variant == 2) ? 8 : jac::tma_tile_shape(c->variant).by;
+    if (flags & JAC_F_NO_TMA) c->variant = kPlain;
+    else c->variant = (g.ex <= 32) ? jac::TMA_EXACT32 : (g.ex <= 64) ? jac::TMA_EXACT64 : jac::TMA_WIDE;
+    if (const char *s = getenv("JAC_VARIANT"); s && c->variant != kPlain) {
+        const int v = atoi(s);  // tuning knob; EXACT* only where one tile spans the block row
+        if (v == jac::TMA_WIDE || v == jac::TMA_NARROW || (v == jac::TMA_EXACT32 && g.ex <= 32) ||
+            (v == jac::TMA_EXACT64 && g.ex <= 64))
+            c->variant = v;
+    }
+    const int tbx = (c->variant == kPlain) ? 64 : jac::tma_tile_shape(c->variant).bx;
+    const int tby = (c->variant == kPlain) ? 8 : jac::tma_tile_shape(c->variant).by;
     c->ntx = (g.ex + tbx - 1) / tbx;
     c->nty = (g.ey + tby - 1) / tby;
     // z-chunk: enough CTAs for several waves on 148 SMs, chunks of >= 16 planes
@@ -319,7 +336,7 @@ int create_common(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, in
         // Column groups of ~one resident wave: inside a group the chunk k+1 item of a
         // column launches about when its chunk k item retires, so the two planes they
         // share are still in L2.
-        int gcols = c->variant == 2 ? c->ncols : jac::sweep_resident_ctas(c->variant);
+        int gcols = c->variant == kPlain ? c->ncols : jac::sweep_resident_ctas(c->variant);
         if (const char *s = getenv("JAC_GCOLS")) gcols = atoi(s);
         c->gcols = std::max(1, std::min(c->ncols, gcols > 0 ? gcols : c->ncols));
     }
@@ -329,11 +346,13 @@ int create_common(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, in
         return fail(JAC_EINVAL, "too many tiles for one launch");
     }
 
-    // allocation: [ctrl 64 KiB][arena][outbox]
+    // allocation: [ctrl 64 KiB][arena][x-ghost arrays][outbox]
     c->ctrl_off = 0;
     c->arena_off = 65536;
     const size_t arena_bytes = (size_t)2 * c->nslots * g.bstride * sizeof(double);
-    c->outbox_off = c->arena_off + arena_bytes;
+    c->xg_off = c->arena_off + arena_bytes;
+    const size_t xg_bytes = (size_t)2 * c->nslots * 2 * g.xgstride * sizeof(double);
+    c->outbox_off = c->xg_off + xg_bytes;
     const size_t outbox_bytes = (size_t)c->nslots * g.ostride * sizeof(double);
     c->alloc_bytes = c->outbox_off + outbox_bytes;
     e = cudaMalloc(&c->alloc, c->alloc_bytes);
@@ -343,6 +362,7 @@ int create_common(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, in
     }
     c->ctrl = reinterpret_cast<uint64_t *>(c->alloc + c->ctrl_off);
     c->arena = reinterpret_cast<double *>(c->alloc + c->arena_off);
+    c->xg = reinterpret_cast<double *>(c->alloc + c->xg_off);
     c->outbox = outbox_bytes ? reinterpret_cast<double *>(c->alloc + c->outbox_off) : nullptr;
     auto bail = [&](int code) { jac_destroy(c); return code; };
     if (cudaMemset(c->alloc, 0, c->alloc_bytes) != cudaSuccess) return bail(fail(JAC_ECUDA, "cudaMemset arena"));
@@ -367,8 +387,8 @@ int create_common(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, in
             else c->remote_faces++;
             if (!same_part) c->remote_bytes += 8 * ((f >> 1) == 0 ? fx : (f >> 1) == 1 ? fy : fz);
             if (local) {
-                d.nb[f][0] = block_ptr_local(c, nb, 0);
-                d.nb[f][1] = block_ptr_local(c, nb, 1);
+                d.nb[f][0] = block_ptr_local(c, nb, 0, f);
+                d.nb[f][1] = block_ptr_local(c, nb, 1, f);
                 if (c->outbox) {
                     int32_t h = (int32_t)(std::find(c->parts.begin(), c->parts.end(), owner) - c->parts.begin());
                     const int32_t ns = h * bpp + plan.local_slot(nb[0], nb[1], nb[2]);
@@ -384,7 +404,7 @@ int create_common(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, in
         return bail(fail(JAC_ENOMEM, "cudaMalloc descriptor table"));
     if (cudaMemcpy(c->dblocks, c->hblocks.data(), sizeof(jac::DevBlock) * c->nslots, cudaMemcpyHostToDevice) != cudaSuccess)
         return bail(fail(JAC_ECUDA, "descriptor table upload"));
-    if (c->variant != 2) {
+    if (c->variant != kPlain) {
         if ((rc = encode_tmap(c))) return bail(rc);
         if (jac::prepare_sweep_tma(c->variant) != cudaSuccess) return bail(fail(JAC_ECUDA, "sweep kernel attribute"));
     }
@@ -505,6 +525,7 @@ int jac_export_ipc(jac_ctx *c, void *out)
     r.arena_off = c->arena_off;
     r.outbox_off = c->outbox_off;
     r.ctrl_off = c->ctrl_off;
+    r.xg_off = c->xg_off;
     CK(cudaIpcGetMemHandle(&r.handle, c->alloc));
     memcpy(out, &r, sizeof r);
     return JAC_OK;
@@ -541,8 +562,10 @@ int jac_import_ipc(jac_ctx *c, const void *all)
             if (q == c->rank) continue;
             const int32_t ns = p.local_slot(nb[0], nb[1], nb[2]);
             double *arena = reinterpret_cast<double *>(base[q] + recs[q].arena_off);
-            c->hblocks[s].nb[f][0] = arena + (int64_t)ns * g.bstride;
-            c->hblocks[s].nb[f][1] = arena + (int64_t)(bpp + ns) * g.bstride;
+            double *xg = reinterpret_cast<double *>(base[q] + recs[q].xg_off);
+            for (int buf = 0; buf < 2; ++buf)
+                c->hblocks[s].nb[f][buf] = (f >> 1) == 0 ? jac::xg_array(xg, g, buf, ns, jac::opposite(f) & 1)
+                                                         : arena + (int64_t)(buf * bpp + ns) * g.bstride;
             if (c->outbox) {
                 const double *ob = reinterpret_cast<const double *>(base[q] + recs[q].outbox_off);
                 c->hblocks[s].nb_out[f] = ob + (int64_t)ns * g.ostride + g.ooff[jac::opposite(f)];
@@ -611,6 +634,7 @@ int jac_set_init_box(jac_ctx *c, const double *box, const int64_t *origin, const
     }
     CK(cudaMemcpyAsync(c->slot_ptr(1, 0), c->slot_ptr(0, 0), (size_t)c->nslots * g.bstride * 8,
                        cudaMemcpyDeviceToDevice, c->stream));
+    CK(jac::launch_xghost_extract(sweep_args(c, 0, 0), c->stream));
     return finish_init(c);
 }
 
@@ -630,6 +654,7 @@ int jac_set_init_hash(jac_ctx *c, uint64_t seed)
     CK(cudaSetDevice(c->device));
     if ((rc = enqueue_barrier(c))) return rc;
     CK(jac::launch_hash_init(sweep_args(c, 0, 0), c->plan.n[0], c->plan.n[1], seed, c->stream));
+    CK(jac::launch_xghost_extract(sweep_args(c, 0, 0), c->stream));
     return finish_init(c);
 }
 
@@ -687,9 +712,24 @@ int jac_profile_sweep(jac_ctx *c, int32_t n, double *avg_ms)
     std::vector<cudaEvent_t> ev(2 * (size_t)n);
     for (auto &e : ev) CK(cudaEventCreate(&e));
     int src = (int)(c->iters & 1);
-    for (int it = 0; it < n; ++it, src ^= 1)
-        if ((rc = enqueue_iteration(c, src, ev[2 * it], ev[2 * it + 1]))) return rc;
-    CK(cudaStreamSynchronize(c->stream));
+    // The n iterations are captured into one graph with event-record nodes around
+    // every sweep launch, so the sweep is timed exactly as jac_step runs it.
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    rc = JAC_OK;
+    for (int it = 0; it < n && rc == JAC_OK; ++it, src ^= 1)
+        rc = enqueue_iteration(c, src, ev[2 * it], ev[2 * it + 1]);
+    cudaError_t e = cudaStreamEndCapture(c->stream, &graph);
+    if (rc) { if (graph) cudaGraphDestroy(graph); return rc; }
+    if (e != cudaSuccess) return fail(JAC_ECUDA, "profile graph capture: %s", cudaGetErrorString(e));
+    e = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) return fail(JAC_ECUDA, "profile graph instantiate: %s", cudaGetErrorString(e));
+    e = cudaGraphLaunch(exec, c->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    cudaGraphExecDestroy(exec);
+    if (e != cudaSuccess) return fail(JAC_ECUDA, "profile graph: %s", cudaGetErrorString(e));
     double tot = 0;
     for (int it = 0; it < n; ++it) {
         float ms = 0;
@@ -718,7 +758,19 @@ int jac_get_block_padded(jac_ctx *c, int32_t ix, int32_t iy, int32_t iz, double 
     m.extent = make_cudaExtent((size_t)(g.ex + 2) * 8, (size_t)(g.ey + 2), (size_t)(g.ez + 2));
     m.kind = cudaMemcpyDeviceToHost;
     CK(cudaMemcpy3DAsync(&m, c->stream));
+    // the x ghosts live in the x-ghost arrays: patch columns 0 and ex+1 (interior j, k)
+    std::vector<double> xgh((size_t)2 * g.ez * g.eyp);
+    const int cur = (int)(c->iters & 1);
+    for (int side = 0; side < 2; ++side)
+        CK(cudaMemcpyAsync(xgh.data() + (size_t)side * g.ez * g.eyp, jac::xg_array(c->xg, g, cur, s, side),
+                           (size_t)g.ez * g.eyp * 8, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
+    const int64_t sx = g.ex + 2, sxy = sx * (g.ey + 2);
+    for (int64_t k = 0; k < g.ez; ++k)
+        for (int64_t j = 0; j < g.ey; ++j) {
+            out[(k + 1) * sxy + (j + 1) * sx] = xgh[k * g.eyp + j];
+            out[(k + 1) * sxy + (j + 1) * sx + g.ex + 1] = xgh[(size_t)g.ez * g.eyp + k * g.eyp + j];
+        }
     return JAC_OK;
 }
 
@@ -812,7 +864,7 @@ int jac_get_stats(const jac_ctx *c, int64_t *st)
     st[JAC_STAT_REMOTE_FACES] = c->remote_faces;
     st[JAC_STAT_REMOTE_BYTES] = c->remote_bytes;
     st[JAC_STAT_ARENA_BYTES] = (int64_t)(2 * (size_t)c->nslots * c->geom.bstride * 8);
-    st[JAC_STAT_SWEEP_VARIANT] = c->variant == 2 ? 1 : 0;
+    st[JAC_STAT_SWEEP_VARIANT] = c->variant;
     return JAC_OK;
 }
 

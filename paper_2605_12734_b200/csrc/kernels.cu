@@ -2,15 +2,16 @@
 //
 //  sweep_tma_kernel   north-star subsystem (2): ONE batched launch per GPU per
 //                     iteration walks every local block through the descriptor
-//                     table.  Each CTA owns a BX x BY column tile of one block and
-//                     marches a z-chunk; z-planes (with x/y halo) are staged into a
-//                     ring of shared-memory buffers by TMA (cp.async.bulk.tensor,
-//                     mbarrier complete_tx), the z-neighbours ride in registers.
-//                     The epilogue stores the new interior AND, for boundary layers,
-//                     the same values straight into the neighbour block's ghost
-//                     cells of the output buffer (fused pack + ghost copy; peer
-//                     blocks on other GPUs are written over NVLink through IPC
-//                     pointers), so ODF costs no extra launch and no extra pass.
+//                     table.  Each CTA owns one (block, BX x BY column tile, z-chunk)
+//                     work item and marches it in z; z-planes (with the in-block
+//                     x/y halo) are staged into a ring of shared-memory buffers by
+//                     TMA (cp.async.bulk.tensor + mbarrier complete_tx), the
+//                     block-edge x ghosts by a 1-D bulk copy into the same stage, the
+//                     z-neighbours ride in registers.  The epilogue stores the new
+//                     interior AND, for boundary layers, the same values straight into
+//                     the neighbour block's ghost cells of the output buffer (fused
+//                     pack + ghost copy; blocks on other GPUs are written over NVLink
+//                     through IPC pointers), so ODF costs no extra launch or pass.
 //  sweep_plain_kernel JAC_F_NO_TMA ablation: per-point global loads (L1/L2 reuse).
 //  ghost_fill_kernel  north-star subsystem (3) as the JAC_F_UNFUSED_PACK path: the
 //                     sweep packs faces into an outbox, this batched kernel copies
@@ -19,7 +20,7 @@
 //  barrier_kernel     cross-rank neighbour barrier on device flags (st.release.sys /
 //                     ld.acquire.sys over NVLink), replacing the paper's IPC event
 //                     pool.
-//  hash_init_kernel   R11 synthetic initial field (input generation, not the method).
+//  xghost_extract_kernel / hash_init_kernel  cold-path init helpers.
 //
 // The update (PAPER.md:281 Jacobi, 3-D lift R1; readings R2-R4 in DESIGN.md):
 //     u' = ((((((c + x-) + x+) + y-) + y+) + z-) + z+) * fl(1/7)
@@ -29,8 +30,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
-#include <cstdlib>
 #include <cstdint>
+#include <cstdlib>
 
 #include "device.hpp"
 #include "kernels.hpp"
@@ -56,67 +57,59 @@ __device__ __forceinline__ void st_pair(double *p, double2 v, bool both)
     else p[0] = v.x;
 }
 
-// Stores the new values of points (i, j, k) and (i+1, j, k) of block `blk` into
-// buffer `dst`, plus the face traffic of the chosen mode.  Caller guarantees
-// j < ey and 0 <= k < ez; i may be past the ragged x edge.
-__device__ __forceinline__ void emit_pair(const SweepArgs &a, const DevBlock &blk, int dst,
-                                          int i, int j, int k, double2 v)
+// Stores the new values of points (i, j, k) and (i+1, j, k) of block `blk` into the
+// output buffer `dst` (own_plane = the block's output array + (k+1)*Q, rowoff =
+// (j+1)*P + A + i), plus the face traffic of the chosen mode.  Caller guarantees
+// j < ey and 0 <= k < ez; i may be past the ragged x edge.  `blk` should live in
+// shared memory or registers: global stores would otherwise force the compiler to
+// re-load it after every store.
+__device__ __forceinline__ void emit_pair(const SweepArgs &a, const DevBlock &blk, int dst, double *own_plane,
+                                          int64_t rowoff, int i, int j, int k, double2 v)
 {
     const Geom &g = a.g;
     if (i >= g.ex) return;
     const bool both = (i + 1) < g.ex;
-    const int64_t row = (int64_t)(j + 1) * g.P + g.A + i;
-    const int64_t off = (int64_t)(k + 1) * g.Q + row;
-    double *own = a.arena + (int64_t)(dst * g.nslots + blk.slot) * g.bstride;
-    st_pair(own + off, v, both);
+    st_pair(own_plane + rowoff, v, both);
     if (a.mode == MODE_NOEXCHANGE) return;
+    const bool zface = (k == 0) || (k == g.ez - 1);
+    const bool yface = (j == 0) || (j == g.ey - 1);
+    const bool last_x = (i == g.ex - 1) || (both && i + 1 == g.ex - 1);
+    const bool xface = (i == 0) || last_x;
+    if (!(zface || yface || xface)) return;  // interior point: done
+    const double last_v = (i == g.ex - 1) ? v.x : v.y;
+    const int64_t xgi = (int64_t)k * g.eyp + j;
     if (a.mode == MODE_FUSED) {
         // direct-to-ghost: the neighbour's ghost layer of the OUTPUT buffer is not
         // read by anyone during this sweep, so writing it here is race-free.
-        if (k == 0) {
-            double *p = blk.nb[ZM][dst];
-            if (p) st_pair(p + (int64_t)(g.ez + 1) * g.Q + row, v, both);
+        if (zface) {
+            if (k == 0) {
+                double *p = blk.nb[ZM][dst];
+                if (p) st_pair(p + (int64_t)(g.ez + 1) * g.Q + rowoff, v, both);
+            }
+            if (k == g.ez - 1) {
+                double *p = blk.nb[ZP][dst];
+                if (p) st_pair(p + rowoff, v, both);
+            }
         }
-        if (k == g.ez - 1) {
-            double *p = blk.nb[ZP][dst];
-            if (p) st_pair(p + row, v, both);
+        if (yface) {
+            if (j == 0) {
+                double *p = blk.nb[YM][dst];
+                if (p) st_pair(p + (int64_t)(k + 1) * g.Q + (int64_t)(g.ey + 1) * g.P + g.A + i, v, both);
+            }
+            if (j == g.ey - 1) {
+                double *p = blk.nb[YP][dst];
+                if (p) st_pair(p + (int64_t)(k + 1) * g.Q + g.A + i, v, both);
+            }
         }
-        if (j == 0) {
-            double *p = blk.nb[YM][dst];
-            if (p) st_pair(p + (int64_t)(k + 1) * g.Q + (int64_t)(g.ey + 1) * g.P + g.A + i, v, both);
-        }
-        if (j == g.ey - 1) {
-            double *p = blk.nb[YP][dst];
-            if (p) st_pair(p + (int64_t)(k + 1) * g.Q + g.A + i, v, both);
-        }
-        // x-faces: the ghost column is strided (one value per row).  Write the
-        // whole 32-byte sector holding it (the rest is row padding) so L2 never
-        // has to fetch a partially written sector from DRAM.
+        // x faces: into the neighbour's contiguous x-ghost array; the 16 rows of a
+        // tile write one 128-byte run per plane (merged in L2 into full sectors).
         if (i == 0) {
             double *p = blk.nb[XM][dst];
-            if (p) {
-                double *q = p + (off - i + g.ex);  // neighbour's ghost column i = ex (col A+ex)
-                if (((g.A + g.ex) & 3) == 0) {  // ghost alone in its sector
-                    *reinterpret_cast<double2 *>(q) = make_double2(v.x, 0.0);
-                    *reinterpret_cast<double2 *>(q + 2) = make_double2(0.0, 0.0);
-                } else {
-                    *q = v.x;
-                }
-            }
+            if (p) p[xgi] = v.x;
         }
-        const bool last_x = (i == g.ex - 1) || (both && i + 1 == g.ex - 1);
         if (last_x) {
             double *p = blk.nb[XP][dst];
-            if (p) {
-                const double val = (i == g.ex - 1) ? v.x : v.y;
-                double *q = p + (off - i - 1);     // neighbour's ghost column i = -1 (col A-1)
-                if ((g.A & 3) == 0) {                // ghost is the last word of its sector
-                    *reinterpret_cast<double2 *>(q - 3) = make_double2(0.0, 0.0);
-                    *reinterpret_cast<double2 *>(q - 1) = make_double2(0.0, val);
-                } else {
-                    *q = val;
-                }
-            }
+            if (p) p[xgi] = last_v;
         }
     } else {  // MODE_PACK: contiguous outbox faces, layouts x:[k][j] y:[k][i] z:[j][i]
         double *ob = a.outbox + (int64_t)blk.slot * g.ostride;
@@ -137,9 +130,7 @@ __device__ __forceinline__ void emit_pair(const SweepArgs &a, const DevBlock &bl
             p[0] = v.x; if (both) p[1] = v.y;
         }
         if (i == 0 && blk.nb[XM][0]) ob[g.ooff[XM] + (int64_t)k * g.ey + j] = v.x;
-        if (i == g.ex - 1 && blk.nb[XP][0]) ob[g.ooff[XP] + (int64_t)k * g.ey + j] = v.x;
-        else if (both && i + 1 == g.ex - 1 && blk.nb[XP][0])
-            ob[g.ooff[XP] + (int64_t)k * g.ey + j] = v.y;
+        if (last_x && blk.nb[XP][0]) ob[g.ooff[XP] + (int64_t)k * g.ey + j] = last_v;
     }
 }
 
@@ -193,23 +184,44 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
         if (globaltimer_ns() - t0 > kSpinLimitNs) __trap();
 }
 
-__device__ __forceinline__ void tma_plane(const CUtensorMap *tm, double *dst, uint64_t *bar,
-                                          uint32_t bytes, int c0, int c1, int c2, int c3)
+__device__ __forceinline__ void mbar_expect(uint64_t *bar, uint32_t bytes)
 {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-                 "r"(bytes)
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                  : "memory");
+}
+
+__device__ __forceinline__ void tma_box(const CUtensorMap *tm, double *dst, uint64_t *bar, int c0, int c1,
+                                        int c2, int c3)
+{
     asm volatile(
         "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
         " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(c2), "r"(c3),
-        "r"(smem_u32(bar))
+        "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
         : "memory");
 }
 
-constexpr size_t tma_smem_bytes(int BX, int BY, int NS)
+__device__ __forceinline__ void bulk_copy(double *dst, const double *src, uint32_t bytes, uint64_t *bar)
 {
-    return (size_t)NS * (((BX + 4) * (BY + 2) + 15) / 16 * 16) * sizeof(double) + NS * sizeof(uint64_t);
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// Ring stage: the W x (BY+2) staged plane, then 2 x BY x-ghost values (side 0, 1).
+template <int BX, int BY, int W>
+struct StageLayout {
+    static constexpr int H = BY + 2;
+    static constexpr uint32_t BOX_BYTES = W * H * sizeof(double);
+    static constexpr int XG_OFF = W * H;  // doubles; 16-byte aligned since W*H is even
+    static constexpr uint32_t XG_BYTES = BY * sizeof(double);
+    static constexpr int STRIDE = ((W * H + 2 * BY) + 15) / 16 * 16;  // 128-byte aligned stages
+};
+
+constexpr size_t tma_smem_bytes(int BX, int BY, int W, int NS)
+{
+    return (size_t)NS * (((W * (BY + 2) + 2 * BY) + 15) / 16 * 16) * sizeof(double) + NS * sizeof(uint64_t);
 }
 
 struct TileItem {
@@ -235,134 +247,135 @@ __device__ __forceinline__ TileItem decode_item(const SweepArgs &a, int item)
     return t;
 }
 
-// Producer state (thread 0 only): walks this CTA's items and their planes in order,
-// keeping up to NS plane loads in flight across item boundaries.
-template <int BX, int BY, int NS>
-struct Producer {
-    int item;    // current item index (global)
-    int p;       // plane offset within the item's load sequence (0 .. ze-zs+1)
-    uint32_t l;  // loads issued so far
-    TileItem t;
-    int c3;
-
-    __device__ __forceinline__ void start(const SweepArgs &a)
-    {
-        item = blockIdx.x;
-        p = 0;
-        l = 0;
-        if (item < a.nitems) {
-            t = decode_item<BX, BY>(a, item);
-            c3 = a.src * a.g.nslots + a.blocks[t.b].slot;
-        }
-    }
-    __device__ __forceinline__ void issue(const SweepArgs &a, const CUtensorMap *tm, double *stage,
-                                          uint64_t *bars, int stage_doubles, uint32_t bytes)
-    {
-        if (item >= a.nitems) return;
-        const int s = (int)(l % NS);
-        // plane k = zs - 1 + p  ->  tensor z index k + 1 = zs + p
-        tma_plane(tm, stage + s * stage_doubles, &bars[s], bytes, a.g.A - 2 + t.x0, t.y0, t.zs + p, c3);
-        ++l;
-        if (++p == t.ze - t.zs + 2) {
-            p = 0;
-            item += gridDim.x;
-            if (item < a.nitems) {
-                t = decode_item<BX, BY>(a, item);
-                c3 = a.src * a.g.nslots + a.blocks[t.b].slot;
-            }
-        }
-    }
-};
-
-// Persistent TMA z-march.  BX x BY column tile per work item, NT threads, NS-deep
-// plane ring.  Each thread owns a pair of x-points (double2) in RY rows; the
-// z-neighbours ride in registers, x/y neighbours come from the staged plane.
-template <int BX, int BY, int NT, int NS>
-__global__ void __launch_bounds__(NT, 4) sweep_tma_kernel(const __grid_constant__ CUtensorMap tmap,
-                                                       const SweepArgs a)
+// Staged column of the tile's first point i = x0.  Interior tiles stage x0-2 ..
+// x0+BX+1 (soff = 2).  The box never reads the inline x-ghost sectors (x ghosts come
+// from the x-ghost arrays): the first tile starts at the interior (soff = 0) and the
+// last tile is pulled back by two columns (soff = 4) so a full last tile ends exactly
+// at the interior's end.  W == BX (single-tile blocks) stages the interior only.
+template <int BX, int W>
+__device__ __forceinline__ int tile_soff(const Geom &g, int x0)
 {
+    if (W == BX || x0 == 0) return 0;
+    return (x0 + BX >= g.ex) ? 4 : 2;
+}
+
+// Persistent-free TMA z-march: one CTA per work item.  BX x BY column tile, NT
+// threads, NS-deep plane ring, staged width W (BX + 4 with in-block x halo, or BX
+// for single-tile blocks).  Each thread owns a pair of x-points (double2) in RY rows.
+template <int BX, int BY, int W, int NT, int NS>
+__global__ void __launch_bounds__(NT, 4) sweep_tma_kernel(const __grid_constant__ CUtensorMap tmap,
+                                                          const SweepArgs a)
+{
+    using L = StageLayout<BX, BY, W>;
     constexpr int TXL = BX / 2;    // threads along x
     constexpr int NRG = NT / TXL;  // row groups
     constexpr int RY = BY / NRG;   // rows per thread
     static_assert(RY >= 1 && RY * NRG == BY, "tile shape");
-    constexpr int W = BX + 4;      // staged width: x0-2 .. x0+BX+1
-    constexpr int H = BY + 2;      // staged height: y0-1 .. y0+BY
-    constexpr uint32_t STAGE_BYTES = W * H * sizeof(double);  // TMA transaction bytes
-    constexpr int STAGE = (W * H + 15) / 16 * 16;  // ring stride: TMA needs 128-byte aligned smem
+    static_assert(W == BX || W == BX + 4, "staged width");
     static_assert(NS >= 3, "ring must hold planes k, k+1 and prefetch");
 
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double *stage = reinterpret_cast<double *>(smem_raw);
-    uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + NS * STAGE * sizeof(double));
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + NS * L::STRIDE * sizeof(double));
 
     const Geom &g = a.g;
-    __shared__ Producer<BX, BY, NS> prod;  // touched by thread 0 only; kept out of registers
+    const TileItem t = decode_item<BX, BY>(a, blockIdx.x);
+    __shared__ DevBlock blk;  // this item's descriptor, read once from the table
+    if (threadIdx.x == 0) blk = a.blocks[t.b];
+    const int soff = tile_soff<BX, W>(g, t.x0);  // staged column of point i = x0 (0, 2 or 4)
+    const int c0 = g.A + t.x0 - soff;
+    const bool xlo = (t.x0 == 0);                 // tile touches the x- block face
+    const bool xhi = (t.x0 + BX >= g.ex);         // tile touches the x+ block face
+    const int nq = t.ze - t.zs + 2;               // planes zs-1 .. ze
+    // producer-only state (thread 0): source block coordinates for TMA / bulk copies
+    int c3 = 0;
+    const double *xg0 = nullptr, *xg1 = nullptr;
+
+    // plane q of the item = interior plane k = zs - 1 + q; x-ghosts only for k in [zs, ze)
+    auto issue = [&](int q) {
+        double *st = stage + (q % NS) * L::STRIDE;
+        uint64_t *bar = &bars[q % NS];
+        const bool mid = (q >= 1) && (q <= nq - 2);
+        const uint32_t bytes = L::BOX_BYTES + (mid ? ((xlo ? L::XG_BYTES : 0) + (xhi ? L::XG_BYTES : 0)) : 0);
+        mbar_expect(bar, bytes);
+        tma_box(&tmap, st, bar, c0, t.y0, t.zs + q, c3);
+        if (mid) {
+            const int64_t ko = (int64_t)(t.zs - 1 + q) * g.eyp;
+            if (xlo) bulk_copy(st + L::XG_OFF, xg0 + ko, L::XG_BYTES, bar);
+            if (xhi) bulk_copy(st + L::XG_OFF + BY, xg1 + ko, L::XG_BYTES, bar);
+        }
+    };
+
     if (threadIdx.x == 0) {
+        const int slot = a.blocks[t.b].slot;
+        c3 = a.src * g.nslots + slot;
+        xg0 = xg_array(a.xg, g, a.src, slot, 0) + t.y0;
+        xg1 = xg_array(a.xg, g, a.src, slot, 1) + t.y0;
         for (int s = 0; s < NS; ++s) mbar_init(&bars[s], 1);
         mbar_fence_init();
-        prod.start(a);
-        for (int s = 0; s < NS; ++s) prod.issue(a, &tmap, stage, bars, STAGE, STAGE_BYTES);
+        for (int q = 0; q < NS && q < nq; ++q) issue(q);
     }
     __syncthreads();
 
     const int lane = threadIdx.x % TXL;
     const int rg = threadIdx.x / TXL;
-    const int col = 2 * lane + 2;  // staged column of point i = x0 + 2*lane
+    const int col = soff + 2 * lane;  // staged column of point i = x0 + 2*lane
+    const int i = t.x0 + 2 * lane;
     const int dst = 1 - a.src;
-    uint32_t l = 0;                // loads consumed
-
-    // release(): every thread is done with the oldest unreleased stage -> refill it
-    auto release = [&]() {
+    const bool ilo = (i == 0);                     // element 0 is the first interior point
+    const bool ihi0 = (i == g.ex - 1);             // element 0 is the last interior point
+    const bool ihi1 = (i + 1 == g.ex - 1);         // element 1 is the last interior point
+    double *own_plane = a.arena + (int64_t)(dst * g.nslots + blk.slot) * g.bstride + (int64_t)t.zs * g.Q;
+    int64_t rowoff[RY];
+#pragma unroll
+    for (int r = 0; r < RY; ++r) rowoff[r] = (int64_t)(t.y0 + rg * RY + r + 1) * g.P + g.A + i;
+    auto plane = [&](int q) { return stage + (q % NS) * L::STRIDE; };
+    auto wait = [&](int q) { mbar_wait(&bars[q % NS], (q / NS) & 1); };
+    auto refill = [&](int q) {  // all threads are done with plane q -> load q + NS
         __syncthreads();
-        if (threadIdx.x == 0) prod.issue(a, &tmap, stage, bars, STAGE, STAGE_BYTES);
+        if (threadIdx.x == 0 && q + NS < nq) issue(q + NS);
     };
-    auto plane = [&](uint32_t li) { return stage + (li % NS) * STAGE; };
-    auto wait = [&](uint32_t li) { mbar_wait(&bars[li % NS], (li / NS) & 1); };
 
-    for (int item = blockIdx.x; item < a.nitems; item += gridDim.x) {
-        const TileItem t = decode_item<BX, BY>(a, item);
-        const DevBlock &blk = a.blocks[t.b];
-        const int i = t.x0 + 2 * lane;
-        double2 zm[RY], c[RY], zp[RY];
-        wait(l);
+    double2 zm[RY], c[RY], zp[RY];
+    wait(0);
+#pragma unroll
+    for (int r = 0; r < RY; ++r)
+        zm[r] = *reinterpret_cast<const double2 *>(plane(0) + (rg * RY + r + 1) * W + col);
+    refill(0);  // plane zs-1 only feeds zm
+    wait(1);
+#pragma unroll
+    for (int r = 0; r < RY; ++r)
+        c[r] = *reinterpret_cast<const double2 *>(plane(1) + (rg * RY + r + 1) * W + col);
+
+    // (Instantiating the loop separately for x-edge and interior tiles was measured
+    // slower than this single version: the per-lane selects are predicated loads.)
+    for (int q = 1; q <= nq - 2; ++q) {
+        const int k = t.zs - 1 + q;
+        wait(q + 1);
+        const double *Sn = plane(q + 1);
 #pragma unroll
         for (int r = 0; r < RY; ++r)
-            zm[r] = *reinterpret_cast<const double2 *>(plane(l) + (rg * RY + r + 1) * W + col);
-        release();  // plane zs-1 only feeds zm
-        ++l;
-        wait(l);
+            zp[r] = *reinterpret_cast<const double2 *>(Sn + (rg * RY + r + 1) * W + col);
+        const double *S = plane(q);
 #pragma unroll
-        for (int r = 0; r < RY; ++r)
-            c[r] = *reinterpret_cast<const double2 *>(plane(l) + (rg * RY + r + 1) * W + col);
-
-        for (int k = t.zs; k < t.ze; ++k) {
-            const double *Sn = plane(l + 1);
-            wait(l + 1);
-#pragma unroll
-            for (int r = 0; r < RY; ++r)
-                zp[r] = *reinterpret_cast<const double2 *>(Sn + (rg * RY + r + 1) * W + col);
-            const double *S = plane(l);
-#pragma unroll
-            for (int r = 0; r < RY; ++r) {
-                const int jl = rg * RY + r;
-                const double *row = S + (jl + 1) * W + col;
-                const double xm = row[-1];
-                const double xp = row[2];
-                const double2 ym = (r == 0) ? *reinterpret_cast<const double2 *>(row - W) : c[r - 1];
-                const double2 yp = (r == RY - 1) ? *reinterpret_cast<const double2 *>(row + W) : c[r + 1];
-                double2 v;
-                v.x = stencil7(c[r].x, xm, c[r].y, ym.x, yp.x, zm[r].x, zp[r].x);
-                v.y = stencil7(c[r].y, c[r].x, xp, ym.y, yp.y, zm[r].y, zp[r].y);
-                const int j = t.y0 + jl;
-                if (j < g.ey) emit_pair(a, blk, dst, i, j, k, v);
-            }
-            release();  // centre plane k is done
-            ++l;
-#pragma unroll
-            for (int r = 0; r < RY; ++r) { zm[r] = c[r]; c[r] = zp[r]; }
+        for (int r = 0; r < RY; ++r) {
+            const int jl = rg * RY + r;
+            const double *row = S + (jl + 1) * W + col;
+            const double xm = ilo ? S[L::XG_OFF + jl] : row[-1];
+            const double xp1 = ihi1 ? S[L::XG_OFF + BY + jl] : row[2];
+            const double xp0 = ihi0 ? S[L::XG_OFF + BY + jl] : c[r].y;
+            const double2 ym = (r == 0) ? *reinterpret_cast<const double2 *>(row - W) : c[r - 1];
+            const double2 yp = (r == RY - 1) ? *reinterpret_cast<const double2 *>(row + W) : c[r + 1];
+            double2 v;
+            v.x = stencil7(c[r].x, xm, xp0, ym.x, yp.x, zm[r].x, zp[r].x);
+            v.y = stencil7(c[r].y, c[r].x, xp1, ym.y, yp.y, zm[r].y, zp[r].y);
+            const int j = t.y0 + jl;
+            if (j < g.ey) emit_pair(a, blk, dst, own_plane + g.Q, rowoff[r], i, j, k, v);
         }
-        release();  // plane ze only fed zp
-        ++l;
+        own_plane += g.Q;
+        refill(q);  // centre plane k is done
+#pragma unroll
+        for (int r = 0; r < RY; ++r) { zm[r] = c[r]; c[r] = zp[r]; }
     }
 }
 
@@ -377,25 +390,31 @@ __global__ void __launch_bounds__(256) sweep_plain_kernel(const SweepArgs a)
     const int ty = t % a.nty; t /= a.nty;
     const int tz = t % a.ntz;
     const int b = t / a.ntz;
-    const DevBlock &blk = a.blocks[b];
+    const DevBlock blk = a.blocks[b];  // register copy (see emit_pair)
     const int i = tx * 64 + 2 * (threadIdx.x & 31);
     const int j = ty * 8 + (threadIdx.x >> 5);
     if (i >= g.ex || j >= g.ey) return;
     const int z0 = tz * a.zc, z1 = min(g.ez, z0 + a.zc);
     const double *s = a.arena + (int64_t)(a.src * g.nslots + blk.slot) * g.bstride;
+    const double *xg0 = xg_array(a.xg, g, a.src, blk.slot, 0);
+    const double *xg1 = xg_array(a.xg, g, a.src, blk.slot, 1);
     const int dst = 1 - a.src;
+    double *own = a.arena + (int64_t)(dst * g.nslots + blk.slot) * g.bstride;
     for (int k = z0; k < z1; ++k) {
         const int64_t o = (int64_t)(k + 1) * g.Q + (int64_t)(j + 1) * g.P + g.A + i;
+        const int64_t xo = (int64_t)k * g.eyp + j;
         const double2 cc = *reinterpret_cast<const double2 *>(s + o);
-        const double xm = s[o - 1], xp = s[o + 2];
+        const double xm = (i == 0) ? xg0[xo] : s[o - 1];
+        const double xp0 = (i == g.ex - 1) ? xg1[xo] : cc.y;
+        const double xp1 = (i + 1 == g.ex - 1) ? xg1[xo] : s[o + 2];
         const double2 ym = *reinterpret_cast<const double2 *>(s + o - g.P);
         const double2 yp = *reinterpret_cast<const double2 *>(s + o + g.P);
         const double2 zm = *reinterpret_cast<const double2 *>(s + o - g.Q);
         const double2 zp = *reinterpret_cast<const double2 *>(s + o + g.Q);
         double2 v;
-        v.x = stencil7(cc.x, xm, cc.y, ym.x, yp.x, zm.x, zp.x);
-        v.y = stencil7(cc.y, cc.x, xp, ym.y, yp.y, zm.y, zp.y);
-        emit_pair(a, blk, dst, i, j, k, v);
+        v.x = stencil7(cc.x, xm, xp0, ym.x, yp.x, zm.x, zp.x);
+        v.y = stencil7(cc.y, cc.x, xp1, ym.y, yp.y, zm.y, zp.y);
+        emit_pair(a, blk, dst, own + (int64_t)(k + 1) * g.Q, (int64_t)(j + 1) * g.P + g.A + i, i, j, k, v);
     }
 }
 
@@ -413,13 +432,16 @@ __global__ void __launch_bounds__(256) ghost_fill_kernel(const SweepArgs a, int 
     double *base = a.arena + (int64_t)(dst * g.nslots + blk.slot) * g.bstride;
     const int d = f >> 1;
     const int64_t n = (d == 0) ? (int64_t)g.ey * g.ez : (d == 1) ? (int64_t)g.ex * g.ez : (int64_t)g.ex * g.ey;
+    double *xg = (d == 0) ? xg_array(a.xg, g, dst, blk.slot, f & 1) : nullptr;
     for (int64_t e = (int64_t)blockIdx.y * blockDim.x + threadIdx.x; e < n;
          e += (int64_t)gridDim.y * blockDim.x) {
-        int64_t off;
         if (d == 0) {
             const int64_t k = e / g.ey, j = e % g.ey;
-            off = (k + 1) * g.Q + (j + 1) * g.P + g.A + ((f == XM) ? -1 : g.ex);
-        } else if (d == 1) {
+            xg[k * g.eyp + j] = src[e];
+            continue;
+        }
+        int64_t off;
+        if (d == 1) {
             const int64_t k = e / g.ex, i = e % g.ex;
             off = (k + 1) * g.Q + ((f == YM) ? 0 : (int64_t)(g.ey + 1) * g.P) + g.A + i;
         } else {
@@ -453,7 +475,26 @@ __global__ void barrier_kernel(const BarrierArgs ba)
     __threadfence_system();
 }
 
-// ------------------------------------------------------------------ R11 hash init
+// ------------------------------------------------------------------ init helpers
+// Copies the inline ghost columns i = -1 / ex of buffer 0 (filled by the init copy)
+// into both buffers' x-ghost arrays.
+__global__ void xghost_extract_kernel(const SweepArgs a)
+{
+    const Geom &g = a.g;
+    const DevBlock &blk = a.blocks[blockIdx.y];
+    const double *b0 = a.arena + (int64_t)blk.slot * g.bstride;
+    const int64_t n = (int64_t)g.ey * g.ez;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t k = e / g.ey, j = e % g.ey;
+        const int64_t row = (k + 1) * g.Q + (j + 1) * g.P + g.A;
+        const double lo = b0[row - 1], hi = b0[row + g.ex];
+        for (int buf = 0; buf < 2; ++buf) {
+            xg_array(a.xg, g, buf, blk.slot, 0)[k * g.eyp + j] = lo;
+            xg_array(a.xg, g, buf, blk.slot, 1)[k * g.eyp + j] = hi;
+        }
+    }
+}
+
 __device__ __forceinline__ double r11_value(uint64_t seed, uint64_t p)
 {
     uint64_t z = (seed << 40) + p;
@@ -485,70 +526,82 @@ __global__ void hash_init_kernel(const SweepArgs a, int64_t nx, int64_t ny, uint
 }
 
 // ------------------------------------------------------------------ host launchers
-template <int BX, int BY, int NT, int NS>
+template <int BX, int BY, int W, int NT, int NS>
 static int resident_tma_t()
 {
     static int resident = 0;  // SMs x CTAs per SM (per process; one device per process)
     if (!resident) {
-        constexpr size_t smem = tma_smem_bytes(BX, BY, NS);
+        constexpr size_t smem = tma_smem_bytes(BX, BY, W, NS);
         int dev = 0, sms = 0, per_sm = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_tma_kernel<BX, BY, NT, NS>, NT, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_tma_kernel<BX, BY, W, NT, NS>, NT, smem);
         resident = std::max(1, sms * std::max(1, per_sm));
     }
     return resident;
 }
 
-template <int BX, int BY, int NT, int NS>
+template <int BX, int BY, int W, int NT, int NS>
+static cudaError_t prepare_tma_t()
+{
+    constexpr size_t smem = tma_smem_bytes(BX, BY, W, NS);
+    return cudaFuncSetAttribute(sweep_tma_kernel<BX, BY, W, NT, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)smem);
+}
+
+template <int BX, int BY, int W, int NT, int NS>
 static cudaError_t launch_tma_t(const CUtensorMap &tm, const SweepArgs &a, cudaStream_t s)
 {
-    constexpr size_t smem = tma_smem_bytes(BX, BY, NS);
-    // One CTA per item by default: the hardware launches CTAs in index order as slots
-    // free up, which keeps x/y-adjacent tiles (and successive z-chunks of a column)
-    // temporally close, so their shared halo planes are L2 hits.  A persistent grid
-    // with static striding lets CTAs drift apart and turns halos into DRAM re-reads
-    // (measured 359 -> 454 us per 512^3 sweep).  JAC_GRID=<n> caps the grid (tuning).
-    static int grid_cap = -1;
-    if (grid_cap < 0) {
-        const char *e = getenv("JAC_GRID");
-        grid_cap = e ? std::max(0, atoi(e)) : 0;
-    }
-    const int grid = grid_cap > 0 ? std::min(a.nitems, grid_cap) : a.nitems;
-    sweep_tma_kernel<BX, BY, NT, NS><<<(unsigned)grid, NT, smem, s>>>(tm, a);
+    constexpr size_t smem = tma_smem_bytes(BX, BY, W, NS);
+    // One CTA per item: the hardware launches CTAs in index order as slots free up,
+    // which keeps x/y-adjacent tiles (and successive z-chunks of a column) temporally
+    // close, so their shared halo planes are L2 hits.  A persistent grid with static
+    // striding lets CTAs drift apart and turns halos into DRAM re-reads (measured
+    // 359 -> 454 us per 512^3 sweep).
+    sweep_tma_kernel<BX, BY, W, NT, NS><<<(unsigned)a.nitems, NT, smem, s>>>(tm, a);
     return cudaGetLastError();
 }
 
-template <int BX, int BY, int NT, int NS>
-static cudaError_t prepare_tma_t()
-{
-    constexpr size_t smem = tma_smem_bytes(BX, BY, NS);
-    return cudaFuncSetAttribute(sweep_tma_kernel<BX, BY, NT, NS>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-}
-
-cudaError_t prepare_sweep_tma(int variant)
-{
-    if (variant == TMA_NARROW) return prepare_tma_t<32, 16, 256, 4>();
-    return prepare_tma_t<64, 16, 256, 4>();
-}
+#define JAC_TMA_VARIANTS(X)              \
+    X(TMA_WIDE, 64, 16, 68, 256, 4)      \
+    X(TMA_NARROW, 32, 16, 36, 256, 4)    \
+    X(TMA_EXACT32, 32, 16, 32, 256, 4)   \
+    X(TMA_EXACT64, 64, 16, 64, 256, 4)
 
 int sweep_resident_ctas(int variant)
 {
-    if (variant == TMA_NARROW) return resident_tma_t<32, 16, 256, 4>();
-    return resident_tma_t<64, 16, 256, 4>();
+#define X(V, BX, BY, W, NT, NS) \
+    if (variant == V) return resident_tma_t<BX, BY, W, NT, NS>();
+    JAC_TMA_VARIANTS(X)
+#undef X
+    return 148;
 }
 
 TileShape tma_tile_shape(int variant)
 {
-    if (variant == TMA_NARROW) return {32, 16};
-    return {64, 16};
+#define X(V, BX, BY, W, NT, NS) \
+    if (variant == V) return {BX, BY, W};
+    JAC_TMA_VARIANTS(X)
+#undef X
+    return {0, 0, 0};
+}
+
+cudaError_t prepare_sweep_tma(int variant)
+{
+#define X(V, BX, BY, W, NT, NS) \
+    if (variant == V) return prepare_tma_t<BX, BY, W, NT, NS>();
+    JAC_TMA_VARIANTS(X)
+#undef X
+    return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_sweep_tma(const CUtensorMap &tm, const SweepArgs &a, int variant, cudaStream_t s)
 {
-    if (variant == TMA_NARROW) return launch_tma_t<32, 16, 256, 4>(tm, a, s);
-    return launch_tma_t<64, 16, 256, 4>(tm, a, s);
+#define X(V, BX, BY, W, NT, NS) \
+    if (variant == V) return launch_tma_t<BX, BY, W, NT, NS>(tm, a, s);
+    JAC_TMA_VARIANTS(X)
+#undef X
+    return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_sweep_plain(const SweepArgs &a, cudaStream_t s)
@@ -576,6 +629,12 @@ cudaError_t launch_barrier(const BarrierArgs &ba, cudaStream_t s)
 cudaError_t launch_hash_init(const SweepArgs &a, int64_t nx, int64_t ny, uint64_t seed, cudaStream_t s)
 {
     hash_init_kernel<<<dim3(64, (unsigned)a.g.nslots), 256, 0, s>>>(a, nx, ny, seed);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_xghost_extract(const SweepArgs &a, cudaStream_t s)
+{
+    xghost_extract_kernel<<<dim3(16, (unsigned)a.g.nslots), 256, 0, s>>>(a);
     return cudaGetLastError();
 }
 

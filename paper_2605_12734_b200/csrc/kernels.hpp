@@ -7,16 +7,22 @@
 
 namespace jac {
 
-enum TmaVariant { TMA_WIDE = 0 /* 64 x 16 tiles */, TMA_NARROW = 1 /* 32 x 16 tiles */ };
-struct TileShape { int bx, by; };
+enum TmaVariant {
+    TMA_WIDE = 0,    /* 64 x 16 tiles, staged 68 wide (blocks wider than 64) */
+    TMA_NARROW = 1,  /* 32 x 16 tiles, staged 36 wide (blocks 33..64 wide) */
+    TMA_EXACT32 = 3, /* 32 x 16 tiles, staged 32 wide: one tile per block row (ex <= 32) */
+    TMA_EXACT64 = 4  /* 64 x 16 tiles, staged 64 wide: one tile per block row (ex <= 64) */
+};
+struct TileShape { int bx, by, w; };
 
 TileShape tma_tile_shape(int variant);
-cudaError_t prepare_sweep_tma(int variant);
-int sweep_resident_ctas(int variant);         // SMs x resident CTAs of the TMA sweep (current device)  // sets the dynamic-smem attribute (current device)
+cudaError_t prepare_sweep_tma(int variant);   // sets the dynamic-smem attribute (current device)
+int sweep_resident_ctas(int variant);         // SMs x resident CTAs of the TMA sweep (current device)
 cudaError_t launch_sweep_tma(const CUtensorMap &tm, const SweepArgs &a, int variant, cudaStream_t s);
 cudaError_t launch_sweep_plain(const SweepArgs &a, cudaStream_t s);  // 64 x 8 tiles
 cudaError_t launch_ghost_fill(const SweepArgs &a, int dst, cudaStream_t s);
 cudaError_t launch_barrier(const BarrierArgs &ba, cudaStream_t s);
+cudaError_t launch_xghost_extract(const SweepArgs &a, cudaStream_t s);
 cudaError_t launch_hash_init(const SweepArgs &a, int64_t nx, int64_t ny, uint64_t seed, cudaStream_t s);
 
 }  // namespace jac

@@ -50,7 +50,8 @@ _lib: Optional[ctypes.CDLL] = None
 
 
 def lib_path() -> str:
-    return _build.LIB
+    # JAC_LIB: load another build of the same ABI (same-box A/B comparisons only)
+    return os.environ.get("JAC_LIB") or _build.LIB
 
 
 def load() -> ctypes.CDLL:
@@ -58,7 +59,7 @@ def load() -> ctypes.CDLL:
     global _lib
     if _lib is not None:
         return _lib
-    path = _build.build()
+    path = os.environ.get("JAC_LIB") or _build.build()
     if not os.path.exists(path):
         raise ImportError(f"libjacobi3d.so missing at {path}; run __graft_entry__.build()")
     L = ctypes.CDLL(path)

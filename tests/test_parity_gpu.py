@@ -199,3 +199,15 @@ def test_c2_full_size_bench_config():
             got = f
     assert len(set(hashes)) == 1
     _lightcone_check(got, u0, n, [(0, 0, 0), (252, 252, 252), (504, 100, 255), (127, 383, 504)])
+
+
+@pytest.mark.parametrize("variant", ["0", "1", "3", "4"])
+@pytest.mark.parametrize("dims,blocks", [((64, 40, 36), (2, 2, 2)), ((128, 34, 20), (2, 1, 1)),
+                                         ((58, 30, 17), (2, 1, 1)), ((130, 51, 33), (1, 3, 1))])
+def test_tma_tile_variants(monkeypatch, variant, dims, blocks):
+    """Every TMA tile variant (wide 64+halo, narrow 32+halo, exact 32, exact 64) on
+    block widths 32, 64, 29 and 130, forced through JAC_VARIANT (ignored where the
+    variant cannot cover the block row)."""
+    monkeypatch.setenv("JAC_VARIANT", variant)
+    u0 = JI.hash_field(*dims, seed=3)
+    assert_bits(run(u0, blocks, 5), ref(u0, 5))

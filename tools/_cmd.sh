@@ -1,2 +1,5 @@
-timeout 300 python -m pytest tests/test_parity_gpu.py -q -x > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$? >> gpurun_out/pytest_gpu.log
-for gc in 0 100000 444 296 592; do echo "== GCOLS=$gc"; if [ $gc = 0 ]; then ITERS=40 timeout 200 python tools/quick_perf.py 2>&1; else JAC_GCOLS=$gc ITERS=40 timeout 200 python tools/quick_perf.py 2>&1; fi; done > gpurun_out/qp_gcols.log
+timeout 500 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$? >> gpurun_out/pytest_gpu.log
+for r in 1 2; do
+echo "== prev"; JAC_LIB=$PWD/build/ab/lib_prev.so ITERS=40 ODFS=1 timeout 200 python tools/quick_perf.py 2>&1 | cut -c1-90
+for d in 0 1 2 3; do echo "== dbg $d"; JAC_DBG=$d ITERS=40 ODFS=1,8 timeout 200 python tools/quick_perf.py 2>&1 | cut -c1-90; done
+done > gpurun_out/ab.log
