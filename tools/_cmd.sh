@@ -1,5 +1,3 @@
-timeout 500 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$? >> gpurun_out/pytest_gpu.log
-for r in 1 2; do
-echo "== prev"; JAC_LIB=$PWD/build/ab/lib_prev.so ITERS=40 ODFS=1 timeout 200 python tools/quick_perf.py 2>&1 | cut -c1-90
-for d in 0 1 2 3; do echo "== dbg $d"; JAC_DBG=$d ITERS=40 ODFS=1,8 timeout 200 python tools/quick_perf.py 2>&1 | cut -c1-90; done
-done > gpurun_out/ab.log
+for z in 32 16 8 4 2; do echo "== zchunk $z"; JAC_ZCHUNK=$z ITERS=200 timeout 100 python tools/perf_shapes.py 64x64x64:2x2x2 64x64x64:1x1x1 128x128x128:2x2x2 2>&1 | cut -c1-100; done > gpurun_out/c1.log
+echo "== default" >> gpurun_out/c1.log; ITERS=200 timeout 100 python tools/perf_shapes.py 64x64x64:2x2x2 64x64x64:1x1x1 128x128x128:2x2x2 2>&1 | cut -c1-100 >> gpurun_out/c1.log
+echo "== default unroll 50" >> gpurun_out/c1.log; JAC_UNROLL=50 ITERS=200 timeout 100 python tools/perf_shapes.py 64x64x64:2x2x2 2>&1 | cut -c1-100 >> gpurun_out/c1.log
