@@ -375,6 +375,24 @@ def run_ours(args, D):
                                "vs_default": ms / K / sweep["16"]["ms_per_iter"]}
             close_ctx(Ja, D)
 
+    # ---- NEXT-2 A/B: paper-style per-block streams (1 and 4 launching threads)
+    paper_style = None
+    if args.gpus == 1 and args.config == "c2" and not args.no_sweep:
+        paper_style = {}
+        for odf in (8, 16, 64):
+            d2, b2, g2, _, _ = workload("c2", 1, odf)
+            for th in (1, 4):
+                Jp = make_ctx(d2, b2, g2, D, flags=JB.JAC_F_PER_BLOCK)
+                Jp.set_option(JB.JAC_OPT_LAUNCH_THREADS, th)
+                Jp.set_init_hash(1)
+                kp = 20
+                ms, launches_p = time_ctx(Jp, kp, W, D)
+                paper_style[f"odf{odf}_threads{th}"] = {
+                    "ms_per_iter": ms / kp, "glups": pts * kp / (ms * 1e-3) / 1e9,
+                    "kernels_per_iter": launches_p // kp,
+                    "vs_batched": ms / kp / sweep[str(odf)]["ms_per_iter"]}
+                close_ctx(Jp, D)
+
     cpu = None
     if args.gpus == 1 and D.rank == 0 and not args.no_cpu:
         cpu = cpu_oracle(box=(512, 512, 512), budget_s=args.cpu_budget)
@@ -409,6 +427,8 @@ def run_ours(args, D):
         if sweep is not None:
             line["odf_sweep"] = sweep
             line["ablations_odf16"] = ablations
+        if paper_style is not None:
+            line["paper_style_per_block"] = paper_style
         print(json.dumps(line), flush=True)
     D.finish()
 

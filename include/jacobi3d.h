@@ -70,7 +70,21 @@ enum jac_flags {
     JAC_F_VIRTUAL_GPUS = 1u << 6, /* test-only: all n_gpus partitions live on device 0 and
                                      are swept by ONE kernel (no cross-partition waits);
                                      exercises the partition / REMOTE-face logic */
-    JAC_F_SKIP_EXCHANGE = 1u << 7 /* timing-only ablation: no face writes. WRONG results */
+    JAC_F_SKIP_EXCHANGE = 1u << 7, /* timing-only ablation: no face writes. WRONG results */
+    JAC_F_PER_BLOCK = 1u << 8      /* paper-style execution: one stream per
+                                      block ("non-blocking per-chare streams")
+                                      and, per iteration and block, one unpack launch per
+                                      face, one stencil launch, one pack launch per face
+                                      (SPEC.md:474), ordered by per-block events; no graph.
+                                      Launching host threads (the paper's PEs per process,
+                                      PAPER.md:95) via jac_set_option.  One GPU only
+                                      (n_gpus == 1 or JAC_F_VIRTUAL_GPUS). */
+};
+
+/* Options for jac_set_option. */
+enum jac_option {
+    JAC_OPT_LAUNCH_THREADS = 1 /* JAC_F_PER_BLOCK: host threads enqueueing the blocks'
+                                  work (1..64, default 1); blocks are dealt round-robin */
 };
 
 /* Face kinds of the block-descriptor table (the analog of the paper's pre-filled
@@ -188,6 +202,10 @@ enum jac_stat {
     JAC_STAT_N = 9
 };
 int jac_get_stats(const jac_ctx *c, int64_t *stats /* [JAC_STAT_N] */);
+
+/* Sets a run-time option (enum jac_option).  JAC_EINVAL for an unknown option or
+ * an out-of-range value. */
+int jac_set_option(jac_ctx *c, int32_t option, int64_t value);
 
 /* NULL-safe.  Rank contexts: every rank must have finished its last jac_step
  * (caller barrier) before any rank destroys. */

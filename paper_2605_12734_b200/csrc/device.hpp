@@ -31,7 +31,7 @@
 namespace jac {
 
 enum Face { XM = 0, XP = 1, YM = 2, YP = 3, ZM = 4, ZP = 5 };
-inline constexpr int opposite(int f) { return f ^ 1; }
+JAC_HD inline constexpr int opposite(int f) { return f ^ 1; }
 
 constexpr int kA = 4;        // x offset of interior column 0 inside a row
 constexpr int kXgPad = 32;   // doubles of slack after each x-ghost array (bulk-copy overrun)

@@ -16,6 +16,9 @@
 
 #include <algorithm>
 #include <climits>
+#include <condition_variable>
+#include <mutex>
+#include <thread>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -100,6 +103,10 @@ struct jac_ctx {
     jac::BarrierArgs bar{};
 
     cudaStream_t stream = nullptr;
+    // JAC_F_PER_BLOCK (paper-style): one stream per block, events per block and parity
+    std::vector<cudaStream_t> bstreams;
+    std::vector<cudaEvent_t> bevents;  // [slot * 2 + parity]
+    int launch_threads = 1;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     cudaGraphExec_t g1[2] = {nullptr, nullptr}, gU[2] = {nullptr, nullptr};
     int unroll = 10;
@@ -113,6 +120,7 @@ struct jac_ctx {
     bool has_remote() const { return !peer_ranks.empty(); }
     int kernels_per_iter() const
     {
+        if (flags & JAC_F_PER_BLOCK) return (int)(nslots + 2 * local_faces + 2 * remote_faces);
         int k = 1;
         if (flags & JAC_F_UNFUSED_PACK) k += 1 + (has_remote() ? 2 : 0);
         else if (has_remote()) k += 1;
@@ -259,6 +267,9 @@ int create_common(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, in
     int rc = jac::make_plan(nx, ny, nz, bx, by, bz, n_gpus, gpu_grid, &plan, &err);
     if (rc) return fail(rc, "%s", err.c_str());
     if (flags & JAC_F_NCCL) return fail(JAC_EINVAL, "flags: JAC_F_NCCL transport is not built in this version");
+    if ((flags & JAC_F_PER_BLOCK) && (rank_mode || (flags & (JAC_F_UNFUSED_PACK | JAC_F_SKIP_EXCHANGE))))
+        return fail(JAC_EINVAL, "flags: JAC_F_PER_BLOCK runs on one GPU (not a rank context) and excludes "
+                                "JAC_F_UNFUSED_PACK / JAC_F_SKIP_EXCHANGE");
     if (rank_mode) {
         if (rank < 0 || rank >= n_gpus) return fail(JAC_EINVAL, "rank %d out of [0,%d)", rank, n_gpus);
         if (flags & JAC_F_VIRTUAL_GPUS) return fail(JAC_EINVAL, "flags: JAC_F_VIRTUAL_GPUS is not valid for rank contexts");
@@ -300,7 +311,7 @@ int create_common(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, in
     int64_t o = 0;
     const int64_t fsz[6] = {fx, fx, fy, fy, fz, fz};
     for (int f = 0; f < 6; ++f) { g.ooff[f] = o; o += round_up(fsz[f], 4); }
-    g.ostride = (flags & JAC_F_UNFUSED_PACK) ? round_up(o, 32) : 0;
+    g.ostride = (flags & (JAC_F_UNFUSED_PACK | JAC_F_PER_BLOCK)) ? round_up(o, 32) : 0;
 
     // tile shape / variant
     if (flags & JAC_F_NO_TMA) c->variant = kPlain;
@@ -357,7 +368,8 @@ int create_common(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, in
     c->xg_off = c->arena_off + arena_bytes;
     const size_t xg_bytes = (size_t)2 * c->nslots * 2 * g.xgstride * sizeof(double);
     c->outbox_off = c->xg_off + xg_bytes;
-    const size_t outbox_bytes = (size_t)c->nslots * g.ostride * sizeof(double);
+    // outbox: one set of faces per block; JAC_F_PER_BLOCK double-buffers it by parity
+    const size_t outbox_bytes = (size_t)((flags & JAC_F_PER_BLOCK) ? 2 : 1) * c->nslots * g.ostride * sizeof(double);
     c->alloc_bytes = c->outbox_off + outbox_bytes;
     e = cudaMalloc(&c->alloc, c->alloc_bytes);
     if (e != cudaSuccess) {
@@ -415,12 +427,118 @@ int create_common(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, in
     if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess)
         return bail(fail(JAC_ECUDA, "stream/event creation"));
+    if (flags & JAC_F_PER_BLOCK) {
+        c->bstreams.assign(c->nslots, nullptr);
+        c->bevents.assign((size_t)2 * c->nslots, nullptr);
+        for (auto &st : c->bstreams)
+            if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess)
+                return bail(fail(JAC_ECUDA, "per-block stream creation"));
+        for (auto &ev : c->bevents)
+            if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess)
+                return bail(fail(JAC_ECUDA, "per-block event creation"));
+    }
     // barrier args (peer slots filled at import)
     c->bar.ctrl = c->ctrl;
     c->bar.npeers = (int32_t)c->peer_ranks.size();
     for (int n = 0; n < c->bar.npeers; ++n) c->bar.peer_id[n] = c->peer_ranks[n];
     c->ipc_done = !c->has_remote() && !rank_mode;
     *out = c;
+    return JAC_OK;
+}
+
+// ---------------------------------------------------------------- paper-style mode
+// One iteration t for the blocks b = first, first + stride, ...: on the block's own
+// stream wait for every neighbour's pack of t-1, unpack each face, stencil, pack
+// each face, record the block's event for parity t.
+int enqueue_per_block(jac_ctx *c, int64_t t, int first, int stride)
+{
+    const int src = (int)(t & 1), dst = 1 - src, par = (int)(t & 1), ppar = 1 - par;
+    jac::SweepArgs base = sweep_args(c, src, jac::MODE_NOEXCHANGE);
+    for (int b = first; b < c->nslots; b += stride) {
+        cudaStream_t s = c->bstreams[b];
+        const jac::DevBlock &d = c->hblocks[b];
+        int nbs[6];
+        for (int f = 0; f < 6; ++f) {
+            nbs[f] = -1;
+            if (!d.nb[f][0]) continue;
+            int32_t blk[3], nb[3];
+            for (int k = 0; k < 3; ++k) blk[k] = (int32_t)(d.org[k] / c->plan.e[k]);
+            c->plan.neighbor(blk, f, nb);
+            const int32_t part = c->plan.owner(nb[0], nb[1], nb[2]);
+            const int32_t h = (int32_t)(std::find(c->parts.begin(), c->parts.end(), part) - c->parts.begin());
+            nbs[f] = h * c->plan.blocks_per_part() + c->plan.local_slot(nb[0], nb[1], nb[2]);
+        }
+        if (t > 0) {  // at t = 0 the ghosts come from jac_set_init*
+            for (int f = 0; f < 6; ++f)
+                if (nbs[f] >= 0) CK(cudaStreamWaitEvent(s, c->bevents[(size_t)nbs[f] * 2 + ppar], 0));
+            for (int f = 0; f < 6; ++f)
+                if (nbs[f] >= 0) CK(jac::launch_unpack_face(base, b, nbs[f], f, src, ppar, s));
+        }
+        jac::SweepArgs a = base;  // the stencil of this block alone
+        a.blocks = c->dblocks + b;
+        a.ncols = c->ntx * c->nty;
+        a.nitems = a.ncols * c->nzc;
+        a.gcols = a.ncols;
+        a.ntz = c->ntz;
+        if (c->variant == kPlain) {
+            CK(jac::launch_sweep_plain_one(a, s));
+        } else {
+            CK(jac::launch_sweep_tma(c->tmap, a, c->variant, s));
+        }
+        for (int f = 0; f < 6; ++f)
+            if (nbs[f] >= 0) CK(jac::launch_pack_face(base, b, f, dst, par, s));
+        CK(cudaEventRecord(c->bevents[(size_t)b * 2 + par], s));
+    }
+    return JAC_OK;
+}
+
+struct HostBarrier {
+    std::mutex m;
+    std::condition_variable cv;
+    int n, waiting = 0;
+    long gen = 0;
+    explicit HostBarrier(int n_) : n(n_) {}
+    void wait()
+    {
+        std::unique_lock<std::mutex> lk(m);
+        const long g = gen;
+        if (++waiting == n) { waiting = 0; ++gen; cv.notify_all(); }
+        else cv.wait(lk, [&] { return gen != g; });
+    }
+};
+
+int per_block_step(jac_ctx *c, int32_t n)
+{
+    for (cudaStream_t s : c->bstreams) CK(cudaStreamWaitEvent(s, c->ev0, 0));
+    const int T = std::max(1, std::min(c->launch_threads, c->nslots));
+    int rc = JAC_OK;
+    if (T == 1) {
+        for (int it = 0; it < n && rc == JAC_OK; ++it) rc = enqueue_per_block(c, c->iters + it, 0, 1);
+    } else {
+        HostBarrier bar(T);
+        std::vector<int> rcs(T, JAC_OK);
+        std::vector<std::string> errs(T);
+        std::vector<std::thread> pes;
+        for (int p = 0; p < T; ++p)
+            pes.emplace_back([&, p] {
+                cudaSetDevice(c->device);
+                for (int it = 0; it < n; ++it) {
+                    if (rcs[p] == JAC_OK) {
+                        rcs[p] = enqueue_per_block(c, c->iters + it, p, T);
+                        if (rcs[p]) errs[p] = g_err;
+                    }
+                    bar.wait();  // every block's event for parity t is recorded before t+1 waits on it
+                }
+            });
+        for (auto &th : pes) th.join();
+        for (int p = 0; p < T; ++p)
+            if (rcs[p]) { g_err = errs[p]; return rcs[p]; }
+    }
+    if (rc) return rc;
+    if (n > 0) {
+        const int last = (int)((c->iters + n - 1) & 1);
+        for (int b = 0; b < c->nslots; ++b) CK(cudaStreamWaitEvent(c->stream, c->bevents[(size_t)b * 2 + last], 0));
+    }
     return JAC_OK;
 }
 
@@ -669,7 +787,7 @@ int jac_step(jac_ctx *c, int32_t n)
     if (n < 0) return fail(JAC_EINVAL, "n_iters = %d < 0", n);
     if (!c->inited) return fail(JAC_ESTATE, "jac_step before jac_set_init / jac_set_init_hash");
     CK(cudaSetDevice(c->device));
-    const bool graphs = !(c->flags & JAC_F_NO_GRAPH);
+    const bool graphs = !(c->flags & (JAC_F_NO_GRAPH | JAC_F_PER_BLOCK));
     if (graphs && !c->g1[0]) {
         for (int s = 0; s < 2; ++s) {
             if ((rc = build_graph(c, s, 1, &c->g1[s]))) return rc;
@@ -680,7 +798,10 @@ int jac_step(jac_ctx *c, int32_t n)
     CK(cudaEventRecord(c->ev0, c->stream));
     int src = (int)(c->iters & 1);
     int left = n;
-    if (graphs) {
+    if (c->flags & JAC_F_PER_BLOCK) {
+        if ((rc = per_block_step(c, n))) return rc;
+        left = 0;
+    } else if (graphs) {
         while (left >= c->unroll) {
             CK(cudaGraphLaunch(c->gU[src], c->stream));
             c->graph_launches++;
@@ -712,6 +833,7 @@ int jac_profile_sweep(jac_ctx *c, int32_t n, double *avg_ms)
     if ((rc = require_ready(c))) return rc;
     if (n < 1 || !avg_ms) return fail(JAC_EINVAL, "n_iters must be >= 1 and avg_sweep_ms non-NULL");
     if (!c->inited) return fail(JAC_ESTATE, "jac_profile_sweep before init");
+    if (c->flags & JAC_F_PER_BLOCK) return fail(JAC_EINVAL, "jac_profile_sweep: not available with JAC_F_PER_BLOCK");
     CK(cudaSetDevice(c->device));
     std::vector<cudaEvent_t> ev(2 * (size_t)n);
     for (auto &e : ev) CK(cudaEventCreate(&e));
@@ -872,11 +994,26 @@ int jac_get_stats(const jac_ctx *c, int64_t *st)
     return JAC_OK;
 }
 
+int jac_set_option(jac_ctx *c, int32_t option, int64_t value)
+{
+    if (!c) return fail(JAC_EINVAL, "ctx is NULL");
+    switch (option) {
+    case JAC_OPT_LAUNCH_THREADS:
+        if (value < 1 || value > 64) return fail(JAC_EINVAL, "JAC_OPT_LAUNCH_THREADS value %lld not in 1..64", (long long)value);
+        c->launch_threads = (int)value;
+        return JAC_OK;
+    default:
+        return fail(JAC_EINVAL, "unknown option %d", option);
+    }
+}
+
 int jac_destroy(jac_ctx *c)
 {
     if (!c) return JAC_OK;
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
+    for (cudaStream_t s : c->bstreams) if (s) { cudaStreamSynchronize(s); cudaStreamDestroy(s); }
+    for (cudaEvent_t e : c->bevents) if (e) cudaEventDestroy(e);
     for (int s = 0; s < 2; ++s) {
         if (c->g1[s]) cudaGraphExecDestroy(c->g1[s]);
         if (c->gU[s]) cudaGraphExecDestroy(c->gU[s]);

@@ -452,6 +452,82 @@ __global__ void __launch_bounds__(256) ghost_fill_kernel(const SweepArgs a, int 
     }
 }
 
+// ------------------------------------------------------------------ paper-style pack / unpack
+// JAC_F_PER_BLOCK (NEXT-2): one pack and one unpack launch per face per block, on
+// the block's own stream, as in the paper's Charm++ Jacobi (PAPER.md:90, SPEC.md:474:
+// "packs 4 boundary strips (pack kernel per face on its own stream) ... on receiving
+// all 4 runs unpack kernels then the stencil kernel").
+// pack: boundary layer of face f of block `slot`, buffer `buf` -> outbox[par][slot][f]
+__global__ void __launch_bounds__(256) pack_face_kernel(const SweepArgs a, int slot, int f, int buf, int par)
+{
+    const Geom &g = a.g;
+    const double *base = a.arena + (int64_t)(buf * g.nslots + slot) * g.bstride;
+    double *ob = a.outbox + ((int64_t)par * g.nslots + slot) * g.ostride + g.ooff[f];
+    const int d = f >> 1;
+    const int64_t n = (d == 0) ? (int64_t)g.ey * g.ez : (d == 1) ? (int64_t)g.ex * g.ez : (int64_t)g.ex * g.ey;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+        int64_t off;
+        if (d == 0) {
+            const int64_t k = e / g.ey, j = e % g.ey;
+            off = (k + 1) * g.Q + (j + 1) * g.P + g.A + ((f == XM) ? 0 : g.ex - 1);
+        } else if (d == 1) {
+            const int64_t k = e / g.ex, i = e % g.ex;
+            off = (k + 1) * g.Q + ((f == YM) ? 1 : (int64_t)g.ey) * g.P + g.A + i;
+        } else {
+            const int64_t j = e / g.ex, i = e % g.ex;
+            off = ((f == ZM) ? 1 : (int64_t)g.ez) * g.Q + (j + 1) * g.P + g.A + i;
+        }
+        ob[e] = base[off];
+    }
+}
+
+// unpack: outbox[par][nslot][opposite(f)] of the neighbour -> ghost face f of block
+// `slot` in buffer `buf` (x ghosts into the x-ghost arrays).
+__global__ void __launch_bounds__(256) unpack_face_kernel(const SweepArgs a, int slot, int nslot, int f, int buf, int par)
+{
+    const Geom &g = a.g;
+    const double *src = a.outbox + ((int64_t)par * g.nslots + nslot) * g.ostride + g.ooff[opposite(f)];
+    double *base = a.arena + (int64_t)(buf * g.nslots + slot) * g.bstride;
+    const int d = f >> 1;
+    const int64_t n = (d == 0) ? (int64_t)g.ey * g.ez : (d == 1) ? (int64_t)g.ex * g.ez : (int64_t)g.ex * g.ey;
+    double *xg = (d == 0) ? xg_array(a.xg, g, buf, slot, f & 1) : nullptr;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+        if (d == 0) {
+            const int64_t k = e / g.ey, j = e % g.ey;
+            xg[k * g.eyp + j] = src[e];
+            continue;
+        }
+        int64_t off;
+        if (d == 1) {
+            const int64_t k = e / g.ex, i = e % g.ex;
+            off = (k + 1) * g.Q + ((f == YM) ? 0 : (int64_t)(g.ey + 1) * g.P) + g.A + i;
+        } else {
+            const int64_t j = e / g.ex, i = e % g.ex;
+            off = ((f == ZM) ? 0 : (int64_t)(g.ez + 1) * g.Q) + (j + 1) * g.P + g.A + i;
+        }
+        base[off] = src[e];
+    }
+}
+
+static unsigned face_grid(const Geom &g, int f)
+{
+    const int d = f >> 1;
+    const int64_t n = (d == 0) ? (int64_t)g.ey * g.ez : (d == 1) ? (int64_t)g.ex * g.ez : (int64_t)g.ex * g.ey;
+    return (unsigned)std::max<int64_t>(1, std::min<int64_t>(1184, (n + 255) / 256));
+}
+
+cudaError_t launch_pack_face(const SweepArgs &a, int slot, int f, int buf, int par, cudaStream_t s)
+{
+    pack_face_kernel<<<face_grid(a.g, f), 256, 0, s>>>(a, slot, f, buf, par);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_unpack_face(const SweepArgs &a, int slot, int nslot, int f, int buf, int par, cudaStream_t s)
+{
+    unpack_face_kernel<<<face_grid(a.g, f), 256, 0, s>>>(a, slot, nslot, f, buf, par);
+    return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------ neighbour barrier
 __global__ void barrier_kernel(const BarrierArgs ba)
 {
@@ -607,6 +683,13 @@ cudaError_t launch_sweep_tma(const CUtensorMap &tm, const SweepArgs &a, int vari
 cudaError_t launch_sweep_plain(const SweepArgs &a, cudaStream_t s)
 {
     const int64_t grid = (int64_t)a.g.nslots * a.ntx * a.nty * a.ntz;
+    sweep_plain_kernel<<<(unsigned)grid, 256, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sweep_plain_one(const SweepArgs &a, cudaStream_t s)
+{
+    const int64_t grid = (int64_t)a.ntx * a.nty * a.ntz;  // a.blocks points at the one block
     sweep_plain_kernel<<<(unsigned)grid, 256, 0, s>>>(a);
     return cudaGetLastError();
 }

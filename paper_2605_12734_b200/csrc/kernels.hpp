@@ -20,8 +20,11 @@ cudaError_t prepare_sweep_tma(int variant);   // sets the dynamic-smem attribute
 int sweep_resident_ctas(int variant);         // SMs x resident CTAs of the TMA sweep (current device)
 cudaError_t launch_sweep_tma(const CUtensorMap &tm, const SweepArgs &a, int variant, cudaStream_t s);
 cudaError_t launch_sweep_plain(const SweepArgs &a, cudaStream_t s);  // 64 x 8 tiles
+cudaError_t launch_sweep_plain_one(const SweepArgs &a, cudaStream_t s);  // a.blocks = one block
 cudaError_t launch_ghost_fill(const SweepArgs &a, int dst, cudaStream_t s);
 cudaError_t launch_barrier(const BarrierArgs &ba, cudaStream_t s);
+cudaError_t launch_pack_face(const SweepArgs &a, int slot, int f, int buf, int par, cudaStream_t s);
+cudaError_t launch_unpack_face(const SweepArgs &a, int slot, int nslot, int f, int buf, int par, cudaStream_t s);
 cudaError_t launch_xghost_extract(const SweepArgs &a, cudaStream_t s);
 cudaError_t launch_hash_init(const SweepArgs &a, int64_t nx, int64_t ny, uint64_t seed, cudaStream_t s);
 

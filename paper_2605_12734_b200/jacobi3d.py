@@ -27,6 +27,8 @@ JAC_F_UNFUSED_PACK = 1 << 4
 JAC_F_NO_TMA = 1 << 5
 JAC_F_VIRTUAL_GPUS = 1 << 6
 JAC_F_SKIP_EXCHANGE = 1 << 7
+JAC_F_PER_BLOCK = 1 << 8
+JAC_OPT_LAUNCH_THREADS = 1
 JAC_FACE_BOUNDARY, JAC_FACE_LOCAL, JAC_FACE_REMOTE = 0, 1, 2
 STAT_NAMES = ["kernel_launches", "graph_launches", "kernels_per_iter", "local_blocks",
               "local_faces", "remote_faces", "remote_bytes", "arena_bytes", "sweep_variant"]
@@ -34,7 +36,7 @@ EXPORTED = ["jac_plan", "jac_plan_face", "jac_create", "jac_create_rank", "jac_i
             "jac_export_ipc", "jac_import_ipc", "jac_set_init", "jac_set_init_hash", "jac_step",
             "jac_get_block", "jac_get_block_padded", "jac_get_field", "jac_get_layout",
             "jac_block_owner", "jac_last_step_ms", "jac_set_init_box", "jac_get_field_box", "jac_local_box", "jac_profile_sweep", "jac_get_stats",
-            "jac_destroy", "jac_last_error", "jac_version"]
+            "jac_destroy", "jac_last_error", "jac_version", "jac_set_option"]
 
 _ERRNAMES = {-1: "JAC_EINVAL", -2: "JAC_EDECOMP", -3: "JAC_EDEVICE", -4: "JAC_ENOMEM",
              -5: "JAC_ECUDA", -6: "JAC_ENCCL", -7: "JAC_ESTATE"}
@@ -88,6 +90,7 @@ def load() -> ctypes.CDLL:
         "jac_profile_sweep": [vp, i32, P(ctypes.c_double)],
         "jac_get_stats": [vp, P(i64)],
         "jac_destroy": [vp],
+        "jac_set_option": [vp, i32, i64],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -250,6 +253,10 @@ def jac_get_stats(ctx) -> dict:
     return dict(zip(STAT_NAMES, list(st)))
 
 
+def jac_set_option(ctx, option: int, value: int) -> None:
+    _check(load().jac_set_option(ctx, option, value), "jac_set_option")
+
+
 def jac_destroy(ctx) -> None:
     _check(load().jac_destroy(ctx), "jac_destroy")
 
@@ -325,6 +332,9 @@ class Jacobi3D:
 
     def profile_sweep(self, n: int) -> float:
         return jac_profile_sweep(self.ctx, n)
+
+    def set_option(self, option: int, value: int) -> None:
+        jac_set_option(self.ctx, option, value)
 
     def stats(self) -> dict:
         return jac_get_stats(self.ctx)

@@ -211,3 +211,24 @@ def test_tma_tile_variants(monkeypatch, variant, dims, blocks):
     monkeypatch.setenv("JAC_VARIANT", variant)
     u0 = JI.hash_field(*dims, seed=3)
     assert_bits(run(u0, blocks, 5), ref(u0, 5))
+
+
+@pytest.mark.parametrize("threads", [1, 3])
+@pytest.mark.parametrize("dims,blocks,extra", [((64, 48, 40), (2, 3, 2), 0), ((96, 64, 64), (3, 2, 4), 0),
+                                               ((64, 64, 64), (2, 2, 2), 1 << 5), ((40, 40, 40), (1, 1, 1), 0)])
+def test_paper_style_per_block_mode(threads, dims, blocks, extra):
+    """NEXT-2: per-block streams, per-face pack/unpack launches, event ordering,
+    several launching host threads -- bit-identical to the oracle (and so to the
+    batched path)."""
+    u0 = JI.hash_field(*dims, seed=1)
+    nz2, ny2, nx2 = u0.shape
+    with jb.Jacobi3D(dims, blocks, flags=J.JAC_F_PER_BLOCK | extra) as s:
+        s.set_option(J.JAC_OPT_LAUNCH_THREADS, threads)
+        s.set_init(u0)
+        s.step(3)
+        s.step(4)
+        got = s.field(u0)
+        st = s.stats()
+    assert_bits(got, ref(u0, 7))
+    nb = blocks[0] * blocks[1] * blocks[2]
+    assert st["kernels_per_iter"] == nb + 2 * st["local_faces"]
