@@ -14,7 +14,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libjacobi3d.so")
-SOURCES = ["engine.cu", "kernels.cu", "plan.cpp"]
+SOURCES = ["engine.cu", "kernels.cu", "microbench.cu", "plan.cpp"]
 HEADERS = ["device.hpp", "kernels.hpp", "plan.hpp"]
 
 NVCC_FLAGS = [
@@ -28,6 +28,7 @@ NVCC_FLAGS = [
 def _inputs():
     files = [os.path.join(CSRC, f) for f in SOURCES + HEADERS]
     files.append(os.path.join(ROOT, "include", "jacobi3d.h"))
+    files.append(os.path.join(ROOT, "include", "jacobi3d_microbench.h"))
     files.append(os.path.abspath(__file__))
     return files
 

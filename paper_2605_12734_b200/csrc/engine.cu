@@ -73,6 +73,15 @@ typedef CUresult (*PFN_encodeTiled)(CUtensorMap *, CUtensorMapDataType, cuuint32
 
 }  // namespace
 
+namespace jac {
+// for the microbenchmarks (microbench.cu): same thread-local error slot
+void set_last_error(int code, const char *msg)
+{
+    (void)code;
+    g_err = msg;
+}
+}  // namespace jac
+
 struct jac_ctx {
     jac::Plan plan{};
     uint32_t flags = 0;

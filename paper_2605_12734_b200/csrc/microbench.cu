@@ -1,0 +1,280 @@
+// microbench.cu -- the paper's runtime microbenchmarks on B200 (SURVEY.md §8(f)
+// NEXT-3 / NEXT-4), include/jacobi3d_microbench.h.  Not part of the Jacobi hot path:
+// they measure the launch, overlap and NVLink costs that overdecomposition pays.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cstdarg>
+#include <cstdio>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/jacobi3d.h"
+#include "../../include/jacobi3d_microbench.h"
+
+namespace jac {
+void set_last_error(int code, const char *msg);  // engine.cu
+}
+
+namespace {
+
+int mb_fail(int code, const char *fmt, ...)
+{
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    jac::set_last_error(code, buf);
+    return code;
+}
+
+#define MCK(call)                                                                                      \
+    do {                                                                                               \
+        cudaError_t e_ = (call);                                                                       \
+        if (e_ != cudaSuccess) return mb_fail(JAC_ECUDA, "%s: %s", #call, cudaGetErrorString(e_));     \
+    } while (0)
+
+double now_us()
+{
+    return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+__global__ void empty_kernel() {}
+
+__device__ __forceinline__ uint64_t gtimer()
+{
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// `work` dependent FMAs per thread; the CTA's first thread stamps start / end.
+__global__ void work_kernel(int work, unsigned long long *t_start, unsigned long long *t_end, float *sink)
+{
+    const uint64_t t0 = gtimer();
+    float x = (float)threadIdx.x * 1e-3f, y = 1.0001f;
+    for (int i = 0; i < work; ++i) x = fmaf(x, y, 1e-7f);
+    if (x == 12345.678f) sink[0] = x;  // keeps the loop alive
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        atomicMin(t_start, (unsigned long long)t0);
+        atomicMax(t_end, (unsigned long long)gtimer());
+    }
+}
+
+// O(n) consumer of a received message (NEXT-3 with compute)
+__global__ void consume_kernel(double *p, int64_t n)
+{
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        p[i] = p[i] * 1.0000001 + 1e-12;
+}
+
+typedef CUresult (*PFN_waitValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+
+}  // namespace
+
+extern "C" {
+
+int jac_mb_launch_latency(int32_t device, int32_t iters, double *us)
+{
+    if (!us || iters < 1) return mb_fail(JAC_EINVAL, "iters must be >= 1, us non-NULL");
+    MCK(cudaSetDevice(device));
+    cudaStream_t s;
+    MCK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    for (int i = 0; i < 50; ++i) {
+        empty_kernel<<<1, 32, 0, s>>>();
+        MCK(cudaStreamSynchronize(s));
+    }
+    const double t0 = now_us();
+    for (int i = 0; i < iters; ++i) {
+        empty_kernel<<<1, 32, 0, s>>>();
+        MCK(cudaStreamSynchronize(s));
+    }
+    *us = (now_us() - t0) / iters;
+    cudaStreamDestroy(s);
+    return JAC_OK;
+}
+
+int jac_mb_overlap(int32_t device, int64_t total_threads, int32_t odf, int32_t work, double *host_us, double *device_us)
+{
+    if (!host_us || !device_us || odf < 1 || total_threads < odf || work < 0)
+        return mb_fail(JAC_EINVAL, "need odf >= 1, total_threads >= odf, work >= 0, non-NULL outputs");
+    MCK(cudaSetDevice(device));
+    static PFN_waitValue32 waitv = nullptr;
+    if (!waitv) {
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        MCK(cudaGetDriverEntryPoint("cuStreamWaitValue32", &fn, cudaEnableDefault, &q));
+        if (!fn) return mb_fail(JAC_ECUDA, "cuStreamWaitValue32 unavailable");
+        waitv = (PFN_waitValue32)fn;
+    }
+    volatile uint32_t *hflag = nullptr;
+    MCK(cudaHostAlloc((void **)&hflag, sizeof(uint32_t), cudaHostAllocMapped));
+    *hflag = 0;
+    void *dflag = nullptr;
+    MCK(cudaHostGetDevicePointer(&dflag, (void *)hflag, 0));
+    unsigned long long *stamps = nullptr;
+    float *sink = nullptr;
+    MCK(cudaMalloc(&stamps, 2 * sizeof(unsigned long long)));
+    MCK(cudaMalloc(&sink, sizeof(float)));
+    const unsigned long long init[2] = {~0ull, 0ull};
+    MCK(cudaMemcpy(stamps, init, sizeof init, cudaMemcpyHostToDevice));
+    std::vector<cudaStream_t> st(odf);
+    for (auto &s : st) MCK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    const int64_t per = total_threads / odf;
+    const int block = 256;
+    const unsigned grid = (unsigned)std::max<int64_t>(1, (per + block - 1) / block);
+    for (int k = 0; k < odf; ++k) {  // everything enqueued up front behind the flag
+        if (waitv(st[k], (CUdeviceptr)dflag, 1, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+            return mb_fail(JAC_ECUDA, "cuStreamWaitValue32 failed");
+        work_kernel<<<grid, block, 0, st[k]>>>(work, stamps, stamps + 1, sink);
+        MCK(cudaGetLastError());
+    }
+    std::this_thread::sleep_for(std::chrono::milliseconds(20));  // let the enqueue settle
+    const double t0 = now_us();
+    std::atomic_thread_fence(std::memory_order_seq_cst);
+    *hflag = 1;  // release every stream at once
+    for (auto &s : st) MCK(cudaStreamSynchronize(s));
+    *host_us = now_us() - t0;
+    unsigned long long out[2];
+    MCK(cudaMemcpy(out, stamps, sizeof out, cudaMemcpyDeviceToHost));
+    *device_us = (double)(out[1] - out[0]) * 1e-3;
+    for (auto &s : st) cudaStreamDestroy(s);
+    cudaFree(stamps);
+    cudaFree(sink);
+    cudaFreeHost((void *)hflag);
+    return JAC_OK;
+}
+
+int jac_mb_launch_rate(int32_t device, int32_t chares, int32_t threads, double seconds, double *kps)
+{
+    if (!kps || chares < 1 || threads < 1 || threads > 64 || seconds <= 0)
+        return mb_fail(JAC_EINVAL, "need chares >= 1, 1 <= threads <= 64, seconds > 0");
+    MCK(cudaSetDevice(device));
+    int sms = 0;
+    MCK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    std::vector<long> done(threads, 0);
+    std::vector<int> err(threads, 0);
+    std::vector<std::thread> pes;
+    const double t_end = now_us() + seconds * 1e6;
+    for (int p = 0; p < threads; ++p)
+        pes.emplace_back([&, p] {
+            cudaSetDevice(device);
+            std::vector<cudaStream_t> st(chares);
+            std::vector<cudaEvent_t> ev(chares);
+            std::vector<char> pending(chares, 0);
+            for (int c = 0; c < chares; ++c) {
+                cudaStreamCreateWithFlags(&st[c], cudaStreamNonBlocking);
+                cudaEventCreateWithFlags(&ev[c], cudaEventDisableTiming);
+            }
+            long n = 0;
+            while (now_us() < t_end) {  // the PE's scheduler loop
+                for (int c = 0; c < chares; ++c) {
+                    if (pending[c]) {
+                        if (cudaEventQuery(ev[c]) != cudaSuccess) continue;
+                        pending[c] = 0;
+                        ++n;
+                    }
+                    empty_kernel<<<sms * 4, 32, 0, st[c]>>>();  // occupies every SM, no work
+                    if (cudaEventRecord(ev[c], st[c]) != cudaSuccess) err[p] = 1;
+                    pending[c] = 1;
+                }
+            }
+            for (int c = 0; c < chares; ++c) {
+                cudaStreamSynchronize(st[c]);
+                cudaStreamDestroy(st[c]);
+                cudaEventDestroy(ev[c]);
+            }
+            done[p] = n;
+        });
+    for (auto &t : pes) t.join();
+    for (int p = 0; p < threads; ++p)
+        if (err[p]) return mb_fail(JAC_ECUDA, "launch-rate: event record failed");
+    long tot = 0;
+    for (long v : done) tot += v;
+    *kps = (double)tot / seconds;
+    return JAC_OK;
+}
+
+int jac_mb_pipeline(int32_t src, int32_t dst, int64_t total_bytes, int32_t odf, int32_t with_compute, double *us)
+{
+    if (!us || odf < 1 || total_bytes < 8 * (int64_t)odf) return mb_fail(JAC_EINVAL, "need odf >= 1, total_bytes >= 8*odf");
+    int ndev = 0;
+    MCK(cudaGetDeviceCount(&ndev));
+    if (src < 0 || dst < 0 || src >= ndev || dst >= ndev) return mb_fail(JAC_EDEVICE, "src/dst device not present");
+    double *a = nullptr, *b = nullptr;
+    MCK(cudaSetDevice(src));
+    MCK(cudaMalloc(&a, total_bytes));
+    MCK(cudaMemset(a, 0, total_bytes));
+    MCK(cudaSetDevice(dst));
+    MCK(cudaMalloc(&b, total_bytes));
+    if (src != dst) {
+        int can = 0;
+        MCK(cudaDeviceCanAccessPeer(&can, dst, src));
+        if (!can) return mb_fail(JAC_EDEVICE, "no peer access between devices %d and %d", src, dst);
+        cudaError_t e = cudaDeviceEnablePeerAccess(src, 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) return mb_fail(JAC_ECUDA, "enable peer access");
+        cudaGetLastError();
+    }
+    std::vector<cudaStream_t> st(odf);
+    std::vector<cudaEvent_t> ev(odf);
+    for (int k = 0; k < odf; ++k) {
+        MCK(cudaStreamCreateWithFlags(&st[k], cudaStreamNonBlocking));
+        MCK(cudaEventCreate(&ev[k]));
+    }
+    cudaStream_t s0;
+    cudaEvent_t e0;
+    MCK(cudaStreamCreateWithFlags(&s0, cudaStreamNonBlocking));
+    MCK(cudaEventCreate(&e0));
+    const int64_t chunk = (total_bytes / odf) / 8 * 8;
+    auto run = [&]() -> int {
+        MCK(cudaEventRecord(e0, s0));
+        for (int k = 0; k < odf; ++k) {
+            MCK(cudaStreamWaitEvent(st[k], e0, 0));
+            char *d = reinterpret_cast<char *>(b) + k * chunk;
+            const char *sp = reinterpret_cast<const char *>(a) + k * chunk;
+            MCK(cudaMemcpyPeerAsync(d, dst, sp, src, chunk, st[k]));
+            if (with_compute) {
+                const int64_t n = chunk / 8;
+                consume_kernel<<<(unsigned)std::min<int64_t>(1184, (n + 255) / 256), 256, 0, st[k]>>>(
+                    reinterpret_cast<double *>(d), n);
+                MCK(cudaGetLastError());
+            }
+            MCK(cudaEventRecord(ev[k], st[k]));
+        }
+        for (int k = 0; k < odf; ++k) MCK(cudaEventSynchronize(ev[k]));
+        return JAC_OK;
+    };
+    int rc;
+    for (int w = 0; w < 3; ++w)
+        if ((rc = run())) return rc;
+    double best = 1e300;
+    for (int rep = 0; rep < 5; ++rep) {
+        if ((rc = run())) return rc;
+        float mx = 0.f;
+        for (int k = 0; k < odf; ++k) {
+            float ms = 0.f;
+            MCK(cudaEventElapsedTime(&ms, e0, ev[k]));
+            mx = std::max(mx, ms);
+        }
+        best = std::min(best, (double)mx * 1e3);
+    }
+    *us = best;
+    for (int k = 0; k < odf; ++k) {
+        cudaStreamDestroy(st[k]);
+        cudaEventDestroy(ev[k]);
+    }
+    cudaStreamDestroy(s0);
+    cudaEventDestroy(e0);
+    cudaFree(b);
+    cudaSetDevice(src);
+    cudaFree(a);
+    return JAC_OK;
+}
+
+}  // extern "C"

@@ -37,6 +37,7 @@ EXPORTED = ["jac_plan", "jac_plan_face", "jac_create", "jac_create_rank", "jac_i
             "jac_get_block", "jac_get_block_padded", "jac_get_field", "jac_get_layout",
             "jac_block_owner", "jac_last_step_ms", "jac_set_init_box", "jac_get_field_box", "jac_local_box", "jac_profile_sweep", "jac_get_stats",
             "jac_destroy", "jac_last_error", "jac_version", "jac_set_option"]
+MICROBENCH_EXPORTED = ["jac_mb_launch_latency", "jac_mb_overlap", "jac_mb_launch_rate", "jac_mb_pipeline"]
 
 _ERRNAMES = {-1: "JAC_EINVAL", -2: "JAC_EDECOMP", -3: "JAC_EDEVICE", -4: "JAC_ENOMEM",
              -5: "JAC_ECUDA", -6: "JAC_ENCCL", -7: "JAC_ESTATE"}
@@ -91,6 +92,10 @@ def load() -> ctypes.CDLL:
         "jac_get_stats": [vp, P(i64)],
         "jac_destroy": [vp],
         "jac_set_option": [vp, i32, i64],
+        "jac_mb_launch_latency": [i32, i32, P(ctypes.c_double)],
+        "jac_mb_overlap": [i32, i64, i32, i32, P(ctypes.c_double), P(ctypes.c_double)],
+        "jac_mb_launch_rate": [i32, i32, i32, ctypes.c_double, P(ctypes.c_double)],
+        "jac_mb_pipeline": [i32, i32, i64, i32, i32, P(ctypes.c_double)],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -255,6 +260,31 @@ def jac_get_stats(ctx) -> dict:
 
 def jac_set_option(ctx, option: int, value: int) -> None:
     _check(load().jac_set_option(ctx, option, value), "jac_set_option")
+
+
+# ------------------------------------------------------------------ microbenchmarks (NEXT-3/4)
+def jac_mb_launch_latency(device=0, iters=2000) -> float:
+    v = ctypes.c_double()
+    _check(load().jac_mb_launch_latency(device, iters, ctypes.byref(v)), "jac_mb_launch_latency")
+    return v.value
+
+
+def jac_mb_overlap(total_threads, odf, work=1000, device=0):
+    h, d = ctypes.c_double(), ctypes.c_double()
+    _check(load().jac_mb_overlap(device, total_threads, odf, work, ctypes.byref(h), ctypes.byref(d)), "jac_mb_overlap")
+    return h.value, d.value
+
+
+def jac_mb_launch_rate(chares, threads, seconds=0.5, device=0) -> float:
+    v = ctypes.c_double()
+    _check(load().jac_mb_launch_rate(device, chares, threads, seconds, ctypes.byref(v)), "jac_mb_launch_rate")
+    return v.value
+
+
+def jac_mb_pipeline(src, dst, total_bytes, odf, with_compute=False) -> float:
+    v = ctypes.c_double()
+    _check(load().jac_mb_pipeline(src, dst, total_bytes, odf, int(bool(with_compute)), ctypes.byref(v)), "jac_mb_pipeline")
+    return v.value
 
 
 def jac_destroy(ctx) -> None:

@@ -15,8 +15,8 @@ from paper_2605_12734_b200 import jacobi3d as J
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def _header_functions():
-    src = open(os.path.join(ROOT, "include", "jacobi3d.h")).read()
+def _header_functions(name="jacobi3d.h"):
+    src = open(os.path.join(ROOT, "include", name)).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
     return sorted(set(re.findall(r"\b(jac_[a-z_]+)\s*\(", src)))
 
@@ -29,6 +29,10 @@ def test_library_exports_every_header_symbol():
         assert hasattr(L, n), n
     assert set(names) == set(J.EXPORTED)
     assert jb.jac_version() == 100
+    mb = _header_functions("jacobi3d_microbench.h")
+    assert set(mb) == set(J.MICROBENCH_EXPORTED)
+    for n in mb:
+        assert hasattr(L, n), n
 
 
 def test_library_is_in_tree_and_built_for_sm100a():
