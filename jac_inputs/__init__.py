@@ -67,6 +67,12 @@ def hash_box(nx: int, ny: int, nz: int, origin, extent, seed: int = 1) -> np.nda
     return u
 
 
+def hash_field2d(nx: int, ny: int, seed: int = 1) -> np.ndarray:
+    """Padded 2-D R11 hash field [ny+2, nx+2]: key (seed << 40) + p, p = j*(nx+2) + i."""
+    p = np.arange((ny + 2) * (nx + 2), dtype=np.uint64)
+    return hash_values(seed, p).reshape(ny + 2, nx + 2)
+
+
 def constant_field(nx: int, ny: int, nz: int, c: float) -> np.ndarray:
     """P1: every padded cell = c."""
     return np.full((nz + 2, ny + 2, nx + 2), c, dtype=np.float64)

@@ -54,6 +54,10 @@ def lib() -> ctypes.CDLL:
         L.oracle_jacobi3d_omp_timed.argtypes = [i64, i64, i64, dp, i64, dp, ctypes.c_int,
                                                  ctypes.POINTER(ctypes.c_double)]
         L.oracle_jacobi3d_omp_timed.restype = ctypes.c_int
+        L.oracle_jacobi2d.argtypes = [i64, i64, dp, i64, dp]
+        L.oracle_jacobi2d.restype = ctypes.c_int
+        L.oracle_jacobi2d_omp.argtypes = [i64, i64, dp, i64, dp, ctypes.c_int]
+        L.oracle_jacobi2d_omp.restype = ctypes.c_int
         L.oracle_checksum.argtypes = [i64, i64, i64, dp]
         L.oracle_checksum.restype = ctypes.c_double
         L.oracle_bithash.argtypes = [i64, i64, i64, dp]
@@ -104,6 +108,32 @@ def jacobi3d_omp_timed(u0: np.ndarray, n: int, nthreads: int = 0):
     if rc < 1:
         raise RuntimeError(f"oracle_jacobi3d_omp_timed failed rc={rc}")
     return out, rc, secs.value
+
+
+def _dims2(u: np.ndarray):
+    if u.dtype != np.float64 or u.ndim != 2 or not u.flags.c_contiguous:
+        raise ValueError("padded 2-D field must be a C-contiguous float64 array [ny+2, nx+2]")
+    ny2, nx2 = u.shape
+    return nx2 - 2, ny2 - 2
+
+
+def jacobi2d(u0: np.ndarray, n: int) -> np.ndarray:
+    """Jacobi2D (NEXT-1): padded 2-D field after ``n`` 5-point sweeps (serial C)."""
+    nx, ny = _dims2(u0)
+    out = np.empty_like(u0)
+    rc = lib().oracle_jacobi2d(nx, ny, _ptr(u0), int(n), _ptr(out))
+    if rc != 0:
+        raise RuntimeError(f"oracle_jacobi2d failed rc={rc}")
+    return out
+
+
+def jacobi2d_omp(u0: np.ndarray, n: int, nthreads: int = 0):
+    nx, ny = _dims2(u0)
+    out = np.empty_like(u0)
+    rc = lib().oracle_jacobi2d_omp(nx, ny, _ptr(u0), int(n), _ptr(out), int(nthreads))
+    if rc < 1:
+        raise RuntimeError(f"oracle_jacobi2d_omp failed rc={rc}")
+    return out, rc
 
 
 def checksum(u: np.ndarray) -> float:

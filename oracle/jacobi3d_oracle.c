@@ -172,6 +172,78 @@ uint64_t oracle_bithash(int64_t nx, int64_t ny, int64_t nz, const double *u)
     return h;
 }
 
+/* ------------------------------------------------------------------ Jacobi2D
+ * the paper's own stencil app, "applies the Jacobi iterative
+ * method on a 2D grid".  SPEC.md:474 fixes the update as a "5-point
+ * average into a double-buffered tile" with "fixed borders (outer halo = initial
+ * boundary values)".  Readings (DESIGN.md §2, 2-D column): mean of the 5 points,
+ * x fl(1/5) = 0x1.999999999999ap-3, fixed order ((((c + x-) + x+) + y-) + y+).
+ * Padded array (ny+2)*(nx+2), x fastest, p(i,j) = j*(nx+2) + i. */
+static const double ORACLE_K5 = 0x1.999999999999ap-3;
+
+static void sweep2d(int64_t nx, int64_t ny, const double *A, double *B, int64_t j_lo, int64_t j_hi)
+{
+    const int64_t sy = nx + 2;
+    for (int64_t j = j_lo; j <= j_hi; ++j)
+        for (int64_t i = 1; i <= nx; ++i) {
+            const int64_t p = j * (nx + 2) + i;
+            double s = A[p];       /* centre */
+            s = s + A[p - 1];      /* x- */
+            s = s + A[p + 1];      /* x+ */
+            s = s + A[p - sy];     /* y- */
+            s = s + A[p + sy];     /* y+ */
+            B[p] = s * ORACLE_K5;
+        }
+}
+
+int oracle_jacobi2d_omp(int64_t nx, int64_t ny, const double *u0, int64_t n, double *out, int nthreads)
+{
+    if (nx < 1 || ny < 1 || n < 0 || !u0 || !out) return -1;
+    const size_t cells = (size_t)(nx + 2) * (size_t)(ny + 2);
+    double *A = (double *)malloc(cells * sizeof(double));
+    double *B = (double *)malloc(cells * sizeof(double));
+    if (!A || !B) { free(A); free(B); return -2; }
+    int used = 1;
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#pragma omp parallel
+    {
+#pragma omp single
+        used = omp_get_num_threads();
+    }
+#endif
+    memcpy(A, u0, cells * sizeof(double));
+    memcpy(B, u0, cells * sizeof(double));
+    for (int64_t it = 0; it < n; ++it) {
+#ifdef _OPENMP
+#pragma omp parallel for schedule(static)
+#endif
+        for (int64_t j = 1; j <= ny; ++j) sweep2d(nx, ny, A, B, j, j);
+        double *t = A; A = B; B = t;
+    }
+    memcpy(out, A, cells * sizeof(double));
+    free(A); free(B);
+    return used;
+}
+
+int oracle_jacobi2d(int64_t nx, int64_t ny, const double *u0, int64_t n, double *out)
+{
+    if (nx < 1 || ny < 1 || n < 0 || !u0 || !out) return -1;
+    const size_t cells = (size_t)(nx + 2) * (size_t)(ny + 2);
+    double *A = (double *)malloc(cells * sizeof(double));
+    double *B = (double *)malloc(cells * sizeof(double));
+    if (!A || !B) { free(A); free(B); return -2; }
+    memcpy(A, u0, cells * sizeof(double));
+    memcpy(B, u0, cells * sizeof(double));
+    for (int64_t it = 0; it < n; ++it) {
+        sweep2d(nx, ny, A, B, 1, ny);
+        double *t = A; A = B; B = t;
+    }
+    memcpy(out, A, cells * sizeof(double));
+    free(A); free(B);
+    return 0;
+}
+
 int oracle_has_openmp(void)
 {
 #ifdef _OPENMP
