@@ -71,7 +71,7 @@ enum jac_flags {
                                      are swept by ONE kernel (no cross-partition waits);
                                      exercises the partition / REMOTE-face logic */
     JAC_F_SKIP_EXCHANGE = 1u << 7, /* timing-only ablation: no face writes. WRONG results */
-    JAC_F_PER_BLOCK = 1u << 8      /* paper-style execution: one stream per
+    JAC_F_PER_BLOCK = 1u << 8,     /* paper-style execution: one stream per
                                       block ("non-blocking per-chare streams")
                                       and, per iteration and block, one unpack launch per
                                       face, one stencil launch, one pack launch per face
@@ -79,6 +79,12 @@ enum jac_flags {
                                       Launching host threads (the paper's PEs per process,
                                       PAPER.md:95) via jac_set_option.  One GPU only
                                       (n_gpus == 1 or JAC_F_VIRTUAL_GPUS). */
+    JAC_F_2D = 1u << 9             /* Jacobi2D (the paper's evaluated app,
+                                      PAPER.md:280-294): nz == 1, bz == 1; 5-point mean
+                                      u' = ((((c + x-) + x+) + y-) + y+) * fl(1/5)
+                                      ("5-point average"); padded host
+                                      arrays are (ny+2)*(nx+2) (no z shell); hash init
+                                      key p = j*(nx+2) + i.  Fused TMA path only. */
 };
 
 /* Options for jac_set_option. */

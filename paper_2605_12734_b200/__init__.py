@@ -6,6 +6,6 @@ the ctypes binding (``jacobi3d.py``) and the one-process-per-GPU plumbing over
 torch.distributed (``dist.py``).  It never imports ``oracle/``.
 """
 from .jacobi3d import *  # noqa: F401,F403
-from .jacobi3d import Jacobi3D, JacError, load  # noqa: F401
+from .jacobi3d import Jacobi2D, Jacobi3D, JacError, load  # noqa: F401
 
 __version__ = "0.1.0"

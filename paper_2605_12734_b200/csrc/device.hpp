@@ -5,7 +5,8 @@
 // HBM layout.  Every block ("chare") owns two ghosted arrays (ping,
 // pong) of (ez+2) planes x (ey+2) rows x P doubles.  Element (i,j,k) of a block,
 // i in [-1,ex], j in [-1,ey], k in [-1,ez] (-1 and e* are ghosts), lives at
-//     base + (k+1)*Q + (j+1)*P + A + i,      Q = P*(ey+2)
+//     base + (k+zg)*Q + (j+1)*P + A + i,     Q = P*(ey+2)
+// (zg = 1; the 2-D mode, JAC_F_2D, has a single plane k = 0 and zg = 0)
 // with A = 4 so the interior row starts on a 32-byte sector (and 16-byte aligned
 // double2 accesses).  All slots of one GPU sit in one arena: slot s of buffer b
 // starts at arena + (b*nslots + s)*bstride, which lets ONE 4-D TMA tensor map
@@ -55,6 +56,8 @@ struct Geom {
     int64_t bstride;         // doubles between consecutive slots (256-byte multiple)
     int32_t nslots;          // slots per buffer in the arena
     int32_t eyp;             // x-ghost array row pitch (ey rounded up to 4)
+    int32_t zg;              // z ghost planes per side: 1 (3-D), 0 (2-D: one plane, k = 0)
+    int32_t pad_;
     int64_t xgstride;        // doubles per x-ghost array (incl. kXgPad, 256-byte multiple)
     int64_t ostride;         // outbox doubles per slot
     int64_t ooff[6];         // outbox face offsets inside a slot

@@ -181,6 +181,7 @@ int enqueue_sweep(jac_ctx *c, int src)
 {
     const jac::SweepArgs a = sweep_args(c, src, sweep_mode(c));
     if (c->variant == kPlain) CK(jac::launch_sweep_plain(a, c->stream));
+    else if (c->flags & JAC_F_2D) CK(jac::launch_sweep2d_tma(c->tmap, a, c->variant, c->stream));
     else CK(jac::launch_sweep_tma(c->tmap, a, c->variant, c->stream));
     return JAC_OK;
 }
@@ -236,7 +237,7 @@ int encode_tmap(jac_ctx *c)
     }
     const jac::Geom &g = c->geom;
     const jac::TileShape ts = jac::tma_tile_shape(c->variant);
-    const cuuint64_t dims[4] = {(cuuint64_t)g.P, (cuuint64_t)(g.ey + 2), (cuuint64_t)(g.ez + 2),
+    const cuuint64_t dims[4] = {(cuuint64_t)g.P, (cuuint64_t)(g.ey + 2), (cuuint64_t)(g.ez + 2 * g.zg),
                                 (cuuint64_t)(2 * c->nslots)};
     const cuuint64_t strides[3] = {(cuuint64_t)g.P * 8, (cuuint64_t)g.Q * 8, (cuuint64_t)g.bstride * 8};
     const cuuint32_t box[4] = {(cuuint32_t)ts.w, (cuuint32_t)(ts.by + 2), 1, 1};
@@ -276,6 +277,10 @@ int create_common(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, in
     int rc = jac::make_plan(nx, ny, nz, bx, by, bz, n_gpus, gpu_grid, &plan, &err);
     if (rc) return fail(rc, "%s", err.c_str());
     if (flags & JAC_F_NCCL) return fail(JAC_EINVAL, "flags: JAC_F_NCCL transport is not built in this version");
+    if ((flags & JAC_F_2D) && (nz != 1 || bz != 1))
+        return fail(JAC_EINVAL, "flags: JAC_F_2D needs nz == 1 and bz == 1 (the 2-D grid is nx x ny)");
+    if ((flags & JAC_F_2D) && (flags & (JAC_F_UNFUSED_PACK | JAC_F_NO_TMA | JAC_F_PER_BLOCK)))
+        return fail(JAC_EINVAL, "flags: JAC_F_2D runs the fused TMA path only (no UNFUSED_PACK / NO_TMA / PER_BLOCK)");
     if ((flags & JAC_F_PER_BLOCK) && (rank_mode || (flags & (JAC_F_UNFUSED_PACK | JAC_F_SKIP_EXCHANGE))))
         return fail(JAC_EINVAL, "flags: JAC_F_PER_BLOCK runs on one GPU (not a rank context) and excludes "
                                 "JAC_F_UNFUSED_PACK / JAC_F_SKIP_EXCHANGE");
@@ -312,7 +317,8 @@ int create_common(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, in
     if (const char *s = getenv("JAC_A")) g.A = std::max(2, atoi(s) & ~1);  // layout experiment knob
     g.P = round_up(g.A + g.ex + 4, 4);  // room for the 32-byte +x ghost sector (A % 4 == 0)
     g.Q = g.P * (g.ey + 2);
-    g.bstride = round_up(g.Q * (g.ez + 2), 32);
+    g.zg = (flags & JAC_F_2D) ? 0 : 1;
+    g.bstride = round_up(g.Q * (g.ez + 2 * g.zg), 32);
     g.nslots = c->nslots;
     g.eyp = (int32_t)round_up(g.ey, 4);
     g.xgstride = round_up((int64_t)g.eyp * g.ez + jac::kXgPad, 32);
@@ -365,6 +371,10 @@ int create_common(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, in
         int gcols = resident;
         if (const char *s = getenv("JAC_GCOLS")) gcols = atoi(s);
         c->gcols = std::max(1, std::min(c->ncols, gcols > 0 ? gcols : c->ncols));
+        if (flags & JAC_F_2D) {  // 2-D: items = (block, x tile, chunk of 8 y tiles), nzc = y chunks
+            c->nzc = std::max(1, (c->nty + 7) / 8);
+            c->nitems = c->nslots * c->ntx * c->nzc;
+        }
     }
     if (const char *s = getenv("JAC_UNROLL")) c->unroll = std::max(2, atoi(s) & ~1);
     if ((int64_t)c->nslots * c->ntx * c->nty * c->ntz > 0x7fffffffLL) {
@@ -434,6 +444,8 @@ int create_common(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, in
     if (c->variant != kPlain) {
         if ((rc = encode_tmap(c))) return bail(rc);
         if (jac::prepare_sweep_tma(c->variant) != cudaSuccess) return bail(fail(JAC_ECUDA, "sweep kernel attribute"));
+        if ((flags & JAC_F_2D) && jac::prepare_sweep2d_tma(c->variant) != cudaSuccess)
+            return bail(fail(JAC_ECUDA, "2-D sweep kernel attribute"));
     }
     if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess)
@@ -723,7 +735,7 @@ int jac_local_box(const jac_ctx *c, int64_t *origin, int64_t *extent)
     for (const jac::DevBlock &d : c->hblocks)
         for (int k = 0; k < 3; ++k) {
             lo[k] = std::min<int64_t>(lo[k], d.org[k]);
-            hi[k] = std::max<int64_t>(hi[k], d.org[k] + p.e[k] + 2);
+            hi[k] = std::max<int64_t>(hi[k], d.org[k] + p.e[k] + (k == 2 ? 2 * c->geom.zg : 2));
         }
     for (int k = 0; k < 3; ++k) { origin[k] = lo[k]; extent[k] = hi[k] - lo[k]; }
     return JAC_OK;
@@ -737,7 +749,7 @@ int check_box(const jac_ctx *c, const void *box, const int64_t *origin, const in
     jac_local_box(c, lo, ex);
     for (int k = 0; k < 3; ++k)
         if (origin[k] < 0 || extent[k] < 1 || origin[k] > lo[k] || origin[k] + extent[k] < lo[k] + ex[k] ||
-            origin[k] + extent[k] > c->plan.n[k] + 2)
+            origin[k] + extent[k] > c->plan.n[k] + (k == 2 ? 2 * c->geom.zg : 2))
             return fail(JAC_EINVAL, "box origin/extent (dim %d: %lld+%lld) does not cover the local blocks (%lld+%lld)",
                         k, (long long)origin[k], (long long)extent[k], (long long)lo[k], (long long)ex[k]);
     return JAC_OK;
@@ -761,7 +773,7 @@ int jac_set_init_box(jac_ctx *c, const double *box, const int64_t *origin, const
                                 (size_t)(d.org[2] - origin[2]));
         m.dstPtr = make_cudaPitchedPtr(c->slot_ptr(0, s), (size_t)g.P * 8, (size_t)g.P, (size_t)(g.ey + 2));
         m.dstPos = make_cudaPos((size_t)(g.A - 1) * 8, 0, 0);
-        m.extent = make_cudaExtent((size_t)(g.ex + 2) * 8, (size_t)(g.ey + 2), (size_t)(g.ez + 2));
+        m.extent = make_cudaExtent((size_t)(g.ex + 2) * 8, (size_t)(g.ey + 2), (size_t)(g.ez + 2 * g.zg));
         m.kind = cudaMemcpyHostToDevice;
         CK(cudaMemcpy3DAsync(&m, c->stream));
     }
@@ -776,7 +788,7 @@ int jac_set_init(jac_ctx *c, const double *padded)
     if (!c) return fail(JAC_EINVAL, "ctx is NULL");
     if (!padded) return fail(JAC_EINVAL, "padded is NULL");
     const int64_t o[3] = {0, 0, 0};
-    const int64_t e[3] = {c->plan.n[0] + 2, c->plan.n[1] + 2, c->plan.n[2] + 2};
+    const int64_t e[3] = {c->plan.n[0] + 2, c->plan.n[1] + 2, c->plan.n[2] + 2 * c->geom.zg};
     return jac_set_init_box(c, padded, o, e);
 }
 
@@ -892,7 +904,7 @@ int jac_get_block_padded(jac_ctx *c, int32_t ix, int32_t iy, int32_t iz, double 
     m.srcPtr = make_cudaPitchedPtr(c->slot_ptr((int)(c->iters & 1), s), (size_t)g.P * 8, (size_t)g.P, (size_t)(g.ey + 2));
     m.srcPos = make_cudaPos((size_t)(g.A - 1) * 8, 0, 0);
     m.dstPtr = make_cudaPitchedPtr(out, (size_t)(g.ex + 2) * 8, (size_t)(g.ex + 2), (size_t)(g.ey + 2));
-    m.extent = make_cudaExtent((size_t)(g.ex + 2) * 8, (size_t)(g.ey + 2), (size_t)(g.ez + 2));
+    m.extent = make_cudaExtent((size_t)(g.ex + 2) * 8, (size_t)(g.ey + 2), (size_t)(g.ez + 2 * g.zg));
     m.kind = cudaMemcpyDeviceToHost;
     CK(cudaMemcpy3DAsync(&m, c->stream));
     // the x ghosts live in the x-ghost arrays: patch columns 0 and ex+1 (interior j, k)
@@ -905,8 +917,8 @@ int jac_get_block_padded(jac_ctx *c, int32_t ix, int32_t iy, int32_t iz, double 
     const int64_t sx = g.ex + 2, sxy = sx * (g.ey + 2);
     for (int64_t k = 0; k < g.ez; ++k)
         for (int64_t j = 0; j < g.ey; ++j) {
-            out[(k + 1) * sxy + (j + 1) * sx] = xgh[k * g.eyp + j];
-            out[(k + 1) * sxy + (j + 1) * sx + g.ex + 1] = xgh[(size_t)g.ez * g.eyp + k * g.eyp + j];
+            out[(k + g.zg) * sxy + (j + 1) * sx] = xgh[k * g.eyp + j];
+            out[(k + g.zg) * sxy + (j + 1) * sx + g.ex + 1] = xgh[(size_t)g.ez * g.eyp + k * g.eyp + j];
         }
     return JAC_OK;
 }
@@ -921,7 +933,7 @@ int jac_get_block(jac_ctx *c, int32_t ix, int32_t iy, int32_t iz, double *out)
     const jac::Geom &g = c->geom;
     cudaMemcpy3DParms m{};
     m.srcPtr = make_cudaPitchedPtr(c->slot_ptr((int)(c->iters & 1), s), (size_t)g.P * 8, (size_t)g.P, (size_t)(g.ey + 2));
-    m.srcPos = make_cudaPos((size_t)g.A * 8, 1, 1);
+    m.srcPos = make_cudaPos((size_t)g.A * 8, 1, (size_t)g.zg);
     m.dstPtr = make_cudaPitchedPtr(out, (size_t)g.ex * 8, (size_t)g.ex, (size_t)g.ey);
     m.extent = make_cudaExtent((size_t)g.ex * 8, (size_t)g.ey, (size_t)g.ez);
     m.kind = cudaMemcpyDeviceToHost;
@@ -941,10 +953,10 @@ int jac_get_field_box(jac_ctx *c, double *box, const int64_t *origin, const int6
         const jac::DevBlock &d = c->hblocks[s];
         cudaMemcpy3DParms m{};
         m.srcPtr = make_cudaPitchedPtr(c->slot_ptr((int)(c->iters & 1), s), (size_t)g.P * 8, (size_t)g.P, (size_t)(g.ey + 2));
-        m.srcPos = make_cudaPos((size_t)g.A * 8, 1, 1);
+        m.srcPos = make_cudaPos((size_t)g.A * 8, 1, (size_t)g.zg);
         m.dstPtr = make_cudaPitchedPtr(box, (size_t)extent[0] * 8, (size_t)extent[0], (size_t)extent[1]);
         m.dstPos = make_cudaPos((size_t)(d.org[0] + 1 - origin[0]) * 8, (size_t)(d.org[1] + 1 - origin[1]),
-                                (size_t)(d.org[2] + 1 - origin[2]));
+                                (size_t)(d.org[2] + g.zg - origin[2]));
         m.extent = make_cudaExtent((size_t)g.ex * 8, (size_t)g.ey, (size_t)g.ez);
         m.kind = cudaMemcpyDeviceToHost;
         CK(cudaMemcpy3DAsync(&m, c->stream));
@@ -958,7 +970,7 @@ int jac_get_field(jac_ctx *c, double *padded)
     if (!c) return fail(JAC_EINVAL, "ctx is NULL");
     if (!padded) return fail(JAC_EINVAL, "padded is NULL");
     const int64_t o[3] = {0, 0, 0};
-    const int64_t e[3] = {c->plan.n[0] + 2, c->plan.n[1] + 2, c->plan.n[2] + 2};
+    const int64_t e[3] = {c->plan.n[0] + 2, c->plan.n[1] + 2, c->plan.n[2] + 2 * c->geom.zg};
     return jac_get_field_box(c, padded, o, e);
 }
 

@@ -63,6 +63,7 @@ __device__ __forceinline__ void st_pair(double *p, double2 v, bool both)
 // j < ey and 0 <= k < ez; i may be past the ragged x edge.  `blk` should live in
 // shared memory or registers: global stores would otherwise force the compiler to
 // re-load it after every store.
+template <bool HAS_Z = true>
 __device__ __forceinline__ void emit_pair(const SweepArgs &a, const DevBlock &blk, int dst, double *own_plane,
                                           int64_t rowoff, int i, int j, int k, double2 v)
 {
@@ -71,7 +72,7 @@ __device__ __forceinline__ void emit_pair(const SweepArgs &a, const DevBlock &bl
     const bool both = (i + 1) < g.ex;
     st_pair(own_plane + rowoff, v, both);
     if (a.mode == MODE_NOEXCHANGE) return;
-    const bool zface = (k == 0) || (k == g.ez - 1);
+    const bool zface = HAS_Z && ((k == 0) || (k == g.ez - 1));
     const bool yface = (j == 0) || (j == g.ey - 1);
     const bool last_x = (i == g.ex - 1) || (both && i + 1 == g.ex - 1);
     const bool xface = (i == 0) || last_x;
@@ -94,11 +95,11 @@ __device__ __forceinline__ void emit_pair(const SweepArgs &a, const DevBlock &bl
         if (yface) {
             if (j == 0) {
                 double *p = blk.nb[YM][dst];
-                if (p) st_pair(p + (int64_t)(k + 1) * g.Q + (int64_t)(g.ey + 1) * g.P + g.A + i, v, both);
+                if (p) st_pair(p + (int64_t)(k + g.zg) * g.Q + (int64_t)(g.ey + 1) * g.P + g.A + i, v, both);
             }
             if (j == g.ey - 1) {
                 double *p = blk.nb[YP][dst];
-                if (p) st_pair(p + (int64_t)(k + 1) * g.Q + g.A + i, v, both);
+                if (p) st_pair(p + (int64_t)(k + g.zg) * g.Q + g.A + i, v, both);
             }
         }
         // x faces: into the neighbour's contiguous x-ghost array; the 16 rows of a
@@ -379,6 +380,104 @@ __global__ void __launch_bounds__(NT, 4) sweep_tma_kernel(const __grid_constant_
     }
 }
 
+// ------------------------------------------------------------------ Jacobi2D sweep
+// NEXT-1 (JAC_F_2D): u' = ((((c + x-) + x+) + y-) + y+) * fl(1/5) on one plane.
+// Work item = (block, 64-wide x tile, chunk of 16-row y tiles), x tile fastest.  The
+// CTA marches its chunk in y: one staged box per y tile (rows y0-1 .. y0+16, i.e. the
+// y halo or the block's ghost rows, plus the in-block x halo), the block-edge x ghosts
+// by bulk copy, a 4-deep TMA ring of tiles in flight.  Same fused direct-to-ghost
+// epilogue as the 3-D sweep (no z faces).
+__device__ __forceinline__ double stencil5(double c, double xm, double xp, double ym, double yp)
+{
+    constexpr double K5 = 0x1.999999999999ap-3;  // fl(1/5)
+    double s = __dadd_rn(c, xm);
+    s = __dadd_rn(s, xp);
+    s = __dadd_rn(s, ym);
+    s = __dadd_rn(s, yp);
+    return __dmul_rn(s, K5);
+}
+
+template <int BX, int BY, int W, int NT, int NS>
+__global__ void __launch_bounds__(NT, 4) sweep2d_tma_kernel(const __grid_constant__ CUtensorMap tmap,
+                                                            const SweepArgs a)
+{
+    using L = StageLayout<BX, BY, W>;
+    constexpr int TXL = BX / 2;
+    constexpr int NRG = NT / TXL;
+    constexpr int RY = BY / NRG;
+    static_assert(RY >= 1 && RY * NRG == BY, "tile shape");
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    double *stage = reinterpret_cast<double *>(smem_raw);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + NS * L::STRIDE * sizeof(double));
+
+    const Geom &g = a.g;
+    int item = blockIdx.x;
+    const int tx = item % a.ntx; item /= a.ntx;
+    const int yc = item % a.nzc;  // y chunk
+    const int b = item / a.nzc;
+    const int tpc = (a.nty + a.nzc - 1) / a.nzc;  // y tiles per chunk
+    const int ty0 = yc * tpc;
+    const int nq = max(0, min(a.nty, ty0 + tpc) - ty0);
+    const int x0 = tx * BX;
+    __shared__ DevBlock blk;
+    if (threadIdx.x == 0) blk = a.blocks[b];
+    const int soff = tile_soff<BX, W>(g, x0);
+    const int c0 = g.A + x0 - soff;
+    const bool xlo = (x0 == 0), xhi = (x0 + BX >= g.ex);
+    int c3 = 0;
+    const double *xg0 = nullptr, *xg1 = nullptr;
+    auto issue = [&](int q) {
+        double *st = stage + (q % NS) * L::STRIDE;
+        uint64_t *bar = &bars[q % NS];
+        const int y0 = (ty0 + q) * BY;
+        mbar_expect(bar, L::BOX_BYTES + (xlo ? L::XG_BYTES : 0) + (xhi ? L::XG_BYTES : 0));
+        tma_box(&tmap, st, bar, c0, y0, 0, c3);
+        if (xlo) bulk_copy(st + L::XG_OFF, xg0 + y0, L::XG_BYTES, bar);
+        if (xhi) bulk_copy(st + L::XG_OFF + BY, xg1 + y0, L::XG_BYTES, bar);
+    };
+    if (threadIdx.x == 0) {
+        const int slot = a.blocks[b].slot;
+        c3 = a.src * g.nslots + slot;
+        xg0 = xg_array(a.xg, g, a.src, slot, 0);
+        xg1 = xg_array(a.xg, g, a.src, slot, 1);
+        for (int s = 0; s < NS; ++s) mbar_init(&bars[s], 1);
+        mbar_fence_init();
+        for (int q = 0; q < NS && q < nq; ++q) issue(q);
+    }
+    __syncthreads();
+
+    const int lane = threadIdx.x % TXL;
+    const int rg = threadIdx.x / TXL;
+    const int col = soff + 2 * lane;
+    const int i = x0 + 2 * lane;
+    const int dst = 1 - a.src;
+    const bool ilo = (i == 0), ihi0 = (i == g.ex - 1), ihi1 = (i + 1 == g.ex - 1);
+    double *own = a.arena + (int64_t)(dst * g.nslots + blk.slot) * g.bstride;  // plane k = 0 (zg = 0)
+    for (int q = 0; q < nq; ++q) {
+        mbar_wait(&bars[q % NS], (q / NS) & 1);
+        const double *S = stage + (q % NS) * L::STRIDE;
+        const int y0 = (ty0 + q) * BY;
+#pragma unroll
+        for (int r = 0; r < RY; ++r) {
+            const int jl = rg * RY + r;
+            const double *row = S + (jl + 1) * W + col;
+            const double2 c = *reinterpret_cast<const double2 *>(row);
+            const double xm = ilo ? S[L::XG_OFF + jl] : row[-1];
+            const double xp1 = ihi1 ? S[L::XG_OFF + BY + jl] : row[2];
+            const double xp0 = ihi0 ? S[L::XG_OFF + BY + jl] : c.y;
+            const double2 ym = *reinterpret_cast<const double2 *>(row - W);
+            const double2 yp = *reinterpret_cast<const double2 *>(row + W);
+            double2 v;
+            v.x = stencil5(c.x, xm, xp0, ym.x, yp.x);
+            v.y = stencil5(c.y, c.x, xp1, ym.y, yp.y);
+            const int j = y0 + jl;
+            if (j < g.ey) emit_pair<false>(a, blk, dst, own, (int64_t)(j + 1) * g.P + g.A + i, i, j, 0, v);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0 && q + NS < nq) issue(q + NS);
+    }
+}
+
 // ------------------------------------------------------------------ plain sweep
 // JAC_F_NO_TMA: each thread reads its 7 neighbours from global memory (L1/L2 serve
 // the reuse).  Tile 64 x 8 points, z-chunk of a.zc planes.
@@ -562,7 +661,7 @@ __global__ void xghost_extract_kernel(const SweepArgs a)
     const int64_t n = (int64_t)g.ey * g.ez;
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
         const int64_t k = e / g.ey, j = e % g.ey;
-        const int64_t row = (k + 1) * g.Q + (j + 1) * g.P + g.A;
+        const int64_t row = (k + g.zg) * g.Q + (j + 1) * g.P + g.A;
         const double lo = b0[row - 1], hi = b0[row + g.ex];
         for (int buf = 0; buf < 2; ++buf) {
             xg_array(a.xg, g, buf, blk.slot, 0)[k * g.eyp + j] = lo;
@@ -586,7 +685,7 @@ __global__ void hash_init_kernel(const SweepArgs a, int64_t nx, int64_t ny, uint
     const Geom &g = a.g;
     const DevBlock &blk = a.blocks[blockIdx.y];
     const int64_t sx = g.ex + 2, sy = g.ey + 2;
-    const int64_t n = sx * sy * (g.ez + 2);
+    const int64_t n = sx * sy * (g.ez + 2 * g.zg);
     double *b0 = a.arena + (int64_t)blk.slot * g.bstride;
     double *b1 = a.arena + (int64_t)(g.nslots + blk.slot) * g.bstride;
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
@@ -675,6 +774,37 @@ cudaError_t launch_sweep_tma(const CUtensorMap &tm, const SweepArgs &a, int vari
 {
 #define X(V, BX, BY, W, NT, NS) \
     if (variant == V) return launch_tma_t<BX, BY, W, NT, NS>(tm, a, s);
+    JAC_TMA_VARIANTS(X)
+#undef X
+    return cudaErrorInvalidValue;
+}
+
+template <int BX, int BY, int W, int NT, int NS>
+static cudaError_t launch2d_t(const CUtensorMap &tm, const SweepArgs &a, cudaStream_t s, bool prepare_only)
+{
+    constexpr size_t smem = tma_smem_bytes(BX, BY, W, NS);
+    if (prepare_only)
+        return cudaFuncSetAttribute(sweep2d_tma_kernel<BX, BY, W, NT, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem);
+    sweep2d_tma_kernel<BX, BY, W, NT, NS><<<(unsigned)a.nitems, NT, smem, s>>>(tm, a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sweep2d_tma(const CUtensorMap &tm, const SweepArgs &a, int variant, cudaStream_t s)
+{
+#define X(V, BX, BY, W, NT, NS) \
+    if (variant == V) return launch2d_t<BX, BY, W, NT, NS>(tm, a, s, false);
+    JAC_TMA_VARIANTS(X)
+#undef X
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t prepare_sweep2d_tma(int variant)
+{
+    const CUtensorMap *none = nullptr;
+    SweepArgs dummy{};
+#define X(V, BX, BY, W, NT, NS) \
+    if (variant == V) return launch2d_t<BX, BY, W, NT, NS>(*none, dummy, nullptr, true);
     JAC_TMA_VARIANTS(X)
 #undef X
     return cudaErrorInvalidValue;

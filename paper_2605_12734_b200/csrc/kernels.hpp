@@ -19,6 +19,8 @@ TileShape tma_tile_shape(int variant);
 cudaError_t prepare_sweep_tma(int variant);   // sets the dynamic-smem attribute (current device)
 int sweep_resident_ctas(int variant);         // SMs x resident CTAs of the TMA sweep (current device)
 cudaError_t launch_sweep_tma(const CUtensorMap &tm, const SweepArgs &a, int variant, cudaStream_t s);
+cudaError_t launch_sweep2d_tma(const CUtensorMap &tm, const SweepArgs &a, int variant, cudaStream_t s);
+cudaError_t prepare_sweep2d_tma(int variant);
 cudaError_t launch_sweep_plain(const SweepArgs &a, cudaStream_t s);  // 64 x 8 tiles
 cudaError_t launch_sweep_plain_one(const SweepArgs &a, cudaStream_t s);  // a.blocks = one block
 cudaError_t launch_ghost_fill(const SweepArgs &a, int dst, cudaStream_t s);

@@ -28,6 +28,7 @@ JAC_F_NO_TMA = 1 << 5
 JAC_F_VIRTUAL_GPUS = 1 << 6
 JAC_F_SKIP_EXCHANGE = 1 << 7
 JAC_F_PER_BLOCK = 1 << 8
+JAC_F_2D = 1 << 9
 JAC_OPT_LAUNCH_THREADS = 1
 JAC_FACE_BOUNDARY, JAC_FACE_LOCAL, JAC_FACE_REMOTE = 0, 1, 2
 STAT_NAMES = ["kernel_launches", "graph_launches", "kernels_per_iter", "local_blocks",
@@ -388,3 +389,36 @@ class Jacobi3D:
             self.close()
         except Exception:
             pass
+
+
+class Jacobi2D(Jacobi3D):
+    """Jacobi2D (NEXT-1) through the same library: dims (nx, ny), blocks (bx, by);
+    padded arrays are [ny+2, nx+2]."""
+
+    def __init__(self, dims, blocks, n_gpus=1, gpu_grid=None, flags=0, rank=None, device=0):
+        g = None if gpu_grid is None else (int(gpu_grid[0]), int(gpu_grid[1]), 1)
+        super().__init__((dims[0], dims[1], 1), (blocks[0], blocks[1], 1), n_gpus=n_gpus, gpu_grid=g,
+                         flags=flags | JAC_F_2D, rank=rank, device=device)
+
+    def set_init(self, padded: np.ndarray) -> None:
+        jac_set_init(self.ctx, np.ascontiguousarray(padded).reshape(1, *padded.shape))
+
+    def set_init_box(self, box: np.ndarray, origin) -> None:
+        b = box if box.ndim == 3 else np.ascontiguousarray(box).reshape(1, *box.shape)
+        o = tuple(origin) + (0,) * (3 - len(tuple(origin)))
+        jac_set_init_box(self.ctx, b, o)
+
+    def field(self, like: np.ndarray) -> np.ndarray:
+        out = np.array(like, dtype=np.float64, copy=True).reshape(1, *like.shape)
+        return jac_get_field(self.ctx, out).reshape(like.shape)
+
+    def field_box(self, box: np.ndarray, origin) -> np.ndarray:
+        b = box if box.ndim == 3 else box.reshape(1, *box.shape)
+        o = tuple(origin) + (0,) * (3 - len(tuple(origin)))
+        return jac_get_field_box(self.ctx, b, o).reshape(box.shape)
+
+    def block(self, ix, iy) -> np.ndarray:
+        return super().block(ix, iy, 0)[0]
+
+    def block_padded(self, ix, iy) -> np.ndarray:
+        return super().block_padded(ix, iy, 0)[0]

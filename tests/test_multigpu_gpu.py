@@ -26,6 +26,8 @@ CASES = [
     (4, (64, 64, 64), (2, 2, 4), None, 13, 0, False),          # 1x2x2
     (4, (64, 64, 64), (4, 2, 2), (2, 2, 1), 6, 1 << 5, False), # no TMA
     (8, (64, 64, 64), (4, 4, 4), None, 17, 0, False),          # 2x2x2, ODF 8
+    (2, (256, 192, 1), (2, 4, 1), None, 13, 1 << 9, False),    # Jacobi2D, y split
+    (4, (256, 192, 1), (4, 4, 1), None, 9, 1 << 9, True),      # Jacobi2D, 2x2 GPUs, hash init
 ]
 
 
@@ -46,6 +48,8 @@ def test_multi_process_parity(case):
         cmd += ["--grid", *map(str, grid)]
     if hashed:
         cmd += ["--hash-init"]
+    if flags & (1 << 9):
+        cmd += ["--two-d"]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "OK" in r.stdout
