@@ -17,6 +17,7 @@ uniform dense fp64 grid, fixed iteration count, no convergence check, PAPER.md:2
   c3            configs[2]: 768^3 per GPU, ODF 8, weak scaling.
   c4            configs[3]: 1536^3 global, ODF --odf (1 or 16), strong scaling.
   c5            configs[4]: 1024^3 global, 32^3 blocks, strong scaling.
+  j2d           NEXT-1: the paper's Jacobi2D, 32768^2 per GPU, ODF --odf, weak.
 Inputs are larger than L2 (>= 2 x 1.07 GB per GPU), so no L2 flush is needed.
 
 N > 1: launched by torchrun, one process per GPU; ranks exchange IPC records once
@@ -42,6 +43,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
+MODE_2D = [False]  # set for --config j2d
 BYTES_PER_LUP = 16  # algorithmic HBM bytes per lattice update: 8 B read + 8 B write
 FLOPS_PER_LUP = 7
 
@@ -90,6 +92,24 @@ def workload(cfg, n, odf):
         dims = tuple(box[d] * g[d] for d in range(3))
         blocks = tuple(lb[d] * g[d] for d in range(3))
         return dims, blocks, g, f"jacobi3d_{box[0]}^3_per_gpu_odf{odf}", "weak"
+    if cfg == "j2d":  # NEXT-1: the paper's Jacobi2D, 32768^2 per GPU, weak
+        box = (32768, 32768)
+        g2 = [1, 1]
+        m, d = n, 1
+        while m > 1:  # the global grid doubles y, then x ("alternately increased")
+            g2[d] *= 2
+            d ^= 1
+            m //= 2
+        b = [1, 1]
+        e = list(box)
+        left = odf
+        while left > 1:
+            k = 1 if e[1] >= e[0] else 0
+            e[k] //= 2
+            b[k] *= 2
+            left //= 2
+        dims = (box[0] * g2[0], box[1] * g2[1], 1)
+        return dims, (b[0] * g2[0], b[1] * g2[1], 1), (g2[0], g2[1], 1), f"jacobi2d_32768^2_per_gpu_odf{odf}", "weak"
     if cfg == "c4":
         dims = (1536, 1536, 1536)
         g = weak_gpu_grid(n)
@@ -243,6 +263,32 @@ def cpu_oracle(box=(512, 512, 512), n_target=None, budget_s=15.0, steps=None, wa
                       f"threads, iteration loop only", "ms_per_iter": 1e3 * secs / n, "nproc": os.cpu_count()}
 
 
+def cpu_oracle_2d(box=(8192, 8192), steps=None, warmup=0, budget_s=15.0):
+    """Times the 2-D oracle as it stands (OpenMP over y, all host cores)."""
+    import jac_inputs as JI
+    import oracle
+
+    nx, ny = box
+    u0 = JI.hash_field2d(nx, ny, seed=1)
+    cores = os.cpu_count() or 1
+    if steps is None:
+        t0 = time.perf_counter()
+        oracle.jacobi2d_omp(u0, 1, cores)
+        t1 = time.perf_counter() - t0
+        n = max(2, min(100, int(budget_s / max(t1, 1e-6))))
+    else:
+        if warmup:
+            oracle.jacobi2d_omp(u0, warmup, cores)
+        n = steps
+    t0 = time.perf_counter()
+    _, threads = oracle.jacobi2d_omp(u0, n, cores)
+    secs = time.perf_counter() - t0
+    return {"value": nx * ny * n / secs / 1e9, "unit": "GLUP/s", "cores": threads, "kind": "oracle",
+            "sample": f"{nx}x{ny} 2-D grid, {n} iterations, OpenMP over y on {threads} threads "
+                      f"(call time incl. the oracle's two array copies)", "ms_per_iter": 1e3 * secs / n,
+            "nproc": os.cpu_count()}
+
+
 def run_reference(args, D):
     D.init(need_gpu=False)
     if D.rank != 0:
@@ -250,9 +296,13 @@ def run_reference(args, D):
         return
     dims, blocks, g, label, scaling = workload(args.config, args.gpus, args.odf)
     box = tuple(dims[d] // g[d] for d in range(3))
-    if args.config in ("c4", "c5"):
-        box = (512, 512, 512)  # bounded sample of a strong-scaling grid
-    cb = cpu_oracle(box=box, steps=args.steps, warmup=args.warmup)
+    if args.config in ("c4", "c5", "j2d"):
+        box = (512, 512, 512)  # bounded sample (j2d: the 3-D oracle's box)
+    if args.config == "j2d":
+        box = (8192, 8192)
+        cb = cpu_oracle_2d(box=box, steps=args.steps, warmup=args.warmup)
+    else:
+        cb = cpu_oracle(box=box, steps=args.steps, warmup=args.warmup)
     line = {"impl": "reference", "metric": "Jacobi3D GLUP/s (whole job)", "value": cb["value"],
             "unit": "GLUP/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": cb["ms_per_iter"], "higher_is_better": True, "scaling": scaling,
@@ -287,6 +337,8 @@ def time_ctx(J, K, W, D, sampler=None):
 
 def make_ctx(dims, blocks, g, D, flags=0):
     import paper_2605_12734_b200 as jb
+    if dims[2] == 1 and blocks[2] == 1 and MODE_2D[0]:
+        flags |= 1 << 9  # JAC_F_2D
     if D.world > 1:
         from paper_2605_12734_b200.dist import create_rank_context
         return create_rank_context(dims, blocks, gpu_grid=g, flags=flags, device=D.local)
@@ -311,6 +363,7 @@ def run_ours(args, D):
     from paper_2605_12734_b200 import jacobi3d as JB
 
     K, W = args.steps, max(3, args.warmup)
+    MODE_2D[0] = args.config == "j2d"
     dims, blocks, g, label, scaling = workload(args.config, args.gpus, args.odf)
     pts = dims[0] * dims[1] * dims[2]
     pts_gpu = pts // args.gpus
@@ -333,7 +386,12 @@ def run_ours(args, D):
     import jac_inputs as JI
     origin, extent = J.local_box()
     host_in = torch.empty((extent[2], extent[1], extent[0]), dtype=torch.float64, pin_memory=True).numpy()
-    host_in[...] = JI.hash_box(*dims, origin, extent, seed=1)
+    if MODE_2D[0]:
+        host_in[0] = JI.hash_values(1, (np.arange(origin[1], origin[1] + extent[1], dtype=np.uint64)[:, None]
+                                        * np.uint64(dims[0] + 2)
+                                        + np.arange(origin[0], origin[0] + extent[0], dtype=np.uint64)[None, :]))
+    else:
+        host_in[...] = JI.hash_box(*dims, origin, extent, seed=1)
     host_out = torch.empty_like(torch.from_numpy(host_in), pin_memory=True).numpy()
     D.barrier()
     t0 = time.perf_counter()
@@ -395,7 +453,10 @@ def run_ours(args, D):
 
     cpu = None
     if args.gpus == 1 and D.rank == 0 and not args.no_cpu:
-        cpu = cpu_oracle(box=(512, 512, 512), budget_s=args.cpu_budget)
+        if MODE_2D[0]:
+            cpu = cpu_oracle_2d(box=(8192, 8192), budget_s=args.cpu_budget)
+        else:
+            cpu = cpu_oracle(box=(512, 512, 512), budget_s=args.cpu_budget)
 
     if D.rank == 0:
         line = {
@@ -439,7 +500,7 @@ def main():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=["c2", "c3", "c4", "c5"])
+    ap.add_argument("--config", default="c2", choices=["c2", "c3", "c4", "c5", "j2d"])
     ap.add_argument("--odf", type=int, default=8)
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
