@@ -58,6 +58,8 @@ def lib() -> ctypes.CDLL:
         L.oracle_jacobi2d.restype = ctypes.c_int
         L.oracle_jacobi2d_omp.argtypes = [i64, i64, dp, i64, dp, ctypes.c_int]
         L.oracle_jacobi2d_omp.restype = ctypes.c_int
+        L.oracle_jacobi2d_omp_timed.argtypes = [i64, i64, dp, i64, dp, ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
+        L.oracle_jacobi2d_omp_timed.restype = ctypes.c_int
         L.oracle_checksum.argtypes = [i64, i64, i64, dp]
         L.oracle_checksum.restype = ctypes.c_double
         L.oracle_bithash.argtypes = [i64, i64, i64, dp]
@@ -134,6 +136,17 @@ def jacobi2d_omp(u0: np.ndarray, n: int, nthreads: int = 0):
     if rc < 1:
         raise RuntimeError(f"oracle_jacobi2d_omp failed rc={rc}")
     return out, rc
+
+
+def jacobi2d_omp_timed(u0: np.ndarray, n: int, nthreads: int = 0):
+    """Returns (field, threads_used, seconds of the iteration loop alone)."""
+    nx, ny = _dims2(u0)
+    out = np.empty_like(u0)
+    secs = ctypes.c_double()
+    rc = lib().oracle_jacobi2d_omp_timed(nx, ny, _ptr(u0), int(n), _ptr(out), int(nthreads), ctypes.byref(secs))
+    if rc < 1:
+        raise RuntimeError(f"oracle_jacobi2d_omp_timed failed rc={rc}")
+    return out, rc, secs.value
 
 
 def checksum(u: np.ndarray) -> float:

@@ -196,7 +196,18 @@ static void sweep2d(int64_t nx, int64_t ny, const double *A, double *B, int64_t 
         }
 }
 
+int oracle_jacobi2d_omp_timed(int64_t nx, int64_t ny, const double *u0, int64_t n, double *out, int nthreads,
+                              double *loop_seconds);
+
 int oracle_jacobi2d_omp(int64_t nx, int64_t ny, const double *u0, int64_t n, double *out, int nthreads)
+{
+    return oracle_jacobi2d_omp_timed(nx, ny, u0, n, out, nthreads, 0);
+}
+
+/* As oracle_jacobi2d_omp; *loop_seconds (if non-NULL) = wall time of the iteration
+ * loop alone (for the bench's CPU baseline). */
+int oracle_jacobi2d_omp_timed(int64_t nx, int64_t ny, const double *u0, int64_t n, double *out, int nthreads,
+                              double *loop_seconds)
 {
     if (nx < 1 || ny < 1 || n < 0 || !u0 || !out) return -1;
     const size_t cells = (size_t)(nx + 2) * (size_t)(ny + 2);
@@ -214,6 +225,7 @@ int oracle_jacobi2d_omp(int64_t nx, int64_t ny, const double *u0, int64_t n, dou
 #endif
     memcpy(A, u0, cells * sizeof(double));
     memcpy(B, u0, cells * sizeof(double));
+    const double t0 = now_s();
     for (int64_t it = 0; it < n; ++it) {
 #ifdef _OPENMP
 #pragma omp parallel for schedule(static)
@@ -221,6 +233,7 @@ int oracle_jacobi2d_omp(int64_t nx, int64_t ny, const double *u0, int64_t n, dou
         for (int64_t j = 1; j <= ny; ++j) sweep2d(nx, ny, A, B, j, j);
         double *t = A; A = B; B = t;
     }
+    if (loop_seconds) *loop_seconds = now_s() - t0;
     memcpy(out, A, cells * sizeof(double));
     free(A); free(B);
     return used;
