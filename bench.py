@@ -456,7 +456,7 @@ def run_ours(args, D):
 
     if D.rank == 0:
         line = {
-            "metric": "Jacobi3D GLUP/s (whole job)", "value": value, "unit": "GLUP/s", "n_gpus": args.gpus,
+            "metric": ("Jacobi2D" if MODE_2D[0] else "Jacobi3D") + " GLUP/s (whole job)", "value": value, "unit": "GLUP/s", "n_gpus": args.gpus,
             "steps": K, "warmup": W, "ms_per_step": ms_iter, "higher_is_better": True, "scaling": scaling,
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (R11 splitmix64 hash, seed 1)",
             "config": {"workload": label, "global_dims": dims, "blocks": blocks, "gpu_grid": g,
@@ -465,7 +465,8 @@ def run_ours(args, D):
                        "timing": "CUDA events on the launching stream around K graph-replayed iterations, max over ranks"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         "kernel": "sweep_tma_kernel", "algorithmic_bytes_per_launch": BYTES_PER_LUP * pts_gpu,
+                         "kernel": "sweep2d_tma_kernel" if MODE_2D[0] else "sweep_tma_kernel",
+                         "algorithmic_bytes_per_launch": BYTES_PER_LUP * pts_gpu,
                          "avg_launch_us": 1e3 * sweep_ms,
                          "sweep_share_of_step": sweep_ms / ms_iter},
             "hbm_frac_step": BYTES_PER_LUP * pts_gpu / (ms_iter * 1e-3) / 1e9 / peak,

@@ -1,2 +1,2 @@
-JAC_VARIANT=5 timeout 300 python -m pytest tests/test_parity_gpu.py -q -x -k "odf_sweep or ragged or c1_config" > gpurun_out/pytest_tall.log 2>&1; echo rc=$? >> gpurun_out/pytest_tall.log
-for v in 0 5; do for zc in 16 32; do echo "== variant=$v zchunk=$zc"; JAC_VARIANT=$v JAC_ZCHUNK=$zc ITERS=10 timeout 300 python tools/perf_shapes.py 512x512x512:1x1x1 512x512x512:2x2x2 512x512x512:2x2x4 1024x1024x1024:1x1x1 1536x1536x1536:1x1x1 768x768x768:2x2x2 2>&1 | cut -c1-100; done; done > gpurun_out/tall.log
+FLAGS=512 ITERS=20 timeout 600 python tools/perf_shapes.py 32768x32768x1:1x1x1 32768x32768x1:2x4x1 32768x32768x1:4x4x1 32768x32768x1:8x8x1 32768x32768x1:32x32x1 8192x8192x1:4x4x1 > gpurun_out/j2d_shapes.log 2>&1
+timeout 600 python bench.py --config j2d --steps 50 --warmup 3 > gpurun_out/bench_j2d.json 2> gpurun_out/bench_j2d.err; echo rc=$? >> gpurun_out/bench_j2d.err
