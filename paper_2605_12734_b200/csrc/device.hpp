@@ -37,9 +37,13 @@ JAC_HD inline constexpr int opposite(int f) { return f ^ 1; }
 constexpr int kA = 4;        // x offset of interior column 0 inside a row
 constexpr int kXgPad = 32;   // doubles of slack after each x-ghost array (bulk-copy overrun)
 
+constexpr int kCtrlCounter = 8191;  // ctrl word: CTAs of the current sweep that finished
+
 struct DevBlock {
     int32_t slot;            // own slot in this GPU's arena
     int32_t org[3];          // global interior origin of the block (x, y, z)
+    uint32_t remote_mask;    // bit f: face f's neighbour lives on another rank (process)
+    uint32_t pad_;
     double *nb[6][2];        // per face and buffer, where this block's boundary layer
                              // goes: y/z faces -> the neighbour block's array base;
                              // x faces -> the neighbour's x-ghost array (side
@@ -80,7 +84,78 @@ struct SweepArgs {
     // group, z-chunk-major inside a group: item = g*gcols*nzc + zi*gsize + (col - g*gcols).
     // z-chunk zi of a column covers planes [zi*ez/nzc, (zi+1)*ez/nzc).
     int32_t nzc, ncols, nitems, gcols;
+    // Fused cross-rank ordering (rank contexts with remote faces, fused mode).  Only
+    // the items that touch a remote face share memory with a neighbour rank: they
+    // launch first (item_map), wait for the neighbours' signal of the previous sweep,
+    // and the last of them (nremote) signals this sweep's.  Other items never wait.
+    const int32_t *item_map; // launch order -> item, or nullptr
+    uint64_t *ctrl;          // own control block ([0] epoch, [1+rank] flags, [kCtrlCounter])
+    uint64_t *peer_slot[6];  // &peer_ctrl[1 + my_rank] per neighbour rank
+    int32_t peer_id[6];
+    int32_t npeers;
+    int32_t fused_sync;
+    int32_t nremote;         // items touching a remote face (the first nremote of item_map)
+    int32_t pad2_;
 };
+
+struct TileItem {
+    int b, x0, y0, zs, ze;   // 2-D: zs, ze = the item's y-tile range [zs, ze)
+};
+
+// item -> (block, tile, z-chunk) for the 3-D sweep (see SweepArgs work list)
+JAC_HD inline TileItem decode_item3d(const SweepArgs &a, int item, int BX, int BY)
+{
+    TileItem t;
+    const int grp = item / (a.gcols * a.nzc);
+    const int r = item - grp * a.gcols * a.nzc;
+    const int rest = a.ncols - grp * a.gcols;
+    const int gsize = a.gcols < rest ? a.gcols : rest;
+    const int zi = r / gsize;
+    int col = grp * a.gcols + (r - zi * gsize);
+    const int tx = col % a.ntx; col /= a.ntx;
+    const int ty = col % a.nty;
+    t.b = col / a.nty;
+    t.x0 = tx * BX;
+    t.y0 = ty * BY;
+    t.zs = (int)(((int64_t)zi * a.g.ez) / a.nzc);
+    t.ze = (int)(((int64_t)(zi + 1) * a.g.ez) / a.nzc);
+    return t;
+}
+
+// item -> (block, x tile, chunk of y tiles) for the 2-D sweep; nzc = y chunks per block
+JAC_HD inline TileItem decode_item2d(const SweepArgs &a, int item, int BX, int BY)
+{
+    TileItem t;
+    const int tx = item % a.ntx; item /= a.ntx;
+    const int yc = item % a.nzc;
+    t.b = item / a.nzc;
+    const int tpc = (a.nty + a.nzc - 1) / a.nzc;
+    t.x0 = tx * BX;
+    t.zs = yc * tpc;
+    t.ze = (t.zs + tpc < a.nty) ? t.zs + tpc : a.nty;
+    t.y0 = t.zs * BY;
+    return t;
+}
+
+// Does the item read or write the ghost layer of a face in `mask`?
+JAC_HD inline bool item_touches(const SweepArgs &a, const TileItem &t, uint32_t mask, int BX, int BY, bool two_d)
+{
+    if (!mask) return false;
+    const Geom &g = a.g;
+    bool hit = false;
+    if (mask & (1u << XM)) hit |= t.x0 == 0;
+    if (mask & (1u << XP)) hit |= t.x0 + BX >= g.ex;
+    if (two_d) {
+        if (mask & (1u << YM)) hit |= t.zs == 0;
+        if (mask & (1u << YP)) hit |= t.ze * BY >= g.ey;
+    } else {
+        if (mask & (1u << YM)) hit |= t.y0 == 0;
+        if (mask & (1u << YP)) hit |= t.y0 + BY >= g.ey;
+        if (mask & (1u << ZM)) hit |= t.zs == 0;
+        if (mask & (1u << ZP)) hit |= t.ze >= g.ez;
+    }
+    return hit;
+}
 
 JAC_HD inline double *xg_array(double *xg, const Geom &g, int buf, int slot, int side)
 {

@@ -110,6 +110,9 @@ struct jac_ctx {
     std::vector<void *> ipc_opened;
     bool ipc_done = false;
     jac::BarrierArgs bar{};
+    bool fused = false;                 // fused cross-rank ordering inside the sweep
+    int32_t *ditem_map = nullptr;       // launch order -> item (remote-touching items first)
+    int32_t nremote = 0;
 
     cudaStream_t stream = nullptr;
     // JAC_F_PER_BLOCK (paper-style): one stream per block, events per block and parity
@@ -130,6 +133,7 @@ struct jac_ctx {
     int kernels_per_iter() const
     {
         if (flags & JAC_F_PER_BLOCK) return (int)(nslots + 2 * local_faces + 2 * remote_faces);
+        if (fused) return 1;
         int k = 1;
         if (flags & JAC_F_UNFUSED_PACK) k += 1 + (has_remote() ? 2 : 0);
         else if (has_remote()) k += 1;
@@ -167,6 +171,17 @@ jac::SweepArgs sweep_args(const jac_ctx *c, int src, int mode)
     a.mode = mode;
     a.ntx = c->ntx; a.nty = c->nty; a.ntz = c->ntz; a.zc = c->zc;
     a.nzc = c->nzc; a.ncols = c->ncols; a.nitems = c->nitems; a.gcols = c->gcols;
+    if (c->fused && mode == jac::MODE_FUSED) {
+        a.fused_sync = 1;
+        a.nremote = c->nremote;
+        a.item_map = c->ditem_map;
+        a.ctrl = c->ctrl;
+        a.npeers = c->bar.npeers;
+        for (int n = 0; n < c->bar.npeers; ++n) {
+            a.peer_slot[n] = c->bar.peer_slot[n];
+            a.peer_id[n] = c->bar.peer_id[n];
+        }
+    }
     return a;
 }
 
@@ -201,7 +216,7 @@ int enqueue_iteration(jac_ctx *c, int src, cudaEvent_t evs = nullptr, cudaEvent_
     if (evs) CK(cudaEventRecordWithFlags(evs, c->stream, cudaEventRecordExternal));
     if ((rc = enqueue_sweep(c, src))) return rc;
     if (eve) CK(cudaEventRecordWithFlags(eve, c->stream, cudaEventRecordExternal));
-    if ((rc = enqueue_barrier(c))) return rc;
+    if (!c->fused && (rc = enqueue_barrier(c))) return rc;  // fused: ordering is inside the sweep
     if ((c->flags & JAC_F_UNFUSED_PACK) && !(c->flags & JAC_F_SKIP_EXCHANGE)) {
         CK(jac::launch_ghost_fill(sweep_args(c, src, jac::MODE_PACK), 1 - src, c->stream));
         if ((rc = enqueue_barrier(c))) return rc;
@@ -431,12 +446,37 @@ int create_common(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, in
                     const int32_t ns = h * bpp + plan.local_slot(nb[0], nb[1], nb[2]);
                     d.nb_out[f] = c->outbox + (int64_t)ns * g.ostride + g.ooff[jac::opposite(f)];
                 }
-            } else if (std::find(c->peer_ranks.begin(), c->peer_ranks.end(), owner) == c->peer_ranks.end()) {
-                c->peer_ranks.push_back(owner);  // pointers filled by jac_import_ipc
+            } else {
+                d.remote_mask |= 1u << f;  // pointers filled by jac_import_ipc
+                if (std::find(c->peer_ranks.begin(), c->peer_ranks.end(), owner) == c->peer_ranks.end())
+                    c->peer_ranks.push_back(owner);
             }
         }
     }
     if (c->peer_ranks.size() > 6) return bail(fail(JAC_EINVAL, "more than 6 neighbour ranks"));
+    if (n_gpus >= jac::kCtrlCounter) return bail(fail(JAC_EINVAL, "n_gpus too large for the control block"));
+    // Fused cross-rank ordering: remote-touching work items launch last and wait for
+    // the neighbours' end-of-sweep signal; everything else starts at once.
+    c->fused = rank_mode && !c->peer_ranks.empty() && sweep_mode(c) == jac::MODE_FUSED && c->variant != kPlain &&
+               !getenv("JAC_NO_FUSED_SYNC");
+    if (c->fused) {
+        const jac::SweepArgs a0 = sweep_args(c, 0, jac::MODE_NOEXCHANGE);
+        const jac::TileShape ts = jac::tma_tile_shape(c->variant);
+        const bool two_d = (flags & JAC_F_2D) != 0;
+        std::vector<int32_t> first, last;
+        for (int32_t it = 0; it < c->nitems; ++it) {
+            const jac::TileItem t = two_d ? jac::decode_item2d(a0, it, ts.bx, ts.by) : jac::decode_item3d(a0, it, ts.bx, ts.by);
+            (jac::item_touches(a0, t, c->hblocks[t.b].remote_mask, ts.bx, ts.by, two_d) ? last : first).push_back(it);
+        }
+        // remote-touching items first: their signal leaves early in the sweep, so the
+        // next sweep's remote items (which wait for it) find it already set
+        c->nremote = (int32_t)last.size();
+        last.insert(last.end(), first.begin(), first.end());
+        if (cudaMalloc(&c->ditem_map, sizeof(int32_t) * last.size()) != cudaSuccess ||
+            cudaMemcpy(c->ditem_map, last.data(), sizeof(int32_t) * last.size(), cudaMemcpyHostToDevice) != cudaSuccess)
+            return bail(fail(JAC_ENOMEM, "item map"));
+        if (c->nremote == 0) c->fused = false;
+    }
     if (cudaMalloc(&c->dblocks, sizeof(jac::DevBlock) * c->nslots) != cudaSuccess)
         return bail(fail(JAC_ENOMEM, "cudaMalloc descriptor table"));
     if (cudaMemcpy(c->dblocks, c->hblocks.data(), sizeof(jac::DevBlock) * c->nslots, cudaMemcpyHostToDevice) != cudaSuccess)
@@ -1046,6 +1086,7 @@ int jac_destroy(jac_ctx *c)
     if (c->ev1) cudaEventDestroy(c->ev1);
     if (c->stream) cudaStreamDestroy(c->stream);
     if (c->dblocks) cudaFree(c->dblocks);
+    if (c->ditem_map) cudaFree(c->ditem_map);
     if (c->alloc) cudaFree(c->alloc);
     delete c;
     return JAC_OK;

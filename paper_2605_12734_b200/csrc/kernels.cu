@@ -225,27 +225,45 @@ constexpr size_t tma_smem_bytes(int BX, int BY, int W, int NS)
     return (size_t)NS * (((W * (BY + 2) + 2 * BY) + 15) / 16 * 16) * sizeof(double) + NS * sizeof(uint64_t);
 }
 
-struct TileItem {
-    int b, x0, y0, zs, ze;
-};
-
 template <int BX, int BY>
 __device__ __forceinline__ TileItem decode_item(const SweepArgs &a, int item)
 {
-    TileItem t;
-    const int grp = item / (a.gcols * a.nzc);
-    const int r = item - grp * a.gcols * a.nzc;
-    const int gsize = min(a.gcols, a.ncols - grp * a.gcols);
-    const int zi = r / gsize;
-    int col = grp * a.gcols + (r - zi * gsize);
-    const int tx = col % a.ntx; col /= a.ntx;
-    const int ty = col % a.nty;
-    t.b = col / a.nty;
-    t.x0 = tx * BX;
-    t.y0 = ty * BY;
-    t.zs = (int)(((int64_t)zi * a.g.ez) / a.nzc);
-    t.ze = (int)(((int64_t)(zi + 1) * a.g.ez) / a.nzc);
-    return t;
+    return decode_item3d(a, item, BX, BY);
+}
+
+// ---- fused cross-rank ordering (see SweepArgs) --------------------------------
+__device__ __forceinline__ void wait_peers(const SweepArgs &a)
+{
+    const uint64_t e = *reinterpret_cast<volatile uint64_t *>(a.ctrl);  // phases completed here
+    for (int n = 0; n < a.npeers; ++n) {
+        const uint64_t *f = a.ctrl + 1 + a.peer_id[n];
+        uint64_t v;
+        const uint64_t t0 = globaltimer_ns();
+        for (;;) {
+            asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(f) : "memory");
+            if (v >= e) break;
+            if (globaltimer_ns() - t0 > kSpinLimitNs) __trap();
+            __nanosleep(100);
+        }
+    }
+}
+
+// All threads of a remote-touching item: after the CTA's last store.  The last such
+// CTA of the launch bumps the epoch and releases it to every neighbour rank.
+__device__ __forceinline__ void signal_done(const SweepArgs &a)
+{
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    __threadfence_system();  // this CTA's stores (peer stores included) before the count
+    unsigned long long *cnt = reinterpret_cast<unsigned long long *>(a.ctrl + kCtrlCounter);
+    if (atomicAdd(cnt, 1ull) == (unsigned long long)a.nremote - 1) {
+        *cnt = 0;
+        __threadfence_system();
+        const uint64_t e = a.ctrl[0] + 1;
+        a.ctrl[0] = e;
+        for (int n = 0; n < a.npeers; ++n)
+            asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(a.peer_slot[n]), "l"(e) : "memory");
+    }
 }
 
 // Staged column of the tile's first point i = x0.  Interior tiles stage x0-2 ..
@@ -280,7 +298,8 @@ __global__ void __launch_bounds__(NT, 4) sweep_tma_kernel(const __grid_constant_
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + NS * L::STRIDE * sizeof(double));
 
     const Geom &g = a.g;
-    const TileItem t = decode_item<BX, BY>(a, blockIdx.x);
+    const TileItem t = decode_item<BX, BY>(a, a.item_map ? a.item_map[blockIdx.x] : (int)blockIdx.x);
+    const bool remote = a.fused_sync && (int)blockIdx.x < a.nremote;  // item_map puts them first
     __shared__ DevBlock blk;  // this item's descriptor, read once from the table
     if (threadIdx.x == 0) blk = a.blocks[t.b];
     const int soff = tile_soff<BX, W>(g, t.x0);  // staged column of point i = x0 (0, 2 or 4)
@@ -308,7 +327,9 @@ __global__ void __launch_bounds__(NT, 4) sweep_tma_kernel(const __grid_constant_
     };
 
     if (threadIdx.x == 0) {
-        const int slot = a.blocks[t.b].slot;
+        const DevBlock &gb = a.blocks[t.b];
+        const int slot = gb.slot;
+        if (remote) wait_peers(a);
         c3 = a.src * g.nslots + slot;
         xg0 = xg_array(a.xg, g, a.src, slot, 0) + t.y0;
         xg1 = xg_array(a.xg, g, a.src, slot, 1) + t.y0;
@@ -378,6 +399,7 @@ __global__ void __launch_bounds__(NT, 4) sweep_tma_kernel(const __grid_constant_
 #pragma unroll
         for (int r = 0; r < RY; ++r) { zm[r] = c[r]; c[r] = zp[r]; }
     }
+    if (remote) signal_done(a);
 }
 
 // ------------------------------------------------------------------ Jacobi2D sweep
@@ -411,14 +433,12 @@ __global__ void __launch_bounds__(NT, 4) sweep2d_tma_kernel(const __grid_constan
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + NS * L::STRIDE * sizeof(double));
 
     const Geom &g = a.g;
-    int item = blockIdx.x;
-    const int tx = item % a.ntx; item /= a.ntx;
-    const int yc = item % a.nzc;  // y chunk
-    const int b = item / a.nzc;
-    const int tpc = (a.nty + a.nzc - 1) / a.nzc;  // y tiles per chunk
-    const int ty0 = yc * tpc;
-    const int nq = max(0, min(a.nty, ty0 + tpc) - ty0);
-    const int x0 = tx * BX;
+    const TileItem t = decode_item2d(a, a.item_map ? a.item_map[blockIdx.x] : (int)blockIdx.x, BX, BY);
+    const bool remote = a.fused_sync && (int)blockIdx.x < a.nremote;
+    const int b = t.b;
+    const int ty0 = t.zs;
+    const int nq = max(0, t.ze - t.zs);
+    const int x0 = t.x0;
     __shared__ DevBlock blk;
     if (threadIdx.x == 0) blk = a.blocks[b];
     const int soff = tile_soff<BX, W>(g, x0);
@@ -436,7 +456,9 @@ __global__ void __launch_bounds__(NT, 4) sweep2d_tma_kernel(const __grid_constan
         if (xhi) bulk_copy(st + L::XG_OFF + BY, xg1 + y0, L::XG_BYTES, bar);
     };
     if (threadIdx.x == 0) {
-        const int slot = a.blocks[b].slot;
+        const DevBlock &gb = a.blocks[b];
+        const int slot = gb.slot;
+        if (remote) wait_peers(a);
         c3 = a.src * g.nslots + slot;
         xg0 = xg_array(a.xg, g, a.src, slot, 0);
         xg1 = xg_array(a.xg, g, a.src, slot, 1);
@@ -476,6 +498,7 @@ __global__ void __launch_bounds__(NT, 4) sweep2d_tma_kernel(const __grid_constan
         __syncthreads();
         if (threadIdx.x == 0 && q + NS < nq) issue(q + NS);
     }
+    if (remote) signal_done(a);
 }
 
 // ------------------------------------------------------------------ plain sweep
