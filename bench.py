@@ -400,6 +400,16 @@ def run_ours(args, D):
     d2h = pts_gpu * 8
     close_ctx(J, D)
 
+    # ---- N > 1 ablation: NCCL send/recv of packed faces instead of in-kernel peer stores
+    nccl_ablation = None
+    if D.world > 1 and not args.no_sweep:
+        Jn = make_ctx(dims, blocks, g, D, flags=JB.JAC_F_NCCL)
+        Jn.set_init_hash(1)
+        ms_n, _ = time_ctx(Jn, K, W, D)
+        nccl_ablation = {"ms_per_iter": ms_n / K, "glups": pts * K / (ms_n * 1e-3) / 1e9,
+                         "vs_peer_stores": ms_n / K / ms_iter}
+        close_ctx(Jn, D)
+
     # ---- ODF sweep + ablations (N = 1, c2)
     sweep = None
     ablations = None
@@ -487,6 +497,8 @@ def run_ours(args, D):
             line["ablations_odf16"] = ablations
         if paper_style is not None:
             line["paper_style_per_block"] = paper_style
+        if nccl_ablation is not None:
+            line["ablation_nccl_sendrecv"] = nccl_ablation
         print(json.dumps(line), flush=True)
     D.finish()
 

@@ -62,7 +62,11 @@ enum jac_flags {
     JAC_F_FMA = 1u << 0,          /* accepted, no effect: the update has no a*b+c (R5) */
     JAC_F_NO_GRAPH = 1u << 1,     /* launch every kernel from the host each iteration
                                      (ablation of the CUDA-Graph iteration) */
-    JAC_F_NCCL = 1u << 2,         /* reserved: NCCL send/recv transport (not built yet) */
+    JAC_F_NCCL = 1u << 2,         /* rank contexts, ablation of the peer-store exchange: the
+                                     sweep packs REMOTE faces into send buffers, grouped
+                                     ncclSend / ncclRecv move them (one per face), the
+                                     batched ghost kernel unpacks (north-star subsystem 4,
+                                     "NCCL send/recv").  Bootstrap with jac_nccl_* below. */
     JAC_F_UNFUSED_PACK = 1u << 4, /* north-star layout: the sweep packs faces into an
                                      outbox and a separate batched ghost-copy kernel
                                      fills the ghosts (PAPER.md:90 pack/unpack kernels) */
@@ -144,6 +148,14 @@ int jac_export_ipc(jac_ctx *c, void *out);
 /* all = n_gpus records in rank order (all-gathered by the caller).  Opens the
  * neighbours' memory, fills REMOTE face pointers of the device table. */
 int jac_import_ipc(jac_ctx *c, const void *all);
+
+/* JAC_F_NCCL bootstrap (instead of the IPC exchange): rank 0 calls
+ * jac_nccl_get_unique_id(out[jac_nccl_id_bytes()]), the caller broadcasts the bytes,
+ * every rank calls jac_nccl_init (collective; creates the communicator on the
+ * context's device).  libnccl.so.2 is loaded at run time; JAC_ENCCL if missing. */
+size_t jac_nccl_id_bytes(void);
+int jac_nccl_get_unique_id(void *out);
+int jac_nccl_init(jac_ctx *c, const void *id);
 
 /* Copies the padded initial field (host, see conventions) into BOTH ghosted
  * buffers of every local block, ghosts included, so the shell is Dirichlet data in

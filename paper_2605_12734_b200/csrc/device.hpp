@@ -43,7 +43,8 @@ struct DevBlock {
     int32_t slot;            // own slot in this GPU's arena
     int32_t org[3];          // global interior origin of the block (x, y, z)
     uint32_t remote_mask;    // bit f: face f's neighbour lives on another rank (process)
-    uint32_t pad_;
+    uint32_t pack_mask;      // bit f: nb[f][*] is a packed send buffer (JAC_F_NCCL), layout
+                             // x: [k][eyp] (x-ghost layout), y: [k][ex], z: [j][ex]
     double *nb[6][2];        // per face and buffer, where this block's boundary layer
                              // goes: y/z faces -> the neighbour block's array base;
                              // x faces -> the neighbour's x-ghost array (side

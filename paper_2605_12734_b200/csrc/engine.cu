@@ -13,6 +13,8 @@
 // preallocated scratch instead of allocations that imply fences).
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <climits>
@@ -66,6 +68,43 @@ struct IpcRecord {
 };
 static_assert(sizeof(IpcRecord) == 256, "IPC record size");
 
+// NCCL, loaded at run time (JAC_F_NCCL only): no link-time dependency, and the
+// process's already-loaded libnccl.so.2 (torch's) is the one resolved.
+struct NcclApi {
+    ncclResult_t (*getUniqueId)(ncclUniqueId *);
+    ncclResult_t (*commInitRank)(ncclComm_t *, int, ncclUniqueId, int);
+    ncclResult_t (*commDestroy)(ncclComm_t);
+    ncclResult_t (*send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+    ncclResult_t (*recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+    ncclResult_t (*groupStart)();
+    ncclResult_t (*groupEnd)();
+    const char *(*errorString)(ncclResult_t);
+};
+
+const NcclApi *nccl_api()
+{
+    static NcclApi api;
+    static int state = 0;  // 0 untried, 1 ok, -1 failed
+    if (state == 0) {
+        void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        state = -1;
+        if (h) {
+            api.getUniqueId = (decltype(api.getUniqueId))dlsym(h, "ncclGetUniqueId");
+            api.commInitRank = (decltype(api.commInitRank))dlsym(h, "ncclCommInitRank");
+            api.commDestroy = (decltype(api.commDestroy))dlsym(h, "ncclCommDestroy");
+            api.send = (decltype(api.send))dlsym(h, "ncclSend");
+            api.recv = (decltype(api.recv))dlsym(h, "ncclRecv");
+            api.groupStart = (decltype(api.groupStart))dlsym(h, "ncclGroupStart");
+            api.groupEnd = (decltype(api.groupEnd))dlsym(h, "ncclGroupEnd");
+            api.errorString = (decltype(api.errorString))dlsym(h, "ncclGetErrorString");
+            if (api.getUniqueId && api.commInitRank && api.commDestroy && api.send && api.recv && api.groupStart &&
+                api.groupEnd && api.errorString)
+                state = 1;
+        }
+    }
+    return state == 1 ? &api : nullptr;
+}
+
 typedef CUresult (*PFN_encodeTiled)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
                                     const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
                                     const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
@@ -81,6 +120,13 @@ void set_last_error(int code, const char *msg)
     g_err = msg;
 }
 }  // namespace jac
+
+struct NcclFace {
+    int32_t peer;
+    int64_t key;    // min(global block ids) * 3 + axis: identical on both ranks
+    int64_t count;  // doubles
+    double *send, *recv;
+};
 
 struct jac_ctx {
     jac::Plan plan{};
@@ -111,6 +157,8 @@ struct jac_ctx {
     bool ipc_done = false;
     jac::BarrierArgs bar{};
     bool fused = false;                 // fused cross-rank ordering inside the sweep
+    std::vector<NcclFace> nccl_faces;   // JAC_F_NCCL: remote faces, sorted (peer, key)
+    void *nccl_comm = nullptr;
     int32_t *ditem_map = nullptr;       // launch order -> item (remote-touching items first)
     int32_t nremote = 0;
 
@@ -134,6 +182,7 @@ struct jac_ctx {
     {
         if (flags & JAC_F_PER_BLOCK) return (int)(nslots + 2 * local_faces + 2 * remote_faces);
         if (fused) return 1;
+        if (flags & JAC_F_NCCL) return 2;  // sweep + unpack (NCCL's own kernels not counted)
         int k = 1;
         if (flags & JAC_F_UNFUSED_PACK) k += 1 + (has_remote() ? 2 : 0);
         else if (has_remote()) k += 1;
@@ -203,7 +252,8 @@ int enqueue_sweep(jac_ctx *c, int src)
 
 int enqueue_barrier(jac_ctx *c)
 {
-    if (!c->has_remote()) return JAC_OK;
+    // NCCL contexts share no memory with their peers: NCCL orders the exchange
+    if (!c->has_remote() || (c->flags & JAC_F_NCCL)) return JAC_OK;
     CK(jac::launch_barrier(c->bar, c->stream));
     return JAC_OK;
 }
@@ -216,6 +266,21 @@ int enqueue_iteration(jac_ctx *c, int src, cudaEvent_t evs = nullptr, cudaEvent_
     if (evs) CK(cudaEventRecordWithFlags(evs, c->stream, cudaEventRecordExternal));
     if ((rc = enqueue_sweep(c, src))) return rc;
     if (eve) CK(cudaEventRecordWithFlags(eve, c->stream, cudaEventRecordExternal));
+    if (c->flags & JAC_F_NCCL) {  // ablation: library point-to-point instead of peer stores
+        const NcclApi *N = nccl_api();
+        ncclComm_t comm = (ncclComm_t)c->nccl_comm;
+        if (!N || !comm) return fail(JAC_ENCCL, "NCCL not initialised (jac_nccl_init)");
+        ncclResult_t r = N->groupStart();
+        for (const NcclFace &f : c->nccl_faces) {
+            if (r == ncclSuccess) r = N->send(f.send, (size_t)f.count, ncclDouble, f.peer, comm, c->stream);
+            if (r == ncclSuccess) r = N->recv(f.recv, (size_t)f.count, ncclDouble, f.peer, comm, c->stream);
+        }
+        const ncclResult_t r2 = N->groupEnd();
+        if (r != ncclSuccess || r2 != ncclSuccess)
+            return fail(JAC_ENCCL, "ncclSend/ncclRecv: %s", N->errorString(r != ncclSuccess ? r : r2));
+        CK(jac::launch_ghost_fill(sweep_args(c, src, jac::MODE_FUSED), 1 - src, c->stream));
+        return JAC_OK;
+    }
     if (!c->fused && (rc = enqueue_barrier(c))) return rc;  // fused: ordering is inside the sweep
     if ((c->flags & JAC_F_UNFUSED_PACK) && !(c->flags & JAC_F_SKIP_EXCHANGE)) {
         CK(jac::launch_ghost_fill(sweep_args(c, src, jac::MODE_PACK), 1 - src, c->stream));
@@ -291,7 +356,8 @@ int create_common(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, in
     std::string err;
     int rc = jac::make_plan(nx, ny, nz, bx, by, bz, n_gpus, gpu_grid, &plan, &err);
     if (rc) return fail(rc, "%s", err.c_str());
-    if (flags & JAC_F_NCCL) return fail(JAC_EINVAL, "flags: JAC_F_NCCL transport is not built in this version");
+    if ((flags & JAC_F_NCCL) && (!rank_mode || (flags & (JAC_F_UNFUSED_PACK | JAC_F_PER_BLOCK | JAC_F_SKIP_EXCHANGE))))
+        return fail(JAC_EINVAL, "flags: JAC_F_NCCL needs a rank context (jac_create_rank) and the fused sweep");
     if ((flags & JAC_F_2D) && (nz != 1 || bz != 1))
         return fail(JAC_EINVAL, "flags: JAC_F_2D needs nz == 1 and bz == 1 (the 2-D grid is nx x ny)");
     if ((flags & JAC_F_2D) && (flags & (JAC_F_UNFUSED_PACK | JAC_F_NO_TMA | JAC_F_PER_BLOCK)))
@@ -337,11 +403,12 @@ int create_common(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, in
     g.nslots = c->nslots;
     g.eyp = (int32_t)round_up(g.ey, 4);
     g.xgstride = round_up((int64_t)g.eyp * g.ez + jac::kXgPad, 32);
-    const int64_t fx = (int64_t)g.ey * g.ez, fy = (int64_t)g.ex * g.ez, fz = (int64_t)g.ex * g.ey;
+    // face buffer sizes (x faces in the x-ghost layout, pitch eyp: JAC_F_NCCL packs them so)
+    const int64_t fx = (int64_t)g.eyp * g.ez, fy = (int64_t)g.ex * g.ez, fz = (int64_t)g.ex * g.ey;
     int64_t o = 0;
     const int64_t fsz[6] = {fx, fx, fy, fy, fz, fz};
     for (int f = 0; f < 6; ++f) { g.ooff[f] = o; o += round_up(fsz[f], 4); }
-    g.ostride = (flags & (JAC_F_UNFUSED_PACK | JAC_F_PER_BLOCK)) ? round_up(o, 32) : 0;
+    g.ostride = (flags & (JAC_F_UNFUSED_PACK | JAC_F_PER_BLOCK | JAC_F_NCCL)) ? round_up(o, 32) : 0;
 
     // tile shape / variant
     if (flags & JAC_F_NO_TMA) c->variant = kPlain;
@@ -405,7 +472,8 @@ int create_common(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, in
     const size_t xg_bytes = (size_t)2 * c->nslots * 2 * g.xgstride * sizeof(double);
     c->outbox_off = c->xg_off + xg_bytes;
     // outbox: one set of faces per block; JAC_F_PER_BLOCK double-buffers it by parity
-    const size_t outbox_bytes = (size_t)((flags & JAC_F_PER_BLOCK) ? 2 : 1) * c->nslots * g.ostride * sizeof(double);
+    // (JAC_F_NCCL: send buffers then receive buffers)
+    const size_t outbox_bytes = (size_t)((flags & (JAC_F_PER_BLOCK | JAC_F_NCCL)) ? 2 : 1) * c->nslots * g.ostride * sizeof(double);
     c->alloc_bytes = c->outbox_off + outbox_bytes;
     e = cudaMalloc(&c->alloc, c->alloc_bytes);
     if (e != cudaSuccess) {
@@ -441,11 +509,26 @@ int create_common(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, in
             if (local) {
                 d.nb[f][0] = block_ptr_local(c, nb, 0, f);
                 d.nb[f][1] = block_ptr_local(c, nb, 1, f);
-                if (c->outbox) {
+                if (c->outbox && (flags & JAC_F_UNFUSED_PACK)) {
                     int32_t h = (int32_t)(std::find(c->parts.begin(), c->parts.end(), owner) - c->parts.begin());
                     const int32_t ns = h * bpp + plan.local_slot(nb[0], nb[1], nb[2]);
                     d.nb_out[f] = c->outbox + (int64_t)ns * g.ostride + g.ooff[jac::opposite(f)];
                 }
+            } else if (flags & JAC_F_NCCL) {
+                // pack into this block's send buffer; the batched ghost kernel unpacks the
+                // receive buffer after the grouped ncclSend / ncclRecv
+                d.remote_mask |= 1u << f;
+                d.pack_mask |= 1u << f;
+                double *sendb = c->outbox + (int64_t)s * g.ostride + g.ooff[f];
+                double *recvb = c->outbox + (int64_t)(c->nslots + s) * g.ostride + g.ooff[f];
+                d.nb[f][0] = d.nb[f][1] = sendb;
+                d.nb_out[f] = recvb;
+                const int64_t gb = ((int64_t)blk[2] * plan.b[1] + blk[1]) * plan.b[0] + blk[0];
+                const int64_t gn = ((int64_t)nb[2] * plan.b[1] + nb[1]) * plan.b[0] + nb[0];
+                const int64_t count = (f >> 1) == 0 ? fx : (f >> 1) == 1 ? fy : fz;
+                c->nccl_faces.push_back({owner, std::min(gb, gn) * 3 + (f >> 1), count, sendb, recvb});
+                if (std::find(c->peer_ranks.begin(), c->peer_ranks.end(), owner) == c->peer_ranks.end())
+                    c->peer_ranks.push_back(owner);
             } else {
                 d.remote_mask |= 1u << f;  // pointers filled by jac_import_ipc
                 if (std::find(c->peer_ranks.begin(), c->peer_ranks.end(), owner) == c->peer_ranks.end())
@@ -457,8 +540,11 @@ int create_common(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, in
     if (n_gpus >= jac::kCtrlCounter) return bail(fail(JAC_EINVAL, "n_gpus too large for the control block"));
     // Fused cross-rank ordering: remote-touching work items launch last and wait for
     // the neighbours' end-of-sweep signal; everything else starts at once.
+    std::sort(c->nccl_faces.begin(), c->nccl_faces.end(), [](const NcclFace &x, const NcclFace &y) {
+        return x.peer != y.peer ? x.peer < y.peer : x.key < y.key;  // same order on both sides
+    });
     c->fused = rank_mode && !c->peer_ranks.empty() && sweep_mode(c) == jac::MODE_FUSED && c->variant != kPlain &&
-               !getenv("JAC_NO_FUSED_SYNC");
+               !(flags & JAC_F_NCCL) && !getenv("JAC_NO_FUSED_SYNC");
     if (c->fused) {
         const jac::SweepArgs a0 = sweep_args(c, 0, jac::MODE_NOEXCHANGE);
         const jac::TileShape ts = jac::tma_tile_shape(c->variant);
@@ -716,10 +802,43 @@ int jac_export_ipc(jac_ctx *c, void *out)
     return JAC_OK;
 }
 
+int jac_nccl_init(jac_ctx *c, const void *id)
+{
+    if (!c || !id) return fail(JAC_EINVAL, "ctx/id is NULL");
+    if (!(c->flags & JAC_F_NCCL)) return fail(JAC_ESTATE, "jac_nccl_init needs a JAC_F_NCCL rank context");
+    if (c->nccl_comm) return fail(JAC_ESTATE, "jac_nccl_init called twice");
+    const NcclApi *N = nccl_api();
+    if (!N) return fail(JAC_ENCCL, "libnccl.so.2 could not be loaded");
+    CK(cudaSetDevice(c->device));
+    ncclUniqueId uid;
+    memcpy(&uid, id, sizeof uid);
+    ncclComm_t comm = nullptr;
+    const ncclResult_t r = N->commInitRank(&comm, c->plan.n_gpus, uid, c->rank);
+    if (r != ncclSuccess) return fail(JAC_ENCCL, "ncclCommInitRank: %s", N->errorString(r));
+    c->nccl_comm = comm;
+    c->ipc_done = true;
+    return JAC_OK;
+}
+
+size_t jac_nccl_id_bytes(void) { return sizeof(ncclUniqueId); }
+
+int jac_nccl_get_unique_id(void *out)
+{
+    if (!out) return fail(JAC_EINVAL, "out is NULL");
+    const NcclApi *N = nccl_api();
+    if (!N) return fail(JAC_ENCCL, "libnccl.so.2 could not be loaded");
+    ncclUniqueId uid;
+    const ncclResult_t r = N->getUniqueId(&uid);
+    if (r != ncclSuccess) return fail(JAC_ENCCL, "ncclGetUniqueId: %s", N->errorString(r));
+    memcpy(out, &uid, sizeof uid);
+    return JAC_OK;
+}
+
 int jac_import_ipc(jac_ctx *c, const void *all)
 {
     if (!c || !all) return fail(JAC_EINVAL, "ctx/all is NULL");
     if (!c->rank_mode) return fail(JAC_ESTATE, "jac_import_ipc needs a rank context");
+    if (c->flags & JAC_F_NCCL) return fail(JAC_ESTATE, "JAC_F_NCCL contexts use jac_nccl_init, not IPC");
     if (c->ipc_done) return fail(JAC_ESTATE, "jac_import_ipc called twice");
     CK(cudaSetDevice(c->device));
     const IpcRecord *recs = static_cast<const IpcRecord *>(all);
@@ -1082,6 +1201,9 @@ int jac_destroy(jac_ctx *c)
         if (c->gU[s]) cudaGraphExecDestroy(c->gU[s]);
     }
     for (void *p : c->ipc_opened) cudaIpcCloseMemHandle(p);
+    if (c->nccl_comm) {
+        if (const NcclApi *N = nccl_api()) N->commDestroy((ncclComm_t)c->nccl_comm);
+    }
     if (c->ev0) cudaEventDestroy(c->ev0);
     if (c->ev1) cudaEventDestroy(c->ev1);
     if (c->stream) cudaStreamDestroy(c->stream);

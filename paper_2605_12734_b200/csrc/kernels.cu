@@ -82,24 +82,38 @@ __device__ __forceinline__ void emit_pair(const SweepArgs &a, const DevBlock &bl
     if (a.mode == MODE_FUSED) {
         // direct-to-ghost: the neighbour's ghost layer of the OUTPUT buffer is not
         // read by anyone during this sweep, so writing it here is race-free.
+        // (pack_mask faces -- JAC_F_NCCL -- go to a contiguous send buffer instead.)
+        auto packed = [&](double *p, int64_t idx) { p[idx] = v.x; if (both) p[idx + 1] = v.y; };
         if (zface) {
             if (k == 0) {
                 double *p = blk.nb[ZM][dst];
-                if (p) st_pair(p + (int64_t)(g.ez + 1) * g.Q + rowoff, v, both);
+                if (p) {
+                    if (blk.pack_mask & (1u << ZM)) packed(p, (int64_t)j * g.ex + i);
+                    else st_pair(p + (int64_t)(g.ez + 1) * g.Q + rowoff, v, both);
+                }
             }
             if (k == g.ez - 1) {
                 double *p = blk.nb[ZP][dst];
-                if (p) st_pair(p + rowoff, v, both);
+                if (p) {
+                    if (blk.pack_mask & (1u << ZP)) packed(p, (int64_t)j * g.ex + i);
+                    else st_pair(p + rowoff, v, both);
+                }
             }
         }
         if (yface) {
             if (j == 0) {
                 double *p = blk.nb[YM][dst];
-                if (p) st_pair(p + (int64_t)(k + g.zg) * g.Q + (int64_t)(g.ey + 1) * g.P + g.A + i, v, both);
+                if (p) {
+                    if (blk.pack_mask & (1u << YM)) packed(p, (int64_t)k * g.ex + i);
+                    else st_pair(p + (int64_t)(k + g.zg) * g.Q + (int64_t)(g.ey + 1) * g.P + g.A + i, v, both);
+                }
             }
             if (j == g.ey - 1) {
                 double *p = blk.nb[YP][dst];
-                if (p) st_pair(p + (int64_t)(k + g.zg) * g.Q + g.A + i, v, both);
+                if (p) {
+                    if (blk.pack_mask & (1u << YP)) packed(p, (int64_t)k * g.ex + i);
+                    else st_pair(p + (int64_t)(k + g.zg) * g.Q + g.A + i, v, both);
+                }
             }
         }
         // x faces: into the neighbour's contiguous x-ghost array; the 16 rows of a
@@ -559,7 +573,8 @@ __global__ void __launch_bounds__(256) ghost_fill_kernel(const SweepArgs a, int 
          e += (int64_t)gridDim.y * blockDim.x) {
         if (d == 0) {
             const int64_t k = e / g.ey, j = e % g.ey;
-            xg[k * g.eyp + j] = src[e];
+            // JAC_F_NCCL inboxes keep the x-ghost layout (pitch eyp); outboxes [k][ey]
+            xg[k * g.eyp + j] = (blk.pack_mask & (1u << f)) ? src[k * g.eyp + j] : src[e];
             continue;
         }
         int64_t off;

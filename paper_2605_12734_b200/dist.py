@@ -11,7 +11,8 @@ from __future__ import annotations
 import os
 from typing import List, Optional, Sequence
 
-from .jacobi3d import Jacobi3D, jac_export_ipc, jac_import_ipc, jac_plan, jac_plan_face
+from .jacobi3d import (JAC_F_NCCL, Jacobi3D, jac_export_ipc, jac_import_ipc, jac_nccl_get_unique_id,
+                       jac_nccl_init, jac_plan, jac_plan_face)
 
 
 def exchange_records(record: bytes, world: int) -> List[bytes]:
@@ -51,8 +52,13 @@ def create_rank_context(dims: Sequence[int], blocks: Sequence[int], gpu_grid=Non
     if device is None:
         device = int(os.environ.get("LOCAL_RANK", rank))
     J = Jacobi3D(dims, blocks, n_gpus=world, gpu_grid=gpu_grid, flags=flags, rank=rank, device=device)
-    recs = exchange_records(jac_export_ipc(J.ctx), world)
-    jac_import_ipc(J.ctx, recs)
+    if flags & JAC_F_NCCL:  # ablation transport: NCCL communicator instead of IPC peer stores
+        uid = jac_nccl_get_unique_id() if rank == 0 else b""
+        uid = exchange_records(uid, world)[0]
+        jac_nccl_init(J.ctx, uid)
+    else:
+        recs = exchange_records(jac_export_ipc(J.ctx), world)
+        jac_import_ipc(J.ctx, recs)
     dist.barrier()
     return J
 

@@ -37,7 +37,8 @@ EXPORTED = ["jac_plan", "jac_plan_face", "jac_create", "jac_create_rank", "jac_i
             "jac_export_ipc", "jac_import_ipc", "jac_set_init", "jac_set_init_hash", "jac_step",
             "jac_get_block", "jac_get_block_padded", "jac_get_field", "jac_get_layout",
             "jac_block_owner", "jac_last_step_ms", "jac_set_init_box", "jac_get_field_box", "jac_local_box", "jac_profile_sweep", "jac_get_stats",
-            "jac_destroy", "jac_last_error", "jac_version", "jac_set_option"]
+            "jac_destroy", "jac_last_error", "jac_version", "jac_set_option", "jac_nccl_id_bytes",
+            "jac_nccl_get_unique_id", "jac_nccl_init"]
 MICROBENCH_EXPORTED = ["jac_mb_launch_latency", "jac_mb_overlap", "jac_mb_launch_rate", "jac_mb_pipeline"]
 
 _ERRNAMES = {-1: "JAC_EINVAL", -2: "JAC_EDECOMP", -3: "JAC_EDEVICE", -4: "JAC_ENOMEM",
@@ -93,6 +94,8 @@ def load() -> ctypes.CDLL:
         "jac_get_stats": [vp, P(i64)],
         "jac_destroy": [vp],
         "jac_set_option": [vp, i32, i64],
+        "jac_nccl_get_unique_id": [vp],
+        "jac_nccl_init": [vp, vp],
         "jac_mb_launch_latency": [i32, i32, P(ctypes.c_double)],
         "jac_mb_overlap": [i32, i64, i32, i32, P(ctypes.c_double), P(ctypes.c_double)],
         "jac_mb_launch_rate": [i32, i32, i32, ctypes.c_double, P(ctypes.c_double)],
@@ -102,6 +105,8 @@ def load() -> ctypes.CDLL:
         f = getattr(L, name)
         f.argtypes = args
         f.restype = ctypes.c_int
+    L.jac_nccl_id_bytes.argtypes = []
+    L.jac_nccl_id_bytes.restype = ctypes.c_size_t
     L.jac_ipc_handle_bytes.argtypes = []
     L.jac_ipc_handle_bytes.restype = ctypes.c_size_t
     L.jac_last_error.argtypes = []
@@ -170,6 +175,17 @@ def jac_import_ipc(ctx, records: Sequence[bytes]) -> None:
     blob = b"".join(records)
     buf = ctypes.create_string_buffer(blob, len(blob))
     _check(load().jac_import_ipc(ctx, buf), "jac_import_ipc")
+
+
+def jac_nccl_get_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(int(load().jac_nccl_id_bytes()))
+    _check(load().jac_nccl_get_unique_id(buf), "jac_nccl_get_unique_id")
+    return buf.raw
+
+
+def jac_nccl_init(ctx, uid: bytes) -> None:
+    buf = ctypes.create_string_buffer(uid, len(uid))
+    _check(load().jac_nccl_init(ctx, buf), "jac_nccl_init")
 
 
 def jac_set_init(ctx, padded: np.ndarray) -> None:

@@ -28,6 +28,9 @@ CASES = [
     (8, (64, 64, 64), (4, 4, 4), None, 17, 0, False),          # 2x2x2, ODF 8
     (2, (256, 192, 1), (2, 4, 1), None, 13, 1 << 9, False),    # Jacobi2D, y split
     (4, (256, 192, 1), (4, 4, 1), None, 9, 1 << 9, True),      # Jacobi2D, 2x2 GPUs, hash init
+    (2, (64, 48, 80), (2, 2, 4), None, 21, 1 << 2, False),     # NCCL transport ablation
+    (4, (64, 64, 64), (4, 2, 2), (2, 2, 1), 7, 1 << 2, False), # NCCL, x-split (x-ghost layout)
+    (2, (256, 192, 1), (2, 4, 1), None, 5, (1 << 2) | (1 << 9), False),  # NCCL + Jacobi2D
 ]
 
 
