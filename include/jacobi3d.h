@@ -194,6 +194,12 @@ int jac_get_field(jac_ctx *c, double *padded);
  * jac_set_init_box (cells outside local interiors untouched). */
 int jac_get_field_box(jac_ctx *c, double *box, const int64_t *origin, const int64_t *extent);
 
+/* Interior sub-box [lo, lo+ext) (0-based interior coordinates, x fastest) into
+ * caller-owned host `out` (ext[2]*ext[1]*ext[0] doubles).  Every cell must belong to
+ * a block local to this context.  For probes and sampled parity checks of grids too
+ * large to read back whole. */
+int jac_get_region(jac_ctx *c, const int64_t *lo, const int64_t *ext, double *out);
+
 int jac_get_layout(const jac_ctx *c, int32_t *gpu_grid, int64_t *block_extent,
                    int64_t *iterations_done);
 /* Partition (GPU) owning block (ix,iy,iz). */

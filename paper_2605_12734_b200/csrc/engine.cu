@@ -1133,6 +1133,41 @@ int jac_get_field(jac_ctx *c, double *padded)
     return jac_get_field_box(c, padded, o, e);
 }
 
+int jac_get_region(jac_ctx *c, const int64_t *lo, const int64_t *ext, double *out)
+{
+    if (!c || !lo || !ext || !out) return fail(JAC_EINVAL, "ctx/lo/ext/out is NULL");
+    const jac::Plan &p = c->plan;
+    for (int k = 0; k < 3; ++k)
+        if (lo[k] < 0 || ext[k] < 1 || lo[k] + ext[k] > p.n[k])
+            return fail(JAC_EINVAL, "region dim %d [%lld, +%lld) outside the interior", k, (long long)lo[k], (long long)ext[k]);
+    CK(cudaSetDevice(c->device));
+    const jac::Geom &g = c->geom;
+    int64_t covered = 0;
+    for (int32_t s = 0; s < c->nslots; ++s) {
+        const jac::DevBlock &d = c->hblocks[s];
+        int64_t a[3], b[3];
+        bool empty = false;
+        for (int k = 0; k < 3; ++k) {
+            a[k] = std::max<int64_t>(lo[k], d.org[k]);
+            b[k] = std::min<int64_t>(lo[k] + ext[k], d.org[k] + p.e[k]);
+            empty |= a[k] >= b[k];
+        }
+        if (empty) continue;
+        covered += (b[0] - a[0]) * (b[1] - a[1]) * (b[2] - a[2]);
+        cudaMemcpy3DParms m{};
+        m.srcPtr = make_cudaPitchedPtr(c->slot_ptr((int)(c->iters & 1), s), (size_t)g.P * 8, (size_t)g.P, (size_t)(g.ey + 2));
+        m.srcPos = make_cudaPos((size_t)(g.A + a[0] - d.org[0]) * 8, (size_t)(1 + a[1] - d.org[1]), (size_t)(g.zg + a[2] - d.org[2]));
+        m.dstPtr = make_cudaPitchedPtr(out, (size_t)ext[0] * 8, (size_t)ext[0], (size_t)ext[1]);
+        m.dstPos = make_cudaPos((size_t)(a[0] - lo[0]) * 8, (size_t)(a[1] - lo[1]), (size_t)(a[2] - lo[2]));
+        m.extent = make_cudaExtent((size_t)(b[0] - a[0]) * 8, (size_t)(b[1] - a[1]), (size_t)(b[2] - a[2]));
+        m.kind = cudaMemcpyDeviceToHost;
+        CK(cudaMemcpy3DAsync(&m, c->stream));
+    }
+    CK(cudaStreamSynchronize(c->stream));
+    if (covered != ext[0] * ext[1] * ext[2]) return fail(JAC_EINVAL, "region is not entirely local to this context");
+    return JAC_OK;
+}
+
 int jac_get_layout(const jac_ctx *c, int32_t *gpu_grid, int64_t *block_extent, int64_t *iterations_done)
 {
     if (!c) return fail(JAC_EINVAL, "ctx is NULL");

@@ -38,7 +38,7 @@ EXPORTED = ["jac_plan", "jac_plan_face", "jac_create", "jac_create_rank", "jac_i
             "jac_get_block", "jac_get_block_padded", "jac_get_field", "jac_get_layout",
             "jac_block_owner", "jac_last_step_ms", "jac_set_init_box", "jac_get_field_box", "jac_local_box", "jac_profile_sweep", "jac_get_stats",
             "jac_destroy", "jac_last_error", "jac_version", "jac_set_option", "jac_nccl_id_bytes",
-            "jac_nccl_get_unique_id", "jac_nccl_init"]
+            "jac_nccl_get_unique_id", "jac_nccl_init", "jac_get_region"]
 MICROBENCH_EXPORTED = ["jac_mb_launch_latency", "jac_mb_overlap", "jac_mb_launch_rate", "jac_mb_pipeline"]
 
 _ERRNAMES = {-1: "JAC_EINVAL", -2: "JAC_EDECOMP", -3: "JAC_EDEVICE", -4: "JAC_ENOMEM",
@@ -96,6 +96,7 @@ def load() -> ctypes.CDLL:
         "jac_set_option": [vp, i32, i64],
         "jac_nccl_get_unique_id": [vp],
         "jac_nccl_init": [vp, vp],
+        "jac_get_region": [vp, P(i64), P(i64), dp],
         "jac_mb_launch_latency": [i32, i32, P(ctypes.c_double)],
         "jac_mb_overlap": [i32, i64, i32, i32, P(ctypes.c_double), P(ctypes.c_double)],
         "jac_mb_launch_rate": [i32, i32, i32, ctypes.c_double, P(ctypes.c_double)],
@@ -243,6 +244,13 @@ def jac_local_box(ctx):
     return tuple(o), tuple(e)
 
 
+def jac_get_region(ctx, lo, ext) -> np.ndarray:
+    """Interior sub-box [lo, lo+ext) (x, y, z order), returned as [ez][ey][ex]."""
+    out = np.empty((int(ext[2]), int(ext[1]), int(ext[0])), dtype=np.float64)
+    _check(load().jac_get_region(ctx, _i64x3(lo), _i64x3(ext), _dptr(out)), "jac_get_region")
+    return out
+
+
 def jac_get_layout(ctx):
     g = (ctypes.c_int32 * 3)()
     e = (ctypes.c_int64 * 3)()
@@ -359,6 +367,10 @@ class Jacobi3D:
         from the device."""
         out = np.array(like, dtype=np.float64, copy=True)
         return jac_get_field(self.ctx, out)
+
+    def region(self, lo, ext) -> np.ndarray:
+        """Interior sub-box [lo, lo+ext) (x, y, z), as [ez][ey][ex]."""
+        return jac_get_region(self.ctx, lo, ext)
 
     def local_box(self):
         """(origin, extent) of this context's ghosted bounding box, padded coords (x, y, z)."""
