@@ -417,14 +417,20 @@ def run_ours(args, D):
         sweep = {}
         for odf in (1, 2, 4, 8, 16, 32, 64):
             d2, b2, g2, _, _ = workload("c2", 1, odf)
-            Jo = make_ctx(d2, b2, g2, D)
-            Jo.set_init_hash(1)
-            ms, _ = time_ctx(Jo, K, W, D)
-            sw = Jo.profile_sweep(20)
+            runs = []
+            for _rep in range(3):  # median over 3 allocations: multi-block layouts vary +-3-5%
+                Jo = make_ctx(d2, b2, g2, D)
+                Jo.set_init_hash(1)
+                ms, _ = time_ctx(Jo, K, W, D)
+                sw = Jo.profile_sweep(20)
+                runs.append((ms, sw))
+                close_ctx(Jo, D)
+            runs.sort()
+            ms, sw = runs[1]
             sweep[str(odf)] = {"blocks": b2, "ms_per_iter": ms / K, "glups": pts * K / (ms * 1e-3) / 1e9,
                                "hbm_frac": BYTES_PER_LUP * pts / (ms / K * 1e-3) / 1e9 / peak,
-                               "sweep_kernel_us": 1e3 * sw}
-            close_ctx(Jo, D)
+                               "sweep_kernel_us": 1e3 * sw, "allocations": 3,
+                               "ms_per_iter_min_max": [runs[0][0] / K, runs[2][0] / K]}
         base = sweep["1"]["ms_per_iter"]
         for v in sweep.values():
             v["overhead_vs_odf1"] = v["ms_per_iter"] / base - 1.0

@@ -1,1 +1,2 @@
-timeout 900 python -m pytest tests/test_fullsize_gpu.py -q -x --durations=10 > gpurun_out/pytest_full.log 2>&1; echo pytest=$? >> gpurun_out/pytest_full.log
+timeout 300 python tools/order_test.py > gpurun_out/order.log 2>&1
+sleep 20; KEEP=1 timeout 300 python tools/order_test.py >> gpurun_out/order.log 2>&1
