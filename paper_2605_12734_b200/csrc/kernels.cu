@@ -295,9 +295,11 @@ __device__ __forceinline__ int tile_soff(const Geom &g, int x0)
 // Persistent-free TMA z-march: one CTA per work item.  BX x BY column tile, NT
 // threads, NS-deep plane ring, staged width W (BX + 4 with in-block x halo, or BX
 // for single-tile blocks).  Each thread owns a pair of x-points (double2) in RY rows.
+constexpr int min_ctas_per_sm(int NT, int NS) { return NT <= 128 ? 8 : (NS >= 8 ? 2 : (NS >= 6 ? 3 : 4)); }
+
 template <int BX, int BY, int W, int NT, int NS>
-__global__ void __launch_bounds__(NT, 4) sweep_tma_kernel(const __grid_constant__ CUtensorMap tmap,
-                                                          const SweepArgs a)
+__global__ void __launch_bounds__(NT, min_ctas_per_sm(NT, NS))
+    sweep_tma_kernel(const __grid_constant__ CUtensorMap tmap, const SweepArgs a)
 {
     using L = StageLayout<BX, BY, W>;
     constexpr int TXL = BX / 2;    // threads along x
@@ -347,7 +349,7 @@ __global__ void __launch_bounds__(NT, 4) sweep_tma_kernel(const __grid_constant_
         c3 = a.src * g.nslots + slot;
         xg0 = xg_array(a.xg, g, a.src, slot, 0) + t.y0;
         xg1 = xg_array(a.xg, g, a.src, slot, 1) + t.y0;
-        for (int s = 0; s < NS; ++s) mbar_init(&bars[s], 1);
+        for (int s = 0; s < NS; ++s) mbar_init(&bars[s], 1);  // producer arrive + TMA bytes
         mbar_fence_init();
         for (int q = 0; q < NS && q < nq; ++q) issue(q);
     }
@@ -367,7 +369,10 @@ __global__ void __launch_bounds__(NT, 4) sweep_tma_kernel(const __grid_constant_
     for (int r = 0; r < RY; ++r) rowoff[r] = (int64_t)(t.y0 + rg * RY + r + 1) * g.P + g.A + i;
     auto plane = [&](int q) { return stage + (q % NS) * L::STRIDE; };
     auto wait = [&](int q) { mbar_wait(&bars[q % NS], (q / NS) & 1); };
-    auto refill = [&](int q) {  // all threads are done with plane q -> load q + NS
+    // every thread is done with plane q -> the producer refills its stage with q + NS.
+    // (Per-warp "empty" mbarriers instead of this CTA barrier were measured: no robust
+    // gain, and slower for the small-block tiles.)
+    auto refill = [&](int q) {
         __syncthreads();
         if (threadIdx.x == 0 && q + NS < nq) issue(q + NS);
     };
@@ -775,10 +780,16 @@ static cudaError_t launch_tma_t(const CUtensorMap &tm, const SweepArgs &a, cudaS
     return cudaGetLastError();
 }
 
-#define JAC_TMA_VARIANTS(X)              \
-    X(TMA_WIDE, 64, 16, 68, 256, 4)      \
-    X(TMA_NARROW, 32, 16, 36, 256, 4)    \
-    X(TMA_EXACT32, 32, 16, 32, 256, 4)   \
+// Ring depth, measured on several B200 boxes: the wide tile runs a 6-stage ring
+// (3 CTAs / SM at 79 registers): 355 us per 512^3 ODF-1 sweep on every box, where 4
+// stages (4 CTAs / SM) gave 348 us on some boxes and 385 us on others; 5 stages
+// (spills), 7-8 stages (2 CTAs / SM) and 64 x 8 tiles were slower.  The narrow /
+// exact tiles (small blocks) and the 2-D kernel keep 4 stages and 4 CTAs / SM
+// (6 stages: 32^3 blocks 582 -> 655 us, 2-D 32768^2 2.53 -> 2.91 ms).
+#define JAC_TMA_VARIANTS(X)               \
+    X(TMA_WIDE, 64, 16, 68, 256, 6)       \
+    X(TMA_NARROW, 32, 16, 36, 256, 4)     \
+    X(TMA_EXACT32, 32, 16, 32, 256, 4)    \
     X(TMA_EXACT64, 64, 16, 64, 256, 4)
 
 int sweep_resident_ctas(int variant)
@@ -831,7 +842,7 @@ static cudaError_t launch2d_t(const CUtensorMap &tm, const SweepArgs &a, cudaStr
 cudaError_t launch_sweep2d_tma(const CUtensorMap &tm, const SweepArgs &a, int variant, cudaStream_t s)
 {
 #define X(V, BX, BY, W, NT, NS) \
-    if (variant == V) return launch2d_t<BX, BY, W, NT, NS>(tm, a, s, false);
+    if (variant == V) return launch2d_t<BX, BY, W, NT, 4>(tm, a, s, false);
     JAC_TMA_VARIANTS(X)
 #undef X
     return cudaErrorInvalidValue;
@@ -842,7 +853,7 @@ cudaError_t prepare_sweep2d_tma(int variant)
     const CUtensorMap *none = nullptr;
     SweepArgs dummy{};
 #define X(V, BX, BY, W, NT, NS) \
-    if (variant == V) return launch2d_t<BX, BY, W, NT, NS>(*none, dummy, nullptr, true);
+    if (variant == V) return launch2d_t<BX, BY, W, NT, 4>(*none, dummy, nullptr, true);
     JAC_TMA_VARIANTS(X)
 #undef X
     return cudaErrorInvalidValue;
