@@ -412,10 +412,11 @@ int create_common(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, in
 
     // tile shape / variant
     if (flags & JAC_F_NO_TMA) c->variant = kPlain;
-    else c->variant = (g.ex <= 32) ? jac::TMA_EXACT32 : (g.ex <= 64) ? jac::TMA_EXACT64 : jac::TMA_WIDE;
+    else c->variant = (g.ex <= 32) ? (g.ey > 16 ? jac::TMA_EXACT32_TALL : jac::TMA_EXACT32)
+                      : (g.ex <= 64) ? jac::TMA_EXACT64 : jac::TMA_WIDE;
     if (const char *s = getenv("JAC_VARIANT"); s && c->variant != kPlain) {
         const int v = atoi(s);  // tuning knob; EXACT* only where one tile spans the block row
-        if (v == jac::TMA_WIDE || v == jac::TMA_NARROW || (v == jac::TMA_EXACT32 && g.ex <= 32) ||
+        if (v == jac::TMA_WIDE || v == jac::TMA_NARROW || ((v == jac::TMA_EXACT32 || v == jac::TMA_EXACT32_TALL) && g.ex <= 32) ||
             (v == jac::TMA_EXACT64 && g.ex <= 64))
             c->variant = v;
     }
@@ -441,6 +442,7 @@ int create_common(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, in
         // 16 planes: measured best or within 2.5% of best on 512^3 (ODF 1-16), 768^3
         // and 1024^3 (64x16 tiles, 64x32 tiles were slower everywhere)
         int zchunk = 16;
+        if (g.ez <= 64) zchunk = g.ez;  // small blocks: one item marches the whole block depth
         // small grids (C1: 64^3): shorter chunks until the launch fills ~3/4 of a wave
         // (measured 24.5 -> 5.2 us per C1 iteration)
         while (zchunk > 2 && 4 * (int64_t)c->ncols * ((g.ez + zchunk - 1) / zchunk) < 3 * (int64_t)resident) zchunk /= 2;

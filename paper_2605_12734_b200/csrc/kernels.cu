@@ -785,12 +785,15 @@ static cudaError_t launch_tma_t(const CUtensorMap &tm, const SweepArgs &a, cudaS
 // stages (4 CTAs / SM) gave 348 us on some boxes and 385 us on others; 5 stages
 // (spills), 7-8 stages (2 CTAs / SM) and 64 x 8 tiles were slower.  The narrow /
 // exact tiles (small blocks) and the 2-D kernel keep 4 stages and 4 CTAs / SM
-// (6 stages: 32^3 blocks 582 -> 655 us, 2-D 32768^2 2.53 -> 2.91 ms).
+// (6 stages: 32^3 blocks 582 -> 655 us, 2-D 32768^2 2.53 -> 2.91 ms).  32-wide blocks
+// take a whole 32 x 32 face per item (C5's 32^3 blocks: 583 -> 475 us per 512^3);
+// 64 x 32 tiles spill at 64 registers and lose.
 #define JAC_TMA_VARIANTS(X)               \
     X(TMA_WIDE, 64, 16, 68, 256, 6)       \
     X(TMA_NARROW, 32, 16, 36, 256, 4)     \
     X(TMA_EXACT32, 32, 16, 32, 256, 4)    \
-    X(TMA_EXACT64, 64, 16, 64, 256, 4)
+    X(TMA_EXACT64, 64, 16, 64, 256, 4)    \
+    X(TMA_EXACT32_TALL, 32, 32, 32, 256, 4)
 
 int sweep_resident_ctas(int variant)
 {

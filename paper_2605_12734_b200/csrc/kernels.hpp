@@ -11,7 +11,8 @@ enum TmaVariant {
     TMA_WIDE = 0,    /* 64 x 16 tiles, staged 68 wide (blocks wider than 64) */
     TMA_NARROW = 1,  /* 32 x 16 tiles, staged 36 wide (blocks 33..64 wide) */
     TMA_EXACT32 = 3, /* 32 x 16 tiles, staged 32 wide: one tile per block row (ex <= 32) */
-    TMA_EXACT64 = 4  /* 64 x 16 tiles, staged 64 wide: one tile per block row (ex <= 64) */
+    TMA_EXACT64 = 4, /* 64 x 16 tiles, staged 64 wide: one tile per block row (ex <= 64) */
+    TMA_EXACT32_TALL = 12 /* 32 x 32 tiles: a whole 32^2 block face per item (ex <= 32) */
 };
 struct TileShape { int bx, by, w; };
 
