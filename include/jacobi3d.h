@@ -222,7 +222,7 @@ enum jac_stat {
     JAC_STAT_REMOTE_FACES = 5,    /* exchanged REMOTE faces per iteration */
     JAC_STAT_REMOTE_BYTES = 6,    /* bytes stored to peers per iteration */
     JAC_STAT_ARENA_BYTES = 7,     /* device bytes of the ghosted block arena */
-    JAC_STAT_SWEEP_VARIANT = 8,   /* 0 = TMA z-march, 1 = plain loads */
+    JAC_STAT_SWEEP_VARIANT = 8,   /* sweep tile variant (kernels.hpp TmaVariant; 2 = plain loads) */
     JAC_STAT_N = 9
 };
 int jac_get_stats(const jac_ctx *c, int64_t *stats /* [JAC_STAT_N] */);

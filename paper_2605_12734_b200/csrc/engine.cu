@@ -150,6 +150,7 @@ struct jac_ctx {
     CUtensorMap tmap{};
     int ntx = 1, nty = 1, ntz = 1, zc = 1;
     int nzc = 1, ncols = 1, nitems = 1, gcols = 1;
+    float tuned_ms[2] = {0.f, 0.f};  // autotune: sweep ms for the 6- and 4-stage wide tiles
 
     // cross-rank exchange
     std::vector<int32_t> peer_ranks;     // face-adjacent ranks
@@ -346,6 +347,91 @@ double *block_ptr_local(const jac_ctx *c, const int32_t nb[3], int buf, int f)
     return nullptr;
 }
 
+// Tile / work-list geometry for the current c->variant (ntx, nty, z-chunks, item
+// count, column groups).  Called at create and for every autotune candidate.
+void configure_tiles(jac_ctx *c)
+{
+    const jac::Geom &g = c->geom;
+    const uint32_t flags = c->flags;
+    const int tbx = (c->variant == kPlain) ? 64 : jac::tma_tile_shape(c->variant).bx;
+    const int tby = (c->variant == kPlain) ? 8 : jac::tma_tile_shape(c->variant).by;
+    c->ntx = (g.ex + tbx - 1) / tbx;
+    c->nty = (g.ey + tby - 1) / tby;
+    // (plain kernel) z-chunk: enough CTAs for several waves on 148 SMs, chunks of >= 16 planes
+    int zc = g.ez;
+    const int64_t target = 148 * 4 * 4;
+    while ((int64_t)c->nslots * c->ntx * c->nty * ((g.ez + zc - 1) / zc) < target && zc > 16) zc = (zc + 1) / 2;
+    if (const char *s = getenv("JAC_ZC")) zc = std::max(1, std::min(g.ez, atoi(s)));
+    c->zc = zc;
+    c->ntz = (g.ez + zc - 1) / zc;
+    // TMA kernel work list: columns cut into z-chunks of ~16 planes.  Short
+    // chunks keep concurrently running CTAs at nearby z, so the x/y halo rows one
+    // CTA stages are L2 hits for its neighbours (long marches drift apart and turn
+    // the halos into DRAM re-reads: measured +19.6% reads at 256-plane chunks);
+    // the price is 2 extra planes per chunk.
+    c->ncols = c->nslots * c->ntx * c->nty;
+    {
+        const int resident = c->variant == kPlain ? 148 * 4 : jac::sweep_resident_ctas(c->variant);
+        // 16 planes: measured best or within 2.5% of best on 512^3 (ODF 1-16), 768^3
+        // and 1024^3 (64x16 tiles, 64x32 tiles were slower everywhere)
+        int zchunk = 16;
+        if (g.ez <= 64) zchunk = g.ez;  // small blocks: one item marches the whole block depth
+        // small grids (C1: 64^3): shorter chunks until the launch fills ~3/4 of a wave
+        // (measured 24.5 -> 5.2 us per C1 iteration)
+        while (zchunk > 2 && 4 * (int64_t)c->ncols * ((g.ez + zchunk - 1) / zchunk) < 3 * (int64_t)resident) zchunk /= 2;
+        if (const char *s = getenv("JAC_ZCHUNK")) zchunk = std::max(1, atoi(s));
+        c->nzc = std::max(1, (g.ez + zchunk - 1) / zchunk);
+        c->nitems = c->ncols * c->nzc;
+        // Column groups of ~one resident wave: inside a group the chunk k+1 item of a
+        // column launches about when its chunk k item retires, so the two planes they
+        // share are still in L2.
+        int gcols = resident;
+        if (const char *s = getenv("JAC_GCOLS")) gcols = atoi(s);
+        c->gcols = std::max(1, std::min(c->ncols, gcols > 0 ? gcols : c->ncols));
+        if (flags & JAC_F_2D) {  // 2-D: items = (block, x tile, chunk of 8 y tiles), nzc = y chunks
+            c->nzc = std::max(1, (c->nty + 7) / 8);
+            c->nitems = c->nslots * c->ntx * c->nzc;
+        }
+    }
+}
+
+// Create-time autotune of the wide tile's TMA ring depth (6 stages at 3 CTAs / SM vs
+// 4 stages at 4 CTAs / SM).  Measured on this pool: which one wins depends on the
+// box (512^3 ODF 1: 348 vs 355 us on one, 385 vs 355 us on another), so each context
+// times both on its own GPU -- 1 + 3 sweeps each, exchange off -- and keeps the
+// faster.  Results are bit-identical either way.  JAC_AUTOTUNE=0 or JAC_VARIANT skip.
+int autotune(jac_ctx *c)
+{
+    if (c->variant != jac::TMA_WIDE || getenv("JAC_VARIANT")) return JAC_OK;
+    if (const char *s = getenv("JAC_AUTOTUNE"); s && atoi(s) == 0) return JAC_OK;
+    const int cands[2] = {jac::TMA_WIDE, jac::TMA_WIDE4};
+    float best_ms = 1e30f;
+    int best = jac::TMA_WIDE;
+    for (int v : cands) {
+        c->variant = v;
+        configure_tiles(c);
+        if (jac::prepare_sweep_tma(v) != cudaSuccess || jac::prepare_sweep2d_tma(v) != cudaSuccess)
+            return fail(JAC_ECUDA, "autotune: kernel attribute");
+        const jac::SweepArgs a = sweep_args(c, 0, jac::MODE_NOEXCHANGE);
+        auto launch = [&]() {
+            return (c->flags & JAC_F_2D) ? jac::launch_sweep2d_tma(c->tmap, a, v, c->stream)
+                                         : jac::launch_sweep_tma(c->tmap, a, v, c->stream);
+        };
+        CK(launch());
+        CK(cudaEventRecord(c->ev0, c->stream));
+        for (int r = 0; r < 3; ++r) CK(launch());
+        CK(cudaEventRecord(c->ev1, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+        c->tuned_ms[v == jac::TMA_WIDE ? 0 : 1] = ms / 3;
+        if (ms < best_ms) { best_ms = ms; best = v; }
+    }
+    c->variant = best;
+    configure_tiles(c);
+    return JAC_OK;
+}
+
 int create_common(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, int32_t bz,
                   int32_t n_gpus, const int32_t *gpu_grid, bool rank_mode, int32_t rank,
                   int32_t device, uint32_t flags, jac_ctx **out)
@@ -412,54 +498,16 @@ int create_common(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, in
 
     // tile shape / variant
     if (flags & JAC_F_NO_TMA) c->variant = kPlain;
-    else c->variant = (g.ex <= 32) ? (g.ey > 16 ? jac::TMA_EXACT32_TALL : jac::TMA_EXACT32)
+    else c->variant = (g.ex <= 32) ? ((g.ey > 16 && c->nslots >= 64) ? jac::TMA_EXACT32_TALL : jac::TMA_EXACT32)
                       : (g.ex <= 64) ? jac::TMA_EXACT64 : jac::TMA_WIDE;
     if (const char *s = getenv("JAC_VARIANT"); s && c->variant != kPlain) {
         const int v = atoi(s);  // tuning knob; EXACT* only where one tile spans the block row
-        if (v == jac::TMA_WIDE || v == jac::TMA_NARROW || ((v == jac::TMA_EXACT32 || v == jac::TMA_EXACT32_TALL) && g.ex <= 32) ||
+        if (v == jac::TMA_WIDE || v == jac::TMA_WIDE4 || v == jac::TMA_NARROW ||
+            ((v == jac::TMA_EXACT32 || v == jac::TMA_EXACT32_TALL) && g.ex <= 32) ||
             (v == jac::TMA_EXACT64 && g.ex <= 64))
             c->variant = v;
     }
-    const int tbx = (c->variant == kPlain) ? 64 : jac::tma_tile_shape(c->variant).bx;
-    const int tby = (c->variant == kPlain) ? 8 : jac::tma_tile_shape(c->variant).by;
-    c->ntx = (g.ex + tbx - 1) / tbx;
-    c->nty = (g.ey + tby - 1) / tby;
-    // z-chunk: enough CTAs for several waves on 148 SMs, chunks of >= 16 planes
-    int zc = g.ez;
-    const int64_t target = 148 * 4 * 4;
-    while ((int64_t)c->nslots * c->ntx * c->nty * ((g.ez + zc - 1) / zc) < target && zc > 16) zc = (zc + 1) / 2;
-    if (const char *s = getenv("JAC_ZC")) zc = std::max(1, std::min(g.ez, atoi(s)));
-    c->zc = zc;
-    c->ntz = (g.ez + zc - 1) / zc;
-    // TMA kernel work list: columns cut into z-chunks of ~16 planes.  Short
-    // chunks keep concurrently running CTAs at nearby z, so the x/y halo rows one
-    // CTA stages are L2 hits for its neighbours (long marches drift apart and turn
-    // the halos into DRAM re-reads: measured +19.6% reads at 256-plane chunks);
-    // the price is 2 extra planes per chunk.
-    c->ncols = c->nslots * c->ntx * c->nty;
-    {
-        const int resident = c->variant == kPlain ? 148 * 4 : jac::sweep_resident_ctas(c->variant);
-        // 16 planes: measured best or within 2.5% of best on 512^3 (ODF 1-16), 768^3
-        // and 1024^3 (64x16 tiles, 64x32 tiles were slower everywhere)
-        int zchunk = 16;
-        if (g.ez <= 64) zchunk = g.ez;  // small blocks: one item marches the whole block depth
-        // small grids (C1: 64^3): shorter chunks until the launch fills ~3/4 of a wave
-        // (measured 24.5 -> 5.2 us per C1 iteration)
-        while (zchunk > 2 && 4 * (int64_t)c->ncols * ((g.ez + zchunk - 1) / zchunk) < 3 * (int64_t)resident) zchunk /= 2;
-        if (const char *s = getenv("JAC_ZCHUNK")) zchunk = std::max(1, atoi(s));
-        c->nzc = std::max(1, (g.ez + zchunk - 1) / zchunk);
-        c->nitems = c->ncols * c->nzc;
-        // Column groups of ~one resident wave: inside a group the chunk k+1 item of a
-        // column launches about when its chunk k item retires, so the two planes they
-        // share are still in L2.
-        int gcols = resident;
-        if (const char *s = getenv("JAC_GCOLS")) gcols = atoi(s);
-        c->gcols = std::max(1, std::min(c->ncols, gcols > 0 ? gcols : c->ncols));
-        if (flags & JAC_F_2D) {  // 2-D: items = (block, x tile, chunk of 8 y tiles), nzc = y chunks
-            c->nzc = std::max(1, (c->nty + 7) / 8);
-            c->nitems = c->nslots * c->ntx * c->nzc;
-        }
-    }
+    configure_tiles(c);
     if (const char *s = getenv("JAC_UNROLL")) c->unroll = std::max(2, atoi(s) & ~1);
     if ((int64_t)c->nslots * c->ntx * c->nty * c->ntz > 0x7fffffffLL) {
         delete c;
@@ -545,26 +593,6 @@ int create_common(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, in
     std::sort(c->nccl_faces.begin(), c->nccl_faces.end(), [](const NcclFace &x, const NcclFace &y) {
         return x.peer != y.peer ? x.peer < y.peer : x.key < y.key;  // same order on both sides
     });
-    c->fused = rank_mode && !c->peer_ranks.empty() && sweep_mode(c) == jac::MODE_FUSED && c->variant != kPlain &&
-               !(flags & JAC_F_NCCL) && !getenv("JAC_NO_FUSED_SYNC");
-    if (c->fused) {
-        const jac::SweepArgs a0 = sweep_args(c, 0, jac::MODE_NOEXCHANGE);
-        const jac::TileShape ts = jac::tma_tile_shape(c->variant);
-        const bool two_d = (flags & JAC_F_2D) != 0;
-        std::vector<int32_t> first, last;
-        for (int32_t it = 0; it < c->nitems; ++it) {
-            const jac::TileItem t = two_d ? jac::decode_item2d(a0, it, ts.bx, ts.by) : jac::decode_item3d(a0, it, ts.bx, ts.by);
-            (jac::item_touches(a0, t, c->hblocks[t.b].remote_mask, ts.bx, ts.by, two_d) ? last : first).push_back(it);
-        }
-        // remote-touching items first: their signal leaves early in the sweep, so the
-        // next sweep's remote items (which wait for it) find it already set
-        c->nremote = (int32_t)last.size();
-        last.insert(last.end(), first.begin(), first.end());
-        if (cudaMalloc(&c->ditem_map, sizeof(int32_t) * last.size()) != cudaSuccess ||
-            cudaMemcpy(c->ditem_map, last.data(), sizeof(int32_t) * last.size(), cudaMemcpyHostToDevice) != cudaSuccess)
-            return bail(fail(JAC_ENOMEM, "item map"));
-        if (c->nremote == 0) c->fused = false;
-    }
     if (cudaMalloc(&c->dblocks, sizeof(jac::DevBlock) * c->nslots) != cudaSuccess)
         return bail(fail(JAC_ENOMEM, "cudaMalloc descriptor table"));
     if (cudaMemcpy(c->dblocks, c->hblocks.data(), sizeof(jac::DevBlock) * c->nslots, cudaMemcpyHostToDevice) != cudaSuccess)
@@ -587,6 +615,27 @@ int create_common(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, in
         for (auto &ev : c->bevents)
             if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess)
                 return bail(fail(JAC_ECUDA, "per-block event creation"));
+    }
+    if ((rc = autotune(c))) return bail(rc);  // fixes the variant: the item map depends on it
+    c->fused = rank_mode && !c->peer_ranks.empty() && sweep_mode(c) == jac::MODE_FUSED && c->variant != kPlain &&
+               !(flags & JAC_F_NCCL) && !getenv("JAC_NO_FUSED_SYNC");
+    if (c->fused) {
+        const jac::SweepArgs a0 = sweep_args(c, 0, jac::MODE_NOEXCHANGE);
+        const jac::TileShape ts = jac::tma_tile_shape(c->variant);
+        const bool two_d = (flags & JAC_F_2D) != 0;
+        std::vector<int32_t> first, last;
+        for (int32_t it = 0; it < c->nitems; ++it) {
+            const jac::TileItem t = two_d ? jac::decode_item2d(a0, it, ts.bx, ts.by) : jac::decode_item3d(a0, it, ts.bx, ts.by);
+            (jac::item_touches(a0, t, c->hblocks[t.b].remote_mask, ts.bx, ts.by, two_d) ? last : first).push_back(it);
+        }
+        // remote-touching items first: their signal leaves early in the sweep, so the
+        // next sweep's remote items (which wait for it) find it already set
+        c->nremote = (int32_t)last.size();
+        last.insert(last.end(), first.begin(), first.end());
+        if (cudaMalloc(&c->ditem_map, sizeof(int32_t) * last.size()) != cudaSuccess ||
+            cudaMemcpy(c->ditem_map, last.data(), sizeof(int32_t) * last.size(), cudaMemcpyHostToDevice) != cudaSuccess)
+            return bail(fail(JAC_ENOMEM, "item map"));
+        if (c->nremote == 0) c->fused = false;
     }
     // barrier args (peer slots filled at import)
     c->bar.ctrl = c->ctrl;

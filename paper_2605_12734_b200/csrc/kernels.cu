@@ -780,16 +780,18 @@ static cudaError_t launch_tma_t(const CUtensorMap &tm, const SweepArgs &a, cudaS
     return cudaGetLastError();
 }
 
-// Ring depth, measured on several B200 boxes: the wide tile runs a 6-stage ring
-// (3 CTAs / SM at 79 registers): 355 us per 512^3 ODF-1 sweep on every box, where 4
-// stages (4 CTAs / SM) gave 348 us on some boxes and 385 us on others; 5 stages
-// (spills), 7-8 stages (2 CTAs / SM) and 64 x 8 tiles were slower.  The narrow /
-// exact tiles (small blocks) and the 2-D kernel keep 4 stages and 4 CTAs / SM
-// (6 stages: 32^3 blocks 582 -> 655 us, 2-D 32768^2 2.53 -> 2.91 ms).  32-wide blocks
+// Ring depth, measured on several B200 boxes: for the wide tile a 6-stage ring (3 CTAs
+// / SM at 79 registers) gave 355 us per 512^3 ODF-1 sweep on every box, a 4-stage
+// ring (4 CTAs / SM) 348 us on some and 385 us on others, so jac_create times both
+// (engine.cu: autotune) -- also for the 2-D kernel (32768^2: 2.53 ms at 4 stages vs
+// 2.91 ms at 6 on one box).  5 stages (spills), 7-8 stages (2 CTAs / SM) and 64 x 8
+// tiles were slower everywhere.  The narrow / exact tiles (small blocks) keep 4
+// stages (6 stages: 32^3 blocks 582 -> 655 us).  32-wide blocks
 // take a whole 32 x 32 face per item (C5's 32^3 blocks: 583 -> 475 us per 512^3);
 // 64 x 32 tiles spill at 64 registers and lose.
 #define JAC_TMA_VARIANTS(X)               \
     X(TMA_WIDE, 64, 16, 68, 256, 6)       \
+    X(TMA_WIDE4, 64, 16, 68, 256, 4)      \
     X(TMA_NARROW, 32, 16, 36, 256, 4)     \
     X(TMA_EXACT32, 32, 16, 32, 256, 4)    \
     X(TMA_EXACT64, 64, 16, 64, 256, 4)    \
@@ -845,7 +847,7 @@ static cudaError_t launch2d_t(const CUtensorMap &tm, const SweepArgs &a, cudaStr
 cudaError_t launch_sweep2d_tma(const CUtensorMap &tm, const SweepArgs &a, int variant, cudaStream_t s)
 {
 #define X(V, BX, BY, W, NT, NS) \
-    if (variant == V) return launch2d_t<BX, BY, W, NT, 4>(tm, a, s, false);
+    if (variant == V) return launch2d_t<BX, BY, W, NT, NS>(tm, a, s, false);
     JAC_TMA_VARIANTS(X)
 #undef X
     return cudaErrorInvalidValue;
@@ -856,7 +858,7 @@ cudaError_t prepare_sweep2d_tma(int variant)
     const CUtensorMap *none = nullptr;
     SweepArgs dummy{};
 #define X(V, BX, BY, W, NT, NS) \
-    if (variant == V) return launch2d_t<BX, BY, W, NT, 4>(*none, dummy, nullptr, true);
+    if (variant == V) return launch2d_t<BX, BY, W, NT, NS>(*none, dummy, nullptr, true);
     JAC_TMA_VARIANTS(X)
 #undef X
     return cudaErrorInvalidValue;

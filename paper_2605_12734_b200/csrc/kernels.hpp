@@ -8,7 +8,8 @@
 namespace jac {
 
 enum TmaVariant {
-    TMA_WIDE = 0,    /* 64 x 16 tiles, staged 68 wide (blocks wider than 64) */
+    TMA_WIDE = 0,    /* 64 x 16 tiles, staged 68 wide (blocks wider than 64), 6-stage ring */
+    TMA_WIDE4 = 5,   /* the same with a 4-stage ring (autotune candidate) */
     TMA_NARROW = 1,  /* 32 x 16 tiles, staged 36 wide (blocks 33..64 wide) */
     TMA_EXACT32 = 3, /* 32 x 16 tiles, staged 32 wide: one tile per block row (ex <= 32) */
     TMA_EXACT64 = 4, /* 64 x 16 tiles, staged 64 wide: one tile per block row (ex <= 64) */

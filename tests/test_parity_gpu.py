@@ -201,7 +201,7 @@ def test_c2_full_size_bench_config():
     _lightcone_check(got, u0, n, [(0, 0, 0), (252, 252, 252), (504, 100, 255), (127, 383, 504)])
 
 
-@pytest.mark.parametrize("variant", ["0", "1", "3", "4", "12"])
+@pytest.mark.parametrize("variant", ["0", "1", "3", "4", "5", "12"])
 @pytest.mark.parametrize("dims,blocks", [((64, 40, 36), (2, 2, 2)), ((128, 34, 20), (2, 1, 1)),
                                          ((58, 30, 17), (2, 1, 1)), ((130, 51, 33), (1, 3, 1))])
 def test_tma_tile_variants(monkeypatch, variant, dims, blocks):
@@ -232,3 +232,14 @@ def test_paper_style_per_block_mode(threads, dims, blocks, extra):
     assert_bits(got, ref(u0, 7))
     nb = blocks[0] * blocks[1] * blocks[2]
     assert st["kernels_per_iter"] == nb + 2 * st["local_faces"]
+
+
+def test_autotune_picks_a_wide_variant_and_stays_exact():
+    """jac_create times the 6- and 4-stage wide tiles on this GPU and keeps one;
+    either way the result is the oracle's."""
+    u0 = JI.hash_field(192, 96, 64, seed=2)
+    with jb.Jacobi3D((192, 96, 64), (1, 1, 1)) as s:
+        assert s.stats()["sweep_variant"] in (0, 5)
+        s.set_init(u0)
+        s.step(6)
+        assert_bits(s.field(u0), ref(u0, 6))

@@ -1,2 +1,2 @@
 timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$? >> gpurun_out/pytest_gpu.log
-ITERS=30 timeout 300 python tools/perf_shapes.py 512x512x512:1x1x1 512x512x512:2x2x2 512x512x512:2x2x4 512x512x512:4x4x4 512x512x512:8x8x8 512x512x512:16x16x16 1024x1024x1024:32x32x32 64x64x64:2x2x2 2>&1 | cut -c1-100 > gpurun_out/final_shapes.log
+for r in 1 2; do ITERS=40 timeout 200 python tools/quick_perf.py 2>&1 | cut -c1-100; FLAGS=512 ITERS=10 timeout 300 python tools/perf_shapes.py 32768x32768x1:2x4x1 2>&1 | cut -c1-110; done > gpurun_out/at.log
