@@ -381,6 +381,27 @@ def run_ours(args, D):
     # ---- e2e through the public API with pinned host buffers
     import jac_inputs as JI
     origin, extent = J.local_box()
+    if args.no_e2e:
+        close_ctx(J, D)
+        e2e_val, h2d, d2h = None, 0, 0
+    else:
+        e2e_val, h2d, d2h = run_e2e(J, D, dims, origin, extent, pts, pts_gpu, K)
+    nccl_ablation = None
+    if D.world > 1 and not args.no_sweep:  # NCCL send/recv of packed faces instead of peer stores
+        Jn = make_ctx(dims, blocks, g, D, flags=JB.JAC_F_NCCL)
+        Jn.set_init_hash(1)
+        ms_n, _ = time_ctx(Jn, K, W, D)
+        nccl_ablation = {"ms_per_iter": ms_n / K, "glups": pts * K / (ms_n * 1e-3) / 1e9,
+                         "vs_peer_stores": ms_n / K / ms_iter}
+        close_ctx(Jn, D)
+    return finish_ours(args, D, K, W, dims, blocks, g, label, scaling, pts, pts_gpu, peak, peak_src, value, ms_iter,
+                       st, sweep_ms, achieved, traffic, e2e_val, h2d, d2h, launches, sampler, nccl_ablation)
+
+
+def run_e2e(J, D, dims, origin, extent, pts, pts_gpu, K):
+    import numpy as np
+    import torch
+    import jac_inputs as JI
     host_in = torch.empty((extent[2], extent[1], extent[0]), dtype=torch.float64, pin_memory=True).numpy()
     if MODE_2D[0]:
         host_in[0] = JI.hash_values(1, (np.arange(origin[1], origin[1] + extent[1], dtype=np.uint64)[:, None]
@@ -399,16 +420,12 @@ def run_ours(args, D):
     h2d = host_in.nbytes
     d2h = pts_gpu * 8
     close_ctx(J, D)
+    return e2e_val, h2d, d2h
 
-    # ---- N > 1 ablation: NCCL send/recv of packed faces instead of in-kernel peer stores
-    nccl_ablation = None
-    if D.world > 1 and not args.no_sweep:
-        Jn = make_ctx(dims, blocks, g, D, flags=JB.JAC_F_NCCL)
-        Jn.set_init_hash(1)
-        ms_n, _ = time_ctx(Jn, K, W, D)
-        nccl_ablation = {"ms_per_iter": ms_n / K, "glups": pts * K / (ms_n * 1e-3) / 1e9,
-                         "vs_peer_stores": ms_n / K / ms_iter}
-        close_ctx(Jn, D)
+
+def finish_ours(args, D, K, W, dims, blocks, g, label, scaling, pts, pts_gpu, peak, peak_src, value, ms_iter, st,
+                sweep_ms, achieved, traffic, e2e_val, h2d, d2h, launches, sampler, nccl_ablation):
+    from paper_2605_12734_b200 import jacobi3d as JB
 
     # ---- ODF sweep + ablations (N = 1, c2)
     sweep = None
@@ -487,9 +504,10 @@ def run_ours(args, D):
                          "sweep_share_of_step": sweep_ms / ms_iter},
             "hbm_frac_step": BYTES_PER_LUP * pts_gpu / (ms_iter * 1e-3) / 1e9 / peak,
             "hbm_frac_step_vs_8TBs": BYTES_PER_LUP * pts_gpu / (ms_iter * 1e-3) / 1e9 / 8000.0,
-            "e2e": {"value": e2e_val, "unit": "GLUP/s", "h2d_bytes_per_step": h2d / K, "d2h_bytes_per_step": d2h / K,
-                    "note": f"one job = jac_set_init_box (pinned H2D {h2d} B) + jac_step({K}) + "
-                            f"jac_get_field_box (pinned D2H {d2h} B); bytes amortised per iteration"},
+            "e2e": None if e2e_val is None else {
+                "value": e2e_val, "unit": "GLUP/s", "h2d_bytes_per_step": h2d / K, "d2h_bytes_per_step": d2h / K,
+                "note": f"one job = jac_set_init_box (pinned H2D {h2d} B) + jac_step({K}) + "
+                        f"jac_get_field_box (pinned D2H {d2h} B); bytes amortised per iteration"},
             "gpu_launches": launches,
             "kernels_per_iter": st["kernels_per_iter"],
             "clocks": sampler.summary(),
@@ -519,6 +537,7 @@ def main():
     ap.add_argument("--odf", type=int, default=8)
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the e2e job (supplementary runs only)")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     args = ap.parse_args()
     D = Dist()
