@@ -295,7 +295,10 @@ __device__ __forceinline__ int tile_soff(const Geom &g, int x0)
 // Persistent-free TMA z-march: one CTA per work item.  BX x BY column tile, NT
 // threads, NS-deep plane ring, staged width W (BX + 4 with in-block x halo, or BX
 // for single-tile blocks).  Each thread owns a pair of x-points (double2) in RY rows.
-constexpr int min_ctas_per_sm(int NT, int NS) { return NT <= 128 ? 8 : (NS >= 8 ? 2 : (NS >= 6 ? 3 : 4)); }
+constexpr int min_ctas_per_sm(int NT, int NS)
+{
+    return NT >= 512 ? 2 : NT <= 128 ? 8 : (NS >= 8 ? 2 : (NS >= 6 ? 3 : 4));
+}
 
 template <int BX, int BY, int W, int NT, int NS>
 __global__ void __launch_bounds__(NT, min_ctas_per_sm(NT, NS))
@@ -786,7 +789,8 @@ static cudaError_t launch_tma_t(const CUtensorMap &tm, const SweepArgs &a, cudaS
 // (engine.cu: autotune) -- also for the 2-D kernel (32768^2: 2.53 ms at 4 stages vs
 // 2.91 ms at 6 on one box).  5 stages (spills), 7-8 stages (2 CTAs / SM) and 64 x 8
 // tiles were slower everywhere.  The narrow / exact tiles (small blocks) keep 4
-// stages (6 stages: 32^3 blocks 582 -> 655 us).  32-wide blocks
+// stages (6 stages: 32^3 blocks 582 -> 655 us).  128 x 16 tiles (256 threads: spills;
+// 512 threads: 2 CTAs / SM) were 1-8% slower than 64 x 16.  32-wide blocks
 // take a whole 32 x 32 face per item (C5's 32^3 blocks: 583 -> 475 us per 512^3);
 // 64 x 32 tiles spill at 64 registers and lose.
 #define JAC_TMA_VARIANTS(X)               \
