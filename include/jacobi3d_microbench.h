@@ -45,6 +45,14 @@ int jac_mb_launch_rate(int32_t device, int32_t chares, int32_t threads, double s
  * message on the destination.  *us = time until the last transfer (and kernel) done. */
 int jac_mb_pipeline(int32_t src, int32_t dst, int64_t total_bytes, int32_t odf, int32_t with_compute, double *us);
 
+/* E4/E5 with the design's transport: the same `odf` messages (separate buffers,
+ * 4 KiB apart) moved by ONE kernel on `src` that stores them into `dst`'s memory over
+ * NVLink (message table on the device, as the sweep's face table); with
+ * `with_compute` one batched O(n) kernel on `dst` consumes all messages.  Host wall
+ * time from launch until both devices are done, best of 5. */
+int jac_mb_pipeline_batched(int32_t src, int32_t dst, int64_t total_bytes, int32_t odf, int32_t with_compute,
+                            double *us);
+
 #if defined(__GNUC__)
 #pragma GCC visibility pop
 #endif

@@ -76,6 +76,34 @@ __global__ void consume_kernel(double *p, int64_t n)
 
 typedef CUresult (*PFN_waitValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
 
+struct Msg {
+    const double *src;
+    double *dst;
+    int64_t n;  // doubles
+};
+
+// every CTA walks the message table; message m is split over the grid
+__global__ void batched_copy_kernel(const Msg *msgs, int nmsg)
+{
+    for (int m = 0; m < nmsg; ++m) {
+        const Msg g = msgs[m];
+        const int64_t n2 = g.n / 2;
+        const double2 *s = reinterpret_cast<const double2 *>(g.src);
+        double2 *d = reinterpret_cast<double2 *>(g.dst);
+        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n2; i += (int64_t)gridDim.x * blockDim.x)
+            d[i] = s[i];
+    }
+}
+
+__global__ void batched_consume_kernel(const Msg *msgs, int nmsg)
+{
+    for (int m = 0; m < nmsg; ++m) {
+        double *p = msgs[m].dst;
+        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < msgs[m].n; i += (int64_t)gridDim.x * blockDim.x)
+            p[i] = p[i] * 1.0000001 + 1e-12;
+    }
+}
+
 }  // namespace
 
 extern "C" {
@@ -274,6 +302,84 @@ int jac_mb_pipeline(int32_t src, int32_t dst, int64_t total_bytes, int32_t odf, 
     cudaFree(b);
     cudaSetDevice(src);
     cudaFree(a);
+    return JAC_OK;
+}
+
+int jac_mb_pipeline_batched(int32_t src, int32_t dst, int64_t total_bytes, int32_t odf, int32_t with_compute,
+                            double *us)
+{
+    if (!us || odf < 1 || total_bytes < 16 * (int64_t)odf)
+        return mb_fail(JAC_EINVAL, "need odf >= 1, total_bytes >= 16*odf");
+    int ndev = 0;
+    MCK(cudaGetDeviceCount(&ndev));
+    if (src < 0 || dst < 0 || src >= ndev || dst >= ndev) return mb_fail(JAC_EDEVICE, "src/dst device not present");
+    const int64_t chunk = (total_bytes / odf) / 16 * 16;  // bytes per message
+    const int64_t pitch = chunk + 4096;                    // messages live in separate buffers
+    char *a = nullptr, *b = nullptr;
+    MCK(cudaSetDevice(dst));
+    MCK(cudaMalloc(&b, pitch * odf));
+    MCK(cudaSetDevice(src));
+    MCK(cudaMalloc(&a, pitch * odf));
+    MCK(cudaMemset(a, 0, pitch * odf));
+    if (src != dst) {
+        int can = 0;
+        MCK(cudaDeviceCanAccessPeer(&can, src, dst));
+        if (!can) return mb_fail(JAC_EDEVICE, "no peer access between devices %d and %d", src, dst);
+        cudaError_t e = cudaDeviceEnablePeerAccess(dst, 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) return mb_fail(JAC_ECUDA, "enable peer access");
+        cudaGetLastError();
+    }
+    std::vector<Msg> h(odf);
+    for (int k = 0; k < odf; ++k)
+        h[k] = {reinterpret_cast<const double *>(a + k * pitch), reinterpret_cast<double *>(b + k * pitch), chunk / 8};
+    Msg *dmsg_src = nullptr, *dmsg_dst = nullptr;
+    MCK(cudaMalloc(&dmsg_src, sizeof(Msg) * odf));
+    MCK(cudaMemcpy(dmsg_src, h.data(), sizeof(Msg) * odf, cudaMemcpyHostToDevice));
+    cudaStream_t ss, sd;
+    MCK(cudaStreamCreateWithFlags(&ss, cudaStreamNonBlocking));
+    MCK(cudaSetDevice(dst));
+    MCK(cudaMalloc(&dmsg_dst, sizeof(Msg) * odf));
+    MCK(cudaMemcpy(dmsg_dst, h.data(), sizeof(Msg) * odf, cudaMemcpyHostToDevice));
+    MCK(cudaStreamCreateWithFlags(&sd, cudaStreamNonBlocking));
+    cudaEvent_t done;
+    MCK(cudaSetDevice(src));
+    MCK(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, src);
+    auto run = [&]() -> int {
+        MCK(cudaSetDevice(src));
+        batched_copy_kernel<<<sms * 4, 256, 0, ss>>>(dmsg_src, odf);
+        MCK(cudaGetLastError());
+        MCK(cudaEventRecord(done, ss));
+        if (with_compute) {
+            MCK(cudaSetDevice(dst));
+            MCK(cudaStreamWaitEvent(sd, done, 0));
+            batched_consume_kernel<<<sms * 4, 256, 0, sd>>>(dmsg_dst, odf);
+            MCK(cudaGetLastError());
+            MCK(cudaStreamSynchronize(sd));
+        }
+        MCK(cudaSetDevice(src));
+        MCK(cudaStreamSynchronize(ss));
+        return JAC_OK;
+    };
+    int rc;
+    for (int w = 0; w < 3; ++w)
+        if ((rc = run())) return rc;
+    double best = 1e300;
+    for (int rep = 0; rep < 5; ++rep) {
+        const double t0 = now_us();
+        if ((rc = run())) return rc;
+        best = std::min(best, now_us() - t0);
+    }
+    *us = best;
+    cudaEventDestroy(done);
+    cudaStreamDestroy(ss);
+    cudaFree(dmsg_src);
+    cudaFree(a);
+    cudaSetDevice(dst);
+    cudaStreamDestroy(sd);
+    cudaFree(dmsg_dst);
+    cudaFree(b);
     return JAC_OK;
 }
 

@@ -39,7 +39,8 @@ EXPORTED = ["jac_plan", "jac_plan_face", "jac_create", "jac_create_rank", "jac_i
             "jac_block_owner", "jac_last_step_ms", "jac_set_init_box", "jac_get_field_box", "jac_local_box", "jac_profile_sweep", "jac_get_stats",
             "jac_destroy", "jac_last_error", "jac_version", "jac_set_option", "jac_nccl_id_bytes",
             "jac_nccl_get_unique_id", "jac_nccl_init", "jac_get_region"]
-MICROBENCH_EXPORTED = ["jac_mb_launch_latency", "jac_mb_overlap", "jac_mb_launch_rate", "jac_mb_pipeline"]
+MICROBENCH_EXPORTED = ["jac_mb_launch_latency", "jac_mb_overlap", "jac_mb_launch_rate", "jac_mb_pipeline",
+                       "jac_mb_pipeline_batched"]
 
 _ERRNAMES = {-1: "JAC_EINVAL", -2: "JAC_EDECOMP", -3: "JAC_EDEVICE", -4: "JAC_ENOMEM",
              -5: "JAC_ECUDA", -6: "JAC_ENCCL", -7: "JAC_ESTATE"}
@@ -101,6 +102,7 @@ def load() -> ctypes.CDLL:
         "jac_mb_overlap": [i32, i64, i32, i32, P(ctypes.c_double), P(ctypes.c_double)],
         "jac_mb_launch_rate": [i32, i32, i32, ctypes.c_double, P(ctypes.c_double)],
         "jac_mb_pipeline": [i32, i32, i64, i32, i32, P(ctypes.c_double)],
+        "jac_mb_pipeline_batched": [i32, i32, i64, i32, i32, P(ctypes.c_double)],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -309,6 +311,13 @@ def jac_mb_launch_rate(chares, threads, seconds=0.5, device=0) -> float:
 def jac_mb_pipeline(src, dst, total_bytes, odf, with_compute=False) -> float:
     v = ctypes.c_double()
     _check(load().jac_mb_pipeline(src, dst, total_bytes, odf, int(bool(with_compute)), ctypes.byref(v)), "jac_mb_pipeline")
+    return v.value
+
+
+def jac_mb_pipeline_batched(src, dst, total_bytes, odf, with_compute=False) -> float:
+    v = ctypes.c_double()
+    _check(load().jac_mb_pipeline_batched(src, dst, total_bytes, odf, int(bool(with_compute)), ctypes.byref(v)),
+           "jac_mb_pipeline_batched")
     return v.value
 
 

@@ -22,5 +22,6 @@ def test_launch_rate_and_pipeline():
     assert J.jac_mb_launch_rate(2, 1, 0.1) > 1000
     us = J.jac_mb_pipeline(0, 0, 1 << 22, 4, True)
     assert us > 0
+    assert J.jac_mb_pipeline_batched(0, 0, 1 << 22, 16, True) > 0
     with pytest.raises(J.JacError):
         J.jac_mb_pipeline(0, 0, 16, 4, False)

@@ -27,7 +27,9 @@ for mb in (0.5, 2, 8, 64):
     for odf in (1, 2, 4, 8, 16, 32, 64):
         for comp in (0, 1):
             us = J.jac_mb_pipeline(0, dst, nbytes, odf, comp)
+            ub = J.jac_mb_pipeline_batched(0, dst, nbytes, odf, comp)
             e4[f"{mb}MiB_odf{odf}_c{comp}"] = {"MiB": mb, "odf": odf, "compute": comp, "us": us,
-                                                "GBps": nbytes / us / 1e3}
+                                                "GBps": nbytes / us / 1e3, "batched_kernel_us": ub,
+                                                "batched_GBps": nbytes / ub / 1e3}
 out["E4E5_pipeline"] = {"src": 0, "dst": dst, "rows": e4}
 print(json.dumps(out))
