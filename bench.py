@@ -462,22 +462,27 @@ def finish_ours(args, D, K, W, dims, blocks, g, label, scaling, pts, pts_gpu, pe
                                "vs_default": ms / K / sweep["16"]["ms_per_iter"]}
             close_ctx(Ja, D)
 
-    # ---- NEXT-2 A/B: paper-style per-block streams (1 and 4 launching threads)
+    # ---- NEXT-2 A/B: paper-style per-block streams (1 and 4 launching threads), on the
+    # 3-D headline workload and on the paper's own Jacobi2D
     paper_style = None
-    if args.gpus == 1 and args.config == "c2" and not args.no_sweep:
+    if args.gpus == 1 and args.config in ("c2", "j2d") and not args.no_sweep:
         paper_style = {}
         for odf in (8, 16, 64):
-            d2, b2, g2, _, _ = workload("c2", 1, odf)
+            d2, b2, g2, _, _ = workload(args.config, 1, odf)
             for th in (1, 4):
                 Jp = make_ctx(d2, b2, g2, D, flags=JB.JAC_F_PER_BLOCK)
                 Jp.set_option(JB.JAC_OPT_LAUNCH_THREADS, th)
                 Jp.set_init_hash(1)
                 kp = 20
                 ms, launches_p = time_ctx(Jp, kp, W, D)
+                Jb = make_ctx(d2, b2, g2, D)  # the batched path on the same decomposition
+                Jb.set_init_hash(1)
+                ms_b, _ = time_ctx(Jb, kp, W, D)
+                close_ctx(Jb, D)
                 paper_style[f"odf{odf}_threads{th}"] = {
                     "ms_per_iter": ms / kp, "glups": pts * kp / (ms * 1e-3) / 1e9,
-                    "kernels_per_iter": launches_p // kp,
-                    "vs_batched": ms / kp / sweep[str(odf)]["ms_per_iter"]}
+                    "kernels_per_iter": launches_p // kp, "batched_ms_per_iter": ms_b / kp,
+                    "vs_batched": ms / ms_b}
                 close_ctx(Jp, D)
 
     cpu = None

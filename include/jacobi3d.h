@@ -82,13 +82,14 @@ enum jac_flags {
                                       (SPEC.md:474), ordered by per-block events; no graph.
                                       Launching host threads (the paper's PEs per process,
                                       PAPER.md:95) via jac_set_option.  One GPU only
-                                      (n_gpus == 1 or JAC_F_VIRTUAL_GPUS). */
+                                      (n_gpus == 1 or JAC_F_VIRTUAL_GPUS); 3-D or 2-D. */
     JAC_F_2D = 1u << 9             /* Jacobi2D (the paper's evaluated app,
                                       PAPER.md:280-294): nz == 1, bz == 1; 5-point mean
                                       u' = ((((c + x-) + x+) + y-) + y+) * fl(1/5)
                                       ("5-point average"); padded host
                                       arrays are (ny+2)*(nx+2) (no z shell); hash init
-                                      key p = j*(nx+2) + i.  Fused TMA path only. */
+                                      key p = j*(nx+2) + i.  TMA paths only (fused or
+                                      JAC_F_PER_BLOCK). */
 };
 
 /* Options for jac_set_option. */

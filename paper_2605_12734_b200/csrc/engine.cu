@@ -446,8 +446,8 @@ int create_common(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, in
         return fail(JAC_EINVAL, "flags: JAC_F_NCCL needs a rank context (jac_create_rank) and the fused sweep");
     if ((flags & JAC_F_2D) && (nz != 1 || bz != 1))
         return fail(JAC_EINVAL, "flags: JAC_F_2D needs nz == 1 and bz == 1 (the 2-D grid is nx x ny)");
-    if ((flags & JAC_F_2D) && (flags & (JAC_F_UNFUSED_PACK | JAC_F_NO_TMA | JAC_F_PER_BLOCK)))
-        return fail(JAC_EINVAL, "flags: JAC_F_2D runs the fused TMA path only (no UNFUSED_PACK / NO_TMA / PER_BLOCK)");
+    if ((flags & JAC_F_2D) && (flags & (JAC_F_UNFUSED_PACK | JAC_F_NO_TMA)))
+        return fail(JAC_EINVAL, "flags: JAC_F_2D runs the TMA path (no UNFUSED_PACK / NO_TMA)");
     if ((flags & JAC_F_PER_BLOCK) && (rank_mode || (flags & (JAC_F_UNFUSED_PACK | JAC_F_SKIP_EXCHANGE))))
         return fail(JAC_EINVAL, "flags: JAC_F_PER_BLOCK runs on one GPU (not a rank context) and excludes "
                                 "JAC_F_UNFUSED_PACK / JAC_F_SKIP_EXCHANGE");
@@ -682,6 +682,9 @@ int enqueue_per_block(jac_ctx *c, int64_t t, int first, int stride)
         a.ntz = c->ntz;
         if (c->variant == kPlain) {
             CK(jac::launch_sweep_plain_one(a, s));
+        } else if (c->flags & JAC_F_2D) {
+            a.nitems = c->ntx * c->nzc;  // (x tile, y chunk) items of this block
+            CK(jac::launch_sweep2d_tma(c->tmap, a, c->variant, s));
         } else {
             CK(jac::launch_sweep_tma(c->tmap, a, c->variant, s));
         }

@@ -588,7 +588,7 @@ __global__ void __launch_bounds__(256) ghost_fill_kernel(const SweepArgs a, int 
         int64_t off;
         if (d == 1) {
             const int64_t k = e / g.ex, i = e % g.ex;
-            off = (k + 1) * g.Q + ((f == YM) ? 0 : (int64_t)(g.ey + 1) * g.P) + g.A + i;
+            off = (k + g.zg) * g.Q + ((f == YM) ? 0 : (int64_t)(g.ey + 1) * g.P) + g.A + i;
         } else {
             const int64_t j = e / g.ex, i = e % g.ex;
             off = ((f == ZM) ? 0 : (int64_t)(g.ez + 1) * g.Q) + (j + 1) * g.P + g.A + i;
@@ -614,10 +614,10 @@ __global__ void __launch_bounds__(256) pack_face_kernel(const SweepArgs a, int s
         int64_t off;
         if (d == 0) {
             const int64_t k = e / g.ey, j = e % g.ey;
-            off = (k + 1) * g.Q + (j + 1) * g.P + g.A + ((f == XM) ? 0 : g.ex - 1);
+            off = (k + g.zg) * g.Q + (j + 1) * g.P + g.A + ((f == XM) ? 0 : g.ex - 1);
         } else if (d == 1) {
             const int64_t k = e / g.ex, i = e % g.ex;
-            off = (k + 1) * g.Q + ((f == YM) ? 1 : (int64_t)g.ey) * g.P + g.A + i;
+            off = (k + g.zg) * g.Q + ((f == YM) ? 1 : (int64_t)g.ey) * g.P + g.A + i;
         } else {
             const int64_t j = e / g.ex, i = e % g.ex;
             off = ((f == ZM) ? 1 : (int64_t)g.ez) * g.Q + (j + 1) * g.P + g.A + i;
@@ -645,7 +645,7 @@ __global__ void __launch_bounds__(256) unpack_face_kernel(const SweepArgs a, int
         int64_t off;
         if (d == 1) {
             const int64_t k = e / g.ex, i = e % g.ex;
-            off = (k + 1) * g.Q + ((f == YM) ? 0 : (int64_t)(g.ey + 1) * g.P) + g.A + i;
+            off = (k + g.zg) * g.Q + ((f == YM) ? 0 : (int64_t)(g.ey + 1) * g.P) + g.A + i;
         } else {
             const int64_t j = e / g.ex, i = e % g.ex;
             off = ((f == ZM) ? 0 : (int64_t)(g.ez + 1) * g.Q) + (j + 1) * g.P + g.A + i;

@@ -62,3 +62,17 @@ def test_2d_rejects_3d_shapes_and_flags():
         jb.Jacobi3D((8, 8, 2), (1, 1, 1), flags=J.JAC_F_2D)
     with pytest.raises(J.JacError):
         jb.Jacobi2D((8, 8), (1, 1), flags=J.JAC_F_NO_TMA)
+
+
+@pytest.mark.parametrize("threads", [1, 4])
+@pytest.mark.parametrize("dims,blocks", [((256, 192), (4, 3)), ((130, 66), (2, 2)), ((64, 64), (1, 1))])
+def test_2d_paper_style_per_block_mode(threads, dims, blocks):
+    """NEXT-2 on the paper's own app: per-block streams, per-face pack / unpack
+    launches, several launching threads -- bit-identical to the 2-D oracle."""
+    u0 = JI.hash_field2d(*dims, seed=1)
+    with jb.Jacobi2D(dims, blocks, flags=J.JAC_F_PER_BLOCK) as s:
+        s.set_option(J.JAC_OPT_LAUNCH_THREADS, threads)
+        s.set_init(u0)
+        s.step(4)
+        s.step(5)
+        bits(s.field(u0), ref(u0, 9))

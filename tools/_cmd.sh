@@ -1,3 +1,2 @@
-JAC_VARIANT=13 timeout 300 python -m pytest tests/test_parity_gpu.py -q -x -k "odf_sweep or ragged or c1_config" > gpurun_out/pytest_v.log 2>&1; echo rc=$? >> gpurun_out/pytest_v.log
-JAC_VARIANT=14 timeout 300 python -m pytest tests/test_parity_gpu.py -q -x -k "odf_sweep or ragged or c1_config" >> gpurun_out/pytest_v.log 2>&1; echo rc=$? >> gpurun_out/pytest_v.log
-for r in 1 2; do for v in 0 5 13 14; do echo "== variant $v"; JAC_VARIANT=$v ITERS=30 timeout 300 python tools/perf_shapes.py 512x512x512:1x1x1 512x512x512:2x2x2 512x512x512:2x2x4 1024x1024x1024:1x1x1 2>&1 | cut -c1-90; done; done > gpurun_out/xw.log
+timeout 600 python -m pytest tests/test_parity2d_gpu.py tests/test_parity_gpu.py -q -x > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$? >> gpurun_out/pytest_gpu.log
+timeout 900 python bench.py --config j2d --steps 50 --warmup 3 > gpurun_out/bench_j2d.json 2> gpurun_out/bench_j2d.err; echo rc=$? >> gpurun_out/bench_j2d.err
