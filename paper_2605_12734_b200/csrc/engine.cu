@@ -136,7 +136,6 @@ struct jac_ctx {
     int device = 0;
     std::vector<int32_t> parts;  // partitions hosted by this context
     int32_t nslots = 0;
-    std::vector<int32_t> slot_part, slot_local;  // partition / local slot of each slot
 
     jac::Geom geom{};
     char *alloc = nullptr;    // single allocation: [ctrl][arena][outbox]
@@ -1071,7 +1070,12 @@ int jac_profile_sweep(jac_ctx *c, int32_t n, double *avg_ms)
     if (!c->inited) return fail(JAC_ESTATE, "jac_profile_sweep before init");
     if (c->flags & JAC_F_PER_BLOCK) return fail(JAC_EINVAL, "jac_profile_sweep: not available with JAC_F_PER_BLOCK");
     CK(cudaSetDevice(c->device));
-    std::vector<cudaEvent_t> ev(2 * (size_t)n);
+    struct Events {  // destroyed on every return path
+        std::vector<cudaEvent_t> v;
+        ~Events() { for (cudaEvent_t e : v) if (e) cudaEventDestroy(e); }
+    } evs;
+    evs.v.assign(2 * (size_t)n, nullptr);
+    std::vector<cudaEvent_t> &ev = evs.v;
     for (auto &e : ev) CK(cudaEventCreate(&e));
     int src = (int)(c->iters & 1);
     // The n iterations are captured into one graph with event-record nodes around
@@ -1098,7 +1102,6 @@ int jac_profile_sweep(jac_ctx *c, int32_t n, double *avg_ms)
         CK(cudaEventElapsedTime(&ms, ev[2 * it], ev[2 * it + 1]));
         tot += ms;
     }
-    for (auto &e : ev) cudaEventDestroy(e);
     c->iters += n;
     c->kernel_launches += (int64_t)n * c->kernels_per_iter();
     *avg_ms = tot / n;

@@ -859,10 +859,10 @@ cudaError_t launch_sweep2d_tma(const CUtensorMap &tm, const SweepArgs &a, int va
 
 cudaError_t prepare_sweep2d_tma(int variant)
 {
-    const CUtensorMap *none = nullptr;
+    static const CUtensorMap none{};  // not read: prepare_only sets the attribute only
     SweepArgs dummy{};
 #define X(V, BX, BY, W, NT, NS) \
-    if (variant == V) return launch2d_t<BX, BY, W, NT, NS>(*none, dummy, nullptr, true);
+    if (variant == V) return launch2d_t<BX, BY, W, NT, NS>(none, dummy, nullptr, true);
     JAC_TMA_VARIANTS(X)
 #undef X
     return cudaErrorInvalidValue;
