@@ -209,9 +209,10 @@ int jac_block_owner(const jac_ctx *c, int32_t ix, int32_t iy, int32_t iz, int32_
 /* Device time of the last jac_step (CUDA events recorded on the launching
  * stream(s) around its launches; max over this context's devices), in ms. */
 int jac_last_step_ms(const jac_ctx *c, double *ms);
-/* Runs n_iters sweeps launched one by one without a graph, with CUDA events
- * around every sweep-kernel launch; returns the average sweep-kernel duration in
- * ms (for the roofline's per-launch figure).  Advances the state like jac_step. */
+/* Runs n_iters iterations as one captured graph with CUDA event-record nodes around
+ * every sweep-kernel launch (same stream, same kernels as jac_step); returns the
+ * median sweep-kernel duration in ms (the roofline's per-launch figure).  Advances
+ * the state like jac_step. */
 int jac_profile_sweep(jac_ctx *c, int32_t n_iters, double *avg_sweep_ms);
 
 enum jac_stat {

@@ -1096,15 +1096,14 @@ int jac_profile_sweep(jac_ctx *c, int32_t n, double *avg_ms)
     if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
     cudaGraphExecDestroy(exec);
     if (e != cudaSuccess) return fail(JAC_ECUDA, "profile graph: %s", cudaGetErrorString(e));
-    double tot = 0;
-    for (int it = 0; it < n; ++it) {
-        float ms = 0;
-        CK(cudaEventElapsedTime(&ms, ev[2 * it], ev[2 * it + 1]));
-        tot += ms;
-    }
+    std::vector<float> dur(n);
+    for (int it = 0; it < n; ++it) CK(cudaEventElapsedTime(&dur[it], ev[2 * it], ev[2 * it + 1]));
     c->iters += n;
     c->kernel_launches += (int64_t)n * c->kernels_per_iter();
-    *avg_ms = tot / n;
+    // median: robust to the first launches of a multi-rank run, whose remote items may
+    // wait for a neighbour rank that started its profiling graph a little later
+    std::sort(dur.begin(), dur.end());
+    *avg_ms = (n & 1) ? dur[n / 2] : 0.5 * ((double)dur[n / 2 - 1] + dur[n / 2]);
     return JAC_OK;
 }
 
