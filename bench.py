@@ -134,6 +134,7 @@ class ClockSampler:
     def __init__(self, cuda_index):
         self.ok = False
         self.samples, self.reasons = [], 0
+        self.mem_samples, self.temps, self.power = [], [], []
         try:
             import pynvml as N
             N.nvmlInit()
@@ -150,6 +151,9 @@ class ClockSampler:
         while not self._stop.is_set():
             try:
                 self.samples.append(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM))
+                self.mem_samples.append(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_MEM))
+                self.temps.append(N.nvmlDeviceGetTemperature(h, 0))
+                self.power.append(N.nvmlDeviceGetPowerUsage(h) / 1000.0)
                 try:
                     r = N.nvmlDeviceGetCurrentClocksEventReasons(h)
                 except AttributeError:
@@ -176,6 +180,9 @@ class ClockSampler:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "error": getattr(self, "err", "")}
         return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
                 "sm_max_mhz": self.max_mhz, "samples": len(self.samples),
+                "mem_mhz": statistics.median(self.mem_samples) if self.mem_samples else None,
+                "gpu_temp_c_max": max(self.temps) if self.temps else None,
+                "power_w_max": max(self.power) if self.power else None,
                 "reasons": [n for b, n in self.REASONS.items() if self.reasons & b]}
 
 
