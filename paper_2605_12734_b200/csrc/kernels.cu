@@ -366,10 +366,10 @@ __global__ void __launch_bounds__(NT, min_ctas_per_sm(NT, NS))
     const bool ilo = (i == 0);                     // element 0 is the first interior point
     const bool ihi0 = (i == g.ex - 1);             // element 0 is the last interior point
     const bool ihi1 = (i + 1 == g.ex - 1);         // element 1 is the last interior point
-    double *own_plane = a.arena + (int64_t)(dst * g.nslots + blk.slot) * g.bstride + (int64_t)t.zs * g.Q;
-    int64_t rowoff[RY];
-#pragma unroll
-    for (int r = 0; r < RY; ++r) rowoff[r] = (int64_t)(t.y0 + rg * RY + r + 1) * g.P + g.A + i;
+    const int jl0 = rg * RY;                       // tile row of this thread's row 0
+    const int sb = (jl0 + 1) * W + col;            // stage index of (row 0, element 0)
+    const int xg = L::XG_OFF + jl0;                // stage index of row 0's x- ghost (+BY: x+)
+    double *const own = a.arena + (int64_t)(dst * g.nslots + blk.slot) * g.bstride;
     auto plane = [&](int q) { return stage + (q % NS) * L::STRIDE; };
     auto wait = [&](int q) { mbar_wait(&bars[q % NS], (q / NS) & 1); };
     // every thread is done with plane q -> the producer refills its stage with q + NS.
@@ -383,44 +383,139 @@ __global__ void __launch_bounds__(NT, min_ctas_per_sm(NT, NS))
     double2 zm[RY], c[RY], zp[RY];
     wait(0);
 #pragma unroll
-    for (int r = 0; r < RY; ++r)
-        zm[r] = *reinterpret_cast<const double2 *>(plane(0) + (rg * RY + r + 1) * W + col);
+    for (int r = 0; r < RY; ++r) zm[r] = *reinterpret_cast<const double2 *>(plane(0) + sb + r * W);
     refill(0);  // plane zs-1 only feeds zm
     wait(1);
 #pragma unroll
-    for (int r = 0; r < RY; ++r)
-        c[r] = *reinterpret_cast<const double2 *>(plane(1) + (rg * RY + r + 1) * W + col);
+    for (int r = 0; r < RY; ++r) c[r] = *reinterpret_cast<const double2 *>(plane(1) + sb + r * W);
 
-    // (Instantiating the loop separately for x-edge and interior tiles was measured
-    // slower than this single version: the per-lane selects are predicated loads.)
-    for (int q = 1; q <= nq - 2; ++q) {
-        const int k = t.zs - 1 + q;
+    // One z-plane of the march: wait for plane q+1, update centre plane q (k), store.
+    auto update = [&](int q, double2 (&v)[RY], bool full) {
         wait(q + 1);
         const double *Sn = plane(q + 1);
 #pragma unroll
-        for (int r = 0; r < RY; ++r)
-            zp[r] = *reinterpret_cast<const double2 *>(Sn + (rg * RY + r + 1) * W + col);
+        for (int r = 0; r < RY; ++r) zp[r] = *reinterpret_cast<const double2 *>(Sn + sb + r * W);
         const double *S = plane(q);
 #pragma unroll
         for (int r = 0; r < RY; ++r) {
-            const int jl = rg * RY + r;
-            const double *row = S + (jl + 1) * W + col;
-            const double xm = ilo ? S[L::XG_OFF + jl] : row[-1];
-            const double xp1 = ihi1 ? S[L::XG_OFF + BY + jl] : row[2];
-            const double xp0 = ihi0 ? S[L::XG_OFF + BY + jl] : c[r].y;
-            const double2 ym = (r == 0) ? *reinterpret_cast<const double2 *>(row - W) : c[r - 1];
-            const double2 yp = (r == RY - 1) ? *reinterpret_cast<const double2 *>(row + W) : c[r + 1];
-            double2 v;
-            v.x = stencil7(c[r].x, xm, xp0, ym.x, yp.x, zm[r].x, zp[r].x);
-            v.y = stencil7(c[r].y, c[r].x, xp1, ym.y, yp.y, zm[r].y, zp[r].y);
-            const int j = t.y0 + jl;
-            if (j < g.ey) emit_pair(a, blk, dst, own_plane + g.Q, rowoff[r], i, j, k, v);
+            const double xm = ilo ? S[xg + r] : S[sb + r * W - 1];
+            const double xp1 = ihi1 ? S[xg + BY + r] : S[sb + r * W + 2];
+            const double xp0 = (!full && ihi0) ? S[xg + BY + r] : c[r].y;  // full tiles: never
+            const double2 ym = (r == 0) ? *reinterpret_cast<const double2 *>(S + sb - W) : c[r - 1];
+            const double2 yp = (r == RY - 1) ? *reinterpret_cast<const double2 *>(S + sb + RY * W) : c[r + 1];
+            v[r].x = stencil7(c[r].x, xm, xp0, ym.x, yp.x, zm[r].x, zp[r].x);
+            v[r].y = stencil7(c[r].y, c[r].x, xp1, ym.y, yp.y, zm[r].y, zp[r].y);
         }
-        own_plane += g.Q;
+    };
+    auto advance = [&](int q) {
         refill(q);  // centre plane k is done
 #pragma unroll
         for (int r = 0; r < RY; ++r) { zm[r] = c[r]; c[r] = zp[r]; }
+    };
+    // General plane: every store through emit_pair (ragged edges, y faces, z faces,
+    // every exchange mode).
+    auto plane_general = [&](int q) {
+        const int k = t.zs - 1 + q;
+        double2 v[RY];
+        update(q, v, false);
+        double *const own_k = own + (int64_t)(k + 1) * g.Q;
+#pragma unroll
+        for (int r = 0; r < RY; ++r) {
+            const int j = t.y0 + jl0 + r;
+            if (j < g.ey) emit_pair(a, blk, dst, own_k, (int64_t)(j + 1) * g.P + g.A + i, i, j, k, v[r]);
+        }
+        advance(q);
+    };
+
+    // Lean planes (the z-march is issue-bound once the power cap lowers the clock, so
+    // instructions per point count): a CTA-uniform choice for full tiles -- every lane
+    // holds two interior points, every row is interior -- with no y-face row, away
+    // from the block's first and last plane.  They store the pair with one 16-byte
+    // store and, on x-face lanes, the boundary value into the neighbour's x-ghost array
+    // (or outbox), element (j, k) at xf + k*xs + j.  XE = the tile has x-edge lanes
+    // (x-ghost reads, x-face stores); x-interior tiles address every operand as one
+    // per-plane base + immediate.  The loop is unrolled by 3 with rotated register
+    // names (no moves), and the ring slot / parity advance incrementally.
+    const bool exch = (a.mode != MODE_NOEXCHANGE);
+    auto has = [&](int f) { return (a.mode == MODE_FUSED ? blk.nb[f][dst] : blk.nb[f][0]) != nullptr; };
+    const bool lean = (t.x0 + BX <= g.ex) && (t.y0 + BY <= g.ey) && g.ex > 2 &&
+                      !(exch && ((t.y0 == 0 && has(YM)) || (t.y0 + BY == g.ey && has(YP))));
+    int q = 1;
+    const int qlast = nq - 2;
+    if (exch && t.zs == 0) plane_general(q++);  // z- face plane
+    const int qlean_end = (exch && t.ze == g.ez) ? qlast - 1 : qlast;
+    if (lean && q <= qlean_end) {
+        const bool xedge = (t.x0 == 0) || (t.x0 + BX >= g.ex);
+        double *xf = nullptr;  // x-face target of this lane (row 0 of the thread, plane q)
+        int64_t xs = 0;
+        if (exch && (ilo || ihi1)) {
+            const int f = ilo ? XM : XP;
+            if (a.mode == MODE_FUSED) {
+                xf = blk.nb[f][dst];
+                xs = g.eyp;
+            } else if (blk.nb[f][0]) {
+                xf = a.outbox + (int64_t)blk.slot * g.ostride + g.ooff[f];
+                xs = g.ey;
+            }
+            if (xf) xf += t.y0 + jl0 + (int64_t)(t.zs - 1 + q) * xs;
+        }
+        double *op = own + (int64_t)(t.zs + q) * g.Q + (int64_t)(t.y0 + jl0 + 1) * g.P + g.A + i;
+        const int64_t P = g.P, Qs = g.Q;
+        int sn = (q + 1) % NS;               // ring slot of plane q+1
+        uint32_t pn = ((q + 1) / NS) & 1u;   // its mbarrier parity
+        const double *Sc = plane(q);
+        auto step = [&](const bool XE, const double2 (&A)[RY], const double2 (&B)[RY], double2 (&C)[RY]) {
+            mbar_wait(&bars[sn], pn);
+            const double *Sn = stage + sn * L::STRIDE;
+            const double *Sb = Sc + sb;
+#pragma unroll
+            for (int r = 0; r < RY; ++r) C[r] = *reinterpret_cast<const double2 *>(Sn + sb + r * W);
+#pragma unroll
+            for (int r = 0; r < RY; ++r) {
+                double xm = Sb[r * W - 1], xp1 = Sb[r * W + 2];
+                if (XE) {
+                    if (ilo) xm = Sc[xg + r];
+                    if (ihi1) xp1 = Sc[xg + BY + r];
+                }
+                const double2 ym = (r == 0) ? *reinterpret_cast<const double2 *>(Sb - W) : B[r - 1];
+                const double2 yp = (r == RY - 1) ? *reinterpret_cast<const double2 *>(Sb + RY * W) : B[r + 1];
+                double2 v;
+                v.x = stencil7(B[r].x, xm, B[r].y, ym.x, yp.x, A[r].x, C[r].x);
+                v.y = stencil7(B[r].y, B[r].x, xp1, ym.y, yp.y, A[r].y, C[r].y);
+                *reinterpret_cast<double2 *>(op + r * P) = v;
+                if (XE && xf) xf[r] = ilo ? v.x : v.y;
+            }
+            op += Qs;
+            if (XE && xf) xf += xs;
+            refill(q);  // centre plane done
+            ++q;
+            Sc = Sn;
+            if (++sn == NS) { sn = 0; pn ^= 1u; }
+        };
+        auto run = [&](const bool xe) {
+            while (q + 2 <= qlean_end) {
+                step(xe, zm, c, zp);
+                step(xe, c, zp, zm);
+                step(xe, zp, zm, c);
+            }
+            if (q <= qlean_end) {  // 1 or 2 more planes; restore the canonical names
+                step(xe, zm, c, zp);
+                if (q <= qlean_end) {
+                    step(xe, c, zp, zm);
+#pragma unroll
+                    for (int r = 0; r < RY; ++r) { const double2 t0 = zm[r]; zm[r] = zp[r]; zp[r] = c[r]; c[r] = t0; }
+                } else {
+#pragma unroll
+                    for (int r = 0; r < RY; ++r) { const double2 t0 = zm[r]; zm[r] = c[r]; c[r] = zp[r]; zp[r] = t0; }
+                }
+            }
+        };
+        if (xedge) run(true);
+        else run(false);
+    } else {
+        for (; q <= qlean_end; ++q) plane_general(q);
     }
+    if (q <= qlast) plane_general(q);  // z+ face plane
     if (remote) signal_done(a);
 }
 
