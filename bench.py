@@ -319,9 +319,23 @@ def run_reference(args, D):
 
 
 # ------------------------------------------------------------------ our arm
-def time_ctx(J, K, W, D, sampler=None):
+COOL_S = 0.25  # idle before each measured leg: >= 100 ms restores the uncapped clock
+
+
+def cool(D):
+    """Let the board's power controller recover from the previous leg, so every leg
+    starts in the same state (a capped GPU needs ~100 ms idle, tools/recover_probe.py)."""
+    import torch
+    torch.cuda.synchronize()
+    D.barrier()
+    time.sleep(COOL_S)
+
+
+def time_ctx(J, K, W, D, sampler=None, cool_first=True):
     """W warm-up steps, then exactly K timed steps.  Returns device ms (max over ranks)."""
     import torch
+    if cool_first:
+        cool(D)
     J.step(W)
     st0 = J.stats()["kernel_launches"]
     D.barrier()
@@ -381,6 +395,7 @@ def run_ours(args, D):
     ms_iter = dev_ms / K
     st = J.stats()
     # per-launch sweep duration (CUDA events around each sweep launch, same stream)
+    cool(D)
     sweep_ms = D.max(J.profile_sweep(min(max(K, 10), 50)))
     achieved = BYTES_PER_LUP * pts_gpu / (sweep_ms * 1e-3) / 1e9
     traffic = ncu_traffic(label)
@@ -395,7 +410,7 @@ def run_ours(args, D):
         settle = int(min(20000, max(50, 1500.0 / ms_iter)))
         ks = int(min(5000, max(20, 300.0 / ms_iter)))
         s_sampler = ClockSampler(D.local)
-        ms_s, _ = time_ctx(J, ks, settle, D, s_sampler)
+        ms_s, _ = time_ctx(J, ks, settle, D, s_sampler, cool_first=False)
         sustained = {"value": pts * ks / (ms_s * 1e-3) / 1e9, "unit": "GLUP/s", "ms_per_step": ms_s / ks,
                      "settle_iters": settle, "timed_iters": ks,
                      "hbm_frac_step": BYTES_PER_LUP * pts_gpu / (ms_s / ks * 1e-3) / 1e9 / peak,
@@ -463,6 +478,7 @@ def finish_ours(args, D, K, W, dims, blocks, g, label, scaling, pts, pts_gpu, pe
                 Jo = make_ctx(d2, b2, g2, D)
                 Jo.set_init_hash(1)
                 ms, _ = time_ctx(Jo, K, W, D)
+                cool(D)
                 sw = Jo.profile_sweep(20)
                 runs.append((ms, sw))
                 close_ctx(Jo, D)
@@ -524,7 +540,9 @@ def finish_ours(args, D, K, W, dims, blocks, g, label, scaling, pts, pts_gpu, pe
             "config": {"workload": label, "global_dims": dims, "blocks": blocks, "gpu_grid": g,
                        "odf": blocks[0] * blocks[1] * blocks[2] // args.gpus, "step": "one Jacobi iteration",
                        "l2": "inputs larger than L2 (2 ghosted fp64 arrays, >= 2.1 GB per GPU); no flush",
-                       "timing": "CUDA events on the launching stream around K graph-replayed iterations, max over ranks"},
+                       "timing": "CUDA events on the launching stream around K graph-replayed iterations, max over ranks",
+                       "power_state": f"each measured leg starts after {COOL_S} s idle (uncapped clock); "
+                                      "sustained_power_capped = the same context after ~1.5 s at the 1000 W cap"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "kernel": "sweep2d_tma_kernel" if MODE_2D[0] else "sweep_tma_kernel",

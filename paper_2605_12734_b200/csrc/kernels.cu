@@ -592,25 +592,65 @@ __global__ void __launch_bounds__(NT, 4) sweep2d_tma_kernel(const __grid_constan
     const int dst = 1 - a.src;
     const bool ilo = (i == 0), ihi0 = (i == g.ex - 1), ihi1 = (i + 1 == g.ex - 1);
     double *own = a.arena + (int64_t)(dst * g.nslots + blk.slot) * g.bstride;  // plane k = 0 (zg = 0)
+    // Lean y tiles (as in the 3-D sweep): full in x and y, no y-face row -> one 16-byte
+    // store per pair (+ the x-face value on x-edge lanes), rows shared between a
+    // thread's RY rows instead of reloaded.  Other tiles take emit_pair.
+    const bool exch = (a.mode != MODE_NOEXCHANGE);
+    auto has = [&](int f) { return (a.mode == MODE_FUSED ? blk.nb[f][dst] : blk.nb[f][0]) != nullptr; };
+    const bool xfull = (x0 + BX <= g.ex) && g.ex > 2;
+    const bool xedge = xlo || xhi;
+    const int jl0 = rg * RY;
+    const int sb = (jl0 + 1) * W + col;
+    const int xg = L::XG_OFF + jl0;
+    double *xf = nullptr;  // x-face target, element j at xf + j (plane k = 0)
+    if (xfull && exch && (ilo || ihi1)) {
+        const int f = ilo ? XM : XP;
+        if (a.mode == MODE_FUSED) xf = blk.nb[f][dst];
+        else if (blk.nb[f][0]) xf = a.outbox + (int64_t)blk.slot * g.ostride + g.ooff[f];
+    }
     for (int q = 0; q < nq; ++q) {
         mbar_wait(&bars[q % NS], (q / NS) & 1);
         const double *S = stage + (q % NS) * L::STRIDE;
         const int y0 = (ty0 + q) * BY;
+        const bool lean = xfull && (y0 + BY <= g.ey) &&
+                          !(exch && ((y0 == 0 && has(YM)) || (y0 + BY == g.ey && has(YP))));
+        if (lean) {
+            const double *Sb = S + sb;
+            double2 rw[RY + 2];  // rows jl0-1 .. jl0+RY
 #pragma unroll
-        for (int r = 0; r < RY; ++r) {
-            const int jl = rg * RY + r;
-            const double *row = S + (jl + 1) * W + col;
-            const double2 c = *reinterpret_cast<const double2 *>(row);
-            const double xm = ilo ? S[L::XG_OFF + jl] : row[-1];
-            const double xp1 = ihi1 ? S[L::XG_OFF + BY + jl] : row[2];
-            const double xp0 = ihi0 ? S[L::XG_OFF + BY + jl] : c.y;
-            const double2 ym = *reinterpret_cast<const double2 *>(row - W);
-            const double2 yp = *reinterpret_cast<const double2 *>(row + W);
-            double2 v;
-            v.x = stencil5(c.x, xm, xp0, ym.x, yp.x);
-            v.y = stencil5(c.y, c.x, xp1, ym.y, yp.y);
-            const int j = y0 + jl;
-            if (j < g.ey) emit_pair<false>(a, blk, dst, own, (int64_t)(j + 1) * g.P + g.A + i, i, j, 0, v);
+            for (int r = 0; r < RY + 2; ++r) rw[r] = *reinterpret_cast<const double2 *>(Sb + (r - 1) * W);
+            double *op = own + (int64_t)(y0 + jl0 + 1) * g.P + g.A + i;
+#pragma unroll
+            for (int r = 0; r < RY; ++r) {
+                double xm = Sb[r * W - 1], xp1 = Sb[r * W + 2];
+                if (xedge) {
+                    if (ilo) xm = S[xg + r];
+                    if (ihi1) xp1 = S[xg + BY + r];
+                }
+                const double2 c = rw[r + 1];
+                double2 v;
+                v.x = stencil5(c.x, xm, c.y, rw[r].x, rw[r + 2].x);
+                v.y = stencil5(c.y, c.x, xp1, rw[r].y, rw[r + 2].y);
+                *reinterpret_cast<double2 *>(op + r * g.P) = v;
+                if (xedge && xf) xf[y0 + jl0 + r] = ilo ? v.x : v.y;
+            }
+        } else {
+#pragma unroll
+            for (int r = 0; r < RY; ++r) {
+                const int jl = rg * RY + r;
+                const double *row = S + (jl + 1) * W + col;
+                const double2 c = *reinterpret_cast<const double2 *>(row);
+                const double xm = ilo ? S[L::XG_OFF + jl] : row[-1];
+                const double xp1 = ihi1 ? S[L::XG_OFF + BY + jl] : row[2];
+                const double xp0 = ihi0 ? S[L::XG_OFF + BY + jl] : c.y;
+                const double2 ym = *reinterpret_cast<const double2 *>(row - W);
+                const double2 yp = *reinterpret_cast<const double2 *>(row + W);
+                double2 v;
+                v.x = stencil5(c.x, xm, xp0, ym.x, yp.x);
+                v.y = stencil5(c.y, c.x, xp1, ym.y, yp.y);
+                const int j = y0 + jl;
+                if (j < g.ey) emit_pair<false>(a, blk, dst, own, (int64_t)(j + 1) * g.P + g.A + i, i, j, 0, v);
+            }
         }
         __syncthreads();
         if (threadIdx.x == 0 && q + NS < nq) issue(q + NS);
