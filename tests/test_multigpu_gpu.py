@@ -31,6 +31,12 @@ CASES = [
     (2, (64, 48, 80), (2, 2, 4), None, 21, 1 << 2, False),     # NCCL transport ablation
     (4, (64, 64, 64), (4, 2, 2), (2, 2, 1), 7, 1 << 2, False), # NCCL, x-split (x-ghost layout)
     (2, (256, 192, 1), (2, 4, 1), None, 5, (1 << 2) | (1 << 9), False),  # NCCL + Jacobi2D
+    # 128-wide blocks split in x: lean-path tiles (full, no y-face rows) whose x-edge
+    # lanes store remote x faces through IPC pointers / into NCCL send buffers
+    (2, (256, 64, 48), (2, 1, 1), (2, 1, 1), 9, 0, True),
+    (2, (256, 64, 48), (2, 1, 1), (2, 1, 1), 9, 1 << 2, True),
+    (4, (256, 128, 48), (2, 2, 1), (2, 2, 1), 7, 0, True),
+    (2, (512, 96, 1), (2, 1, 1), (2, 1, 1), 9, 1 << 9, True),   # Jacobi2D lean tiles, x split
 ]
 
 
