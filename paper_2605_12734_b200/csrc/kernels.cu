@@ -429,23 +429,22 @@ __global__ void __launch_bounds__(NT, min_ctas_per_sm(NT, NS))
 
     // Lean planes (the z-march is issue-bound once the power cap lowers the clock, so
     // instructions per point count): a CTA-uniform choice for full tiles -- every lane
-    // holds two interior points, every row is interior -- with no y-face row, away
-    // from the block's first and last plane.  They store the pair with one 16-byte
-    // store and, on x-face lanes, the boundary value into the neighbour's x-ghost array
-    // (or outbox), element (j, k) at xf + k*xs + j.  XE = the tile has x-edge lanes
-    // (x-ghost reads, x-face stores); x-interior tiles address every operand as one
+    // holds two interior points, every row is interior -- away from the block's
+    // first and last plane.  They store the pair with one 16-byte
+    // store, x-face lanes the boundary value into the neighbour's x-ghost array (or
+    // outbox), element (j, k) at xf + k*xs + j, and y-face rows the pair into the
+    // neighbour's ghost row (or send buffer / outbox) at yf + k*ys.  XE = edge tile
+    // (x-ghost reads, face stores); interior tiles address every operand as one
     // per-plane base + immediate.  The loop is unrolled by 3 with rotated register
     // names (no moves), and the ring slot / parity advance incrementally.
     const bool exch = (a.mode != MODE_NOEXCHANGE);
-    auto has = [&](int f) { return (a.mode == MODE_FUSED ? blk.nb[f][dst] : blk.nb[f][0]) != nullptr; };
-    const bool lean = (t.x0 + BX <= g.ex) && (t.y0 + BY <= g.ey) && g.ex > 2 &&
-                      !(exch && ((t.y0 == 0 && has(YM)) || (t.y0 + BY == g.ey && has(YP))));
+    const bool lean = (t.x0 + BX <= g.ex) && (t.y0 + BY <= g.ey) && g.ex > 2;
     int q = 1;
     const int qlast = nq - 2;
     if (exch && t.zs == 0) plane_general(q++);  // z- face plane
     const int qlean_end = (exch && t.ze == g.ez) ? qlast - 1 : qlast;
     if (lean && q <= qlean_end) {
-        const bool xedge = (t.x0 == 0) || (t.x0 + BX >= g.ex);
+        const bool edge = (t.x0 == 0) || (t.x0 + BX >= g.ex) || (t.y0 == 0) || (t.y0 + BY >= g.ey);
         double *xf = nullptr;  // x-face target of this lane (row 0 of the thread, plane q)
         int64_t xs = 0;
         if (exch && (ilo || ihi1)) {
@@ -458,6 +457,32 @@ __global__ void __launch_bounds__(NT, min_ctas_per_sm(NT, NS))
                 xs = g.ey;
             }
             if (xf) xf += t.y0 + jl0 + (int64_t)(t.zs - 1 + q) * xs;
+        }
+        // y-face target of this thread (row 0 if yf_lo, else row RY-1; a full tile has
+        // ey >= BY, so no thread holds both): the neighbour's ghost row (plane stride
+        // Q), or a packed send buffer / outbox row [k][ex] (stride ex).
+        double *yf = nullptr;
+        int64_t ys = 0;
+        bool yf_lo = false;
+        if (exch) {
+            int f = -1;
+            if (t.y0 + jl0 == 0) { f = YM; yf_lo = true; }
+            else if (t.y0 + jl0 + RY - 1 == g.ey - 1) f = YP;
+            if (f >= 0) {
+                if (a.mode == MODE_FUSED) {
+                    if (double *p = blk.nb[f][dst]) {
+                        if (blk.pack_mask & (1u << f)) { yf = p + i; ys = g.ex; }
+                        else {
+                            yf = p + (int64_t)g.zg * g.Q + (f == YM ? (int64_t)(g.ey + 1) * g.P : 0) + g.A + i;
+                            ys = g.Q;
+                        }
+                    }
+                } else if (blk.nb[f][0]) {
+                    yf = a.outbox + (int64_t)blk.slot * g.ostride + g.ooff[f] + i;
+                    ys = g.ex;
+                }
+                if (yf) yf += (int64_t)(t.zs - 1 + q) * ys;
+            }
         }
         double *op = own + (int64_t)(t.zs + q) * g.Q + (int64_t)(t.y0 + jl0 + 1) * g.P + g.A + i;
         const int64_t P = g.P, Qs = g.Q;
@@ -484,9 +509,11 @@ __global__ void __launch_bounds__(NT, min_ctas_per_sm(NT, NS))
                 v.y = stencil7(B[r].y, B[r].x, xp1, ym.y, yp.y, A[r].y, C[r].y);
                 *reinterpret_cast<double2 *>(op + r * P) = v;
                 if (XE && xf) xf[r] = ilo ? v.x : v.y;
+                if (XE && yf && ((r == 0 && yf_lo) || (r == RY - 1 && !yf_lo))) { yf[0] = v.x; yf[1] = v.y; }
             }
             op += Qs;
             if (XE && xf) xf += xs;
+            if (XE && yf) yf += ys;
             refill(q);  // centre plane done
             ++q;
             Sc = Sn;
@@ -510,7 +537,7 @@ __global__ void __launch_bounds__(NT, min_ctas_per_sm(NT, NS))
                 }
             }
         };
-        if (xedge) run(true);
+        if (edge) run(true);
         else run(false);
     } else {
         for (; q <= qlean_end; ++q) plane_general(q);

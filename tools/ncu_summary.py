@@ -7,7 +7,8 @@ KEYS = {"gpu__time_duration.sum": "time", "dram__bytes_read.sum": "dram_read", "
         "launch__registers_per_thread": "regs", "launch__grid_size": "grid", "launch__occupancy_limit_registers": "occ_lim_regs",
         "launch__occupancy_limit_shared_mem": "occ_lim_smem", "sm__cycles_elapsed.avg.per_second": "sm_clock",
         "lts__t_sectors_srcunit_tex_op_read.sum": "l2_read_sectors", "lts__t_sectors_srcunit_tex_op_write.sum": "l2_write_sectors",
-        "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed": "dram_pct_peak"}
+        "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed": "dram_pct_peak",
+        "smsp__inst_executed.sum": "warp_instructions", "smsp__issue_active.avg.pct_of_peak_sustained_active": "issue_active_pct"}
 SCALE = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1, "us": 1e-6, "ms": 1e-3, "ns": 1e-9, "Ghz": 1e9, "Mhz": 1e6}
 
 
