@@ -322,9 +322,15 @@ int encode_tmap(jac_ctx *c)
     const cuuint64_t strides[3] = {(cuuint64_t)g.P * 8, (cuuint64_t)g.Q * 8, (cuuint64_t)g.bstride * 8};
     const cuuint32_t box[4] = {(cuuint32_t)ts.w, (cuuint32_t)(ts.by + 2), 1, 1};
     const cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+    if (const char *s = getenv("JAC_L2PROMO")) {  // experiment knob: 0, 64, 128, 256
+        const int v = atoi(s);
+        promo = v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE : v == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+              : v == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+    }
     CUresult r = encode(&c->tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, c->arena, dims, strides, box, estr,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, promo,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(JAC_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
     return JAC_OK;
 }

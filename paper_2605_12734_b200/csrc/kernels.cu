@@ -444,7 +444,10 @@ __global__ void __launch_bounds__(NT, min_ctas_per_sm(NT, NS))
     if (exch && t.zs == 0) plane_general(q++);  // z- face plane
     const int qlean_end = (exch && t.ze == g.ez) ? qlast - 1 : qlast;
     if (lean && q <= qlean_end) {
-        const bool edge = (t.x0 == 0) || (t.x0 + BX >= g.ex) || (t.y0 == 0) || (t.y0 + BY >= g.ey);
+        // edge instantiation: x-ghost lanes, or a y-face row with a target
+        auto has = [&](int f) { return (a.mode == MODE_FUSED ? blk.nb[f][dst] : blk.nb[f][0]) != nullptr; };
+        const bool edge = (t.x0 == 0) || (t.x0 + BX >= g.ex) ||
+                          (exch && ((t.y0 == 0 && has(YM)) || (t.y0 + BY >= g.ey && has(YP))));
         double *xf = nullptr;  // x-face target of this lane (row 0 of the thread, plane q)
         int64_t xs = 0;
         if (exch && (ilo || ihi1)) {

@@ -1,2 +1,19 @@
-timeout 300 python -m pytest tests/test_microbench_gpu.py -q > gpurun_out/pytest_mb.log 2>&1; echo pytest=$? >> gpurun_out/pytest_mb.log
-timeout 900 python tools/microbench.py > gpurun_out/microbench_r01.json 2> gpurun_out/microbench.err
+mkdir -p gpurun_out/final
+F=gpurun_out/final
+python bench.py > $F/bench_c2_n1.json 2> $F/bench_c2_n1.err
+python bench.py --config j2d --no-cpu > $F/bench_j2d_n1.json 2> $F/bench_j2d_n1.err
+python bench.py --impl reference --steps 3 --warmup 3 > $F/bench_ref_n1.json 2> $F/bench_ref_n1.err
+python bench.py --config c3 --no-sweep --no-cpu > $F/bench_c3_n1.json 2> $F/bench_c3_n1.err
+python bench.py --config c4 --odf 1 --no-sweep --no-cpu --no-e2e > $F/bench_c4odf1_n1.json 2> $F/bench_c4odf1_n1.err
+python bench.py --config c4 --odf 16 --no-sweep --no-cpu --no-e2e > $F/bench_c4odf16_n1.json 2> $F/bench_c4odf16_n1.err
+python bench.py --config c5 --no-sweep --no-cpu --no-e2e > $F/bench_c5_n1.json 2> $F/bench_c5_n1.err
+python bench.py --no-sweep --no-cpu --no-e2e --no-sustained --steps 20 --warmup 3 > $F/pre_ncu.log 2>&1 && \
+ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $F/launches_c2.csv python bench.py --no-sweep --no-cpu --no-e2e --no-sustained --steps 20 --warmup 3 > $F/ncu_launch.log 2>&1
+for b in "1 1 1" "2 2 2" "2 2 4" "4 4 4" "16 16 16"; do
+  tag=$(echo $b | tr -d ' ')
+  python tools/profile_sweep.py --blocks $b --iters 3 >> $F/pre_full.log 2>&1 && \
+  ncu --set full --clock-control none --import-source on -k regex:sweep -c 1 -o $F/r01b_sweep_blocks$tag -f python tools/profile_sweep.py --blocks $b --iters 2 > /dev/null 2>&1
+done
+python tools/profile_sweep.py --dims 32768 32768 1 --blocks 2 4 1 --flags 512 --iters 3 >> $F/pre_full.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:sweep -c 1 -o $F/r01b_sweep2d_32768sq_odf8 -f python tools/profile_sweep.py --dims 32768 32768 1 --blocks 2 4 1 --flags 512 --iters 2 > /dev/null 2>&1
+ls $F >> $F/pre_full.log
