@@ -8,7 +8,8 @@
 //     base + (k+zg)*Q + (j+1)*P + A + i,     Q = P*(ey+2)
 // (zg = 1; the 2-D mode, JAC_F_2D, has a single plane k = 0 and zg = 0)
 // with A = 4 so the interior row starts on a 32-byte sector (and 16-byte aligned
-// double2 accesses).  All slots of one GPU sit in one arena: slot s of buffer b
+// double2 accesses); narrow blocks (ex <= 64) use A = 8 and a 64-byte row pitch so
+// rows start on 64-byte DRAM granules (engine.cu, geometry).  All slots of one GPU sit in one arena: slot s of buffer b
 // starts at arena + (b*nslots + s)*bstride, which lets ONE 4-D TMA tensor map
 // {P, ey+2, ez+2, 2*nslots} cover every block of the GPU.
 //
@@ -56,7 +57,7 @@ struct DevBlock {
 
 struct Geom {
     int32_t ex, ey, ez;      // block interior extents
-    int32_t A;               // = kA
+    int32_t A;               // kA, or 2*kA for narrow blocks
     int64_t P, Q;            // row / plane pitch in doubles
     int64_t bstride;         // doubles between consecutive slots (256-byte multiple)
     int32_t nslots;          // slots per buffer in the arena

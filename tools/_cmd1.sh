@@ -1,7 +1,8 @@
-F=gpurun_out/promo; mkdir -p $F
-ODFS=1,8,64,4096 SETTINGS="JAC_L2PROMO=256;JAC_L2PROMO=128;JAC_L2PROMO=64;JAC_L2PROMO=0;JAC_L2PROMO=256" K=2 timeout 600 python tools/steady_probe.py > $F/steady.log 2>&1
-for p in 256 64 0; do
-for b in "16 16 16" "4 4 4" "1 1 1"; do
-JAC_L2PROMO=$p python tools/profile_sweep.py --blocks $b --iters 3 >> $F/pre.log 2>&1 && \
-JAC_L2PROMO=$p ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none -k regex:sweep -c 1 python tools/profile_sweep.py --blocks $b --iters 2 2>&1 | grep -E "dram|duration" | sed "s/^/promo=$p blocks=$b /" >> $F/ncu.log
-done; done
+F=gpurun_out/narrow; mkdir -p $F
+timeout 900 python -m pytest tests/test_parity_gpu.py tests/test_parity2d_gpu.py tests/test_fullsize_gpu.py -m gpu -q 2>&1 | tail -2 > $F/parity.log
+for lib in new prev new prev; do
+  if [ $lib = prev ]; then export JAC_LIB=build/ab/lib_prev.so; else unset JAC_LIB; fi
+  for b in "16 16 16" "8 8 8" "4 4 4" "2 2 2"; do python tools/profile_sweep.py --blocks $b --iters 20 2>&1 | sed "s/^/$lib /"; done
+done > $F/time.log
+unset JAC_LIB
+python bench.py --config c5 --no-sweep --no-cpu --no-e2e > $F/bench_c5.json 2>&1

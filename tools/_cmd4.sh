@@ -1,21 +1,1 @@
-F=gpurun_out/final2; mkdir -p $F
-timeout 900 python -m pytest tests/test_parity_gpu.py tests/test_parity2d_gpu.py tests/test_fullsize_gpu.py -m gpu -q 2>&1 | tail -3 > $F/parity.log
-timeout 1200 python -m pytest tests/test_multigpu_gpu.py -m gpu -q 2>&1 | tail -3 >> $F/parity.log
-R="python -m torch.distributed.run --nnodes 1 --master-addr 127.0.0.1"
-for cfg in c2 c3 j2d; do
-  CUDA_VISIBLE_DEVICES=0 python bench.py --config $cfg --no-sweep --no-cpu > $F/bench_${cfg}_n1.json 2> $F/bench_${cfg}_n1.err
-  for n in 2 4; do $R --nproc-per-node $n --master-port $((29500 + RANDOM % 400)) bench.py --gpus $n --config $cfg > $F/bench_${cfg}_n$n.json 2> $F/bench_${cfg}_n$n.err; done
-done
-for o in 1 16; do
-  CUDA_VISIBLE_DEVICES=0 python bench.py --config c4 --odf $o --no-sweep --no-cpu --no-e2e > $F/bench_c4odf${o}_n1.json 2> $F/bench_c4odf${o}_n1.err
-  for n in 2 4; do $R --nproc-per-node $n --master-port $((29500 + RANDOM % 400)) bench.py --gpus $n --config c4 --odf $o --no-sweep --no-e2e > $F/bench_c4odf${o}_n$n.json 2> $F/bench_c4odf${o}_n$n.err; done
-done
-CUDA_VISIBLE_DEVICES=0 python bench.py --config c5 --no-sweep --no-cpu --no-e2e > $F/bench_c5_n1.json 2> $F/bench_c5_n1.err
-for n in 2 4; do $R --nproc-per-node $n --master-port $((29500 + RANDOM % 400)) bench.py --gpus $n --config c5 --no-sweep --no-e2e > $F/bench_c5_n$n.json 2> $F/bench_c5_n$n.err; done
-$R --nproc-per-node 4 --master-port $((29500 + RANDOM % 400)) bench.py --gpus 4 --impl reference --steps 3 --warmup 3 > $F/bench_ref_n4.json 2> $F/bench_ref_n4.err
-export CUDA_VISIBLE_DEVICES=0
-for b in "1 1 1" "2 2 2" "2 2 4" "4 4 4" "16 16 16"; do
-  tag=$(echo $b | tr -d ' ')
-  python tools/profile_sweep.py --blocks $b --iters 3 >> $F/pre_full.log 2>&1 && \
-  ncu --set full --clock-control none --import-source on -k regex:sweep -c 1 -o $F/r01b_sweep_blocks$tag -f python tools/profile_sweep.py --blocks $b --iters 2 > /dev/null 2>&1
-done
+timeout 1200 python -m pytest tests/test_multigpu_gpu.py -m gpu -q 2>&1 | tail -3 > gpurun_out/mp_tests.log
