@@ -380,7 +380,9 @@ void configure_tiles(jac_ctx *c)
         // 16 planes: measured best or within 2.5% of best on 512^3 (ODF 1-16), 768^3
         // and 1024^3 (64x16 tiles, 64x32 tiles were slower everywhere)
         int zchunk = 16;
-        if (g.ez <= 64) zchunk = g.ez;  // small blocks: one item marches the whole block depth
+        // small blocks: one item marches the whole block depth (32^3 blocks: 445 us
+        // vs 469 at 16 planes; 64^3 blocks keep 16: 404 vs 414 us whole-depth)
+        if (g.ez <= 32) zchunk = g.ez;
         // small grids (C1: 64^3): shorter chunks until the launch fills ~3/4 of a wave
         // (measured 24.5 -> 5.2 us per C1 iteration)
         while (zchunk > 2 && 4 * (int64_t)c->ncols * ((g.ez + zchunk - 1) / zchunk) < 3 * (int64_t)resident) zchunk /= 2;
@@ -511,8 +513,9 @@ int create_common(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, in
 
     // tile shape / variant
     if (flags & JAC_F_NO_TMA) c->variant = kPlain;
-    else c->variant = (g.ex <= 32) ? ((g.ey > 16 && c->nslots >= 64) ? jac::TMA_EXACT32_TALL : jac::TMA_EXACT32)
-                      : (g.ex <= 64) ? jac::TMA_EXACT64 : jac::TMA_WIDE;
+    // (32-wide blocks: 32 x 16 tiles; the 32 x 32 tile won only while y-face rows
+    // took the general epilogue -- lean y faces: 445 vs 462 us for 512^3 in 32^3 blocks)
+    else c->variant = (g.ex <= 32) ? jac::TMA_EXACT32 : (g.ex <= 64) ? jac::TMA_EXACT64 : jac::TMA_WIDE;
     if (const char *s = getenv("JAC_VARIANT"); s && c->variant != kPlain) {
         const int v = atoi(s);  // tuning knob; EXACT* only where one tile spans the block row
         if (v == jac::TMA_WIDE || v == jac::TMA_WIDE4 || v == jac::TMA_NARROW || 
