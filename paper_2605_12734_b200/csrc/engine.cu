@@ -403,18 +403,20 @@ void configure_tiles(jac_ctx *c)
 }
 
 // Create-time autotune of the wide tile's TMA ring depth (6 stages at 3 CTAs / SM vs
-// 4 stages at 4 CTAs / SM).  Measured on this pool: which one wins depends on the
-// box (512^3 ODF 1: 348 vs 355 us on one, 385 vs 355 us on another), so each context
-// times both on its own GPU -- 1 + 3 sweeps each, exchange off -- and keeps the
-// faster.  Results are bit-identical either way.  JAC_AUTOTUNE=0 or JAC_VARIANT skip.
+// 4 stages at 4 CTAs / SM) on the context's own decomposition and GPU: 1 + 8 sweeps
+// each, exchange off, the faster wins (ties within 0.5%: 6 stages in 3-D, 4 in 2-D).
+// Measured with the lean z-march: 3-D 512^3 ODF 1 and 8 within 0.6% either way (a
+// few boxes: 4 stages 2% faster), ODF 16 / 64 6 stages 1.5% / 3% faster; 2-D
+// 32768^2 4 stages 1.7% faster.  Results are bit-identical either way.
+// JAC_AUTOTUNE=0 (6 stages) or JAC_VARIANT skip it.
 int autotune(jac_ctx *c)
 {
     if (c->variant != jac::TMA_WIDE || getenv("JAC_VARIANT")) return JAC_OK;
     if (const char *s = getenv("JAC_AUTOTUNE"); s && atoi(s) == 0) return JAC_OK;
     const int cands[2] = {jac::TMA_WIDE, jac::TMA_WIDE4};
-    float best_ms = 1e30f;
-    int best = jac::TMA_WIDE;
-    for (int v : cands) {
+    float ms_of[2] = {0.f, 0.f};
+    for (int n = 0; n < 2; ++n) {
+        const int v = cands[n];
         c->variant = v;
         configure_tiles(c);
         if (jac::prepare_sweep_tma(v) != cudaSuccess || jac::prepare_sweep2d_tma(v) != cudaSuccess)
@@ -426,15 +428,16 @@ int autotune(jac_ctx *c)
         };
         CK(launch());
         CK(cudaEventRecord(c->ev0, c->stream));
-        for (int r = 0; r < 3; ++r) CK(launch());
+        for (int r = 0; r < 8; ++r) CK(launch());
         CK(cudaEventRecord(c->ev1, c->stream));
         CK(cudaStreamSynchronize(c->stream));
-        float ms = 0.f;
-        CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
-        c->tuned_ms[v == jac::TMA_WIDE ? 0 : 1] = ms / 3;
-        if (ms < best_ms) { best_ms = ms; best = v; }
+        CK(cudaEventElapsedTime(&ms_of[n], c->ev0, c->ev1));
+        c->tuned_ms[n] = ms_of[n] / 8;
     }
-    c->variant = best;
+    // ties (< 0.5%) go to the usual winner: 6 stages in 3-D, 4 stages in 2-D
+    const bool two_d = (c->flags & JAC_F_2D) != 0;
+    c->variant = (two_d ? (ms_of[0] < 0.995f * ms_of[1]) : !(ms_of[1] < 0.995f * ms_of[0])) ? jac::TMA_WIDE
+                                                                                             : jac::TMA_WIDE4;
     configure_tiles(c);
     return JAC_OK;
 }

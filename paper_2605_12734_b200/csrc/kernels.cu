@@ -629,6 +629,7 @@ __global__ void __launch_bounds__(NT, 4) sweep2d_tma_kernel(const __grid_constan
     auto has = [&](int f) { return (a.mode == MODE_FUSED ? blk.nb[f][dst] : blk.nb[f][0]) != nullptr; };
     const bool xfull = (x0 + BX <= g.ex) && g.ex > 2;
     const bool xedge = xlo || xhi;
+    const bool ym_face = exch && has(YM), yp_face = exch && has(YP);  // loop-invariant
     const int jl0 = rg * RY;
     const int sb = (jl0 + 1) * W + col;
     const int xg = L::XG_OFF + jl0;
@@ -642,8 +643,7 @@ __global__ void __launch_bounds__(NT, 4) sweep2d_tma_kernel(const __grid_constan
         mbar_wait(&bars[q % NS], (q / NS) & 1);
         const double *S = stage + (q % NS) * L::STRIDE;
         const int y0 = (ty0 + q) * BY;
-        const bool lean = xfull && (y0 + BY <= g.ey) &&
-                          !(exch && ((y0 == 0 && has(YM)) || (y0 + BY == g.ey && has(YP))));
+        const bool lean = xfull && (y0 + BY <= g.ey) && !((y0 == 0 && ym_face) || (y0 + BY == g.ey && yp_face));
         if (lean) {
             const double *Sb = S + sb;
             double2 rw[RY + 2];  // rows jl0-1 .. jl0+RY
