@@ -429,9 +429,20 @@ def run_ours(args, D):
         Jn = make_ctx(dims, blocks, g, D, flags=JB.JAC_F_NCCL)
         Jn.set_init_hash(1)
         ms_n, _ = time_ctx(Jn, K, W, D)
-        nccl_ablation = {"ms_per_iter": ms_n / K, "glups": pts * K / (ms_n * 1e-3) / 1e9,
-                         "vs_peer_stores": ms_n / K / ms_iter}
+        nccl_ablation = {"nccl_sendrecv": {"ms_per_iter": ms_n / K, "glups": pts * K / (ms_n * 1e-3) / 1e9,
+                                           "vs_peer_stores": ms_n / K / ms_iter}}
         close_ctx(Jn, D)
+        # exchange share: exposed exchange = t(default) - t(skip);
+        # no-overlap = faces packed by the sweep, pulled by a ghost-fill pass after a
+        # cross-rank barrier (JAC_F_UNFUSED_PACK)
+        for name, fl in (("skip_exchange_WRONG", JB.JAC_F_SKIP_EXCHANGE),
+                         ("unfused_pack_no_overlap", JB.JAC_F_UNFUSED_PACK)):
+            Ja = make_ctx(dims, blocks, g, D, flags=fl)
+            Ja.set_init_hash(1)
+            ms_a, _ = time_ctx(Ja, K, W, D)
+            nccl_ablation[name] = {"ms_per_iter": ms_a / K, "vs_default": ms_a / K / ms_iter}
+            close_ctx(Ja, D)
+        nccl_ablation["exposed_exchange_ms_per_iter"] = ms_iter - nccl_ablation["skip_exchange_WRONG"]["ms_per_iter"]
     return finish_ours(args, D, K, W, dims, blocks, g, label, scaling, pts, pts_gpu, peak, peak_src, value, ms_iter,
                        st, sweep_ms, achieved, traffic, e2e_val, h2d, d2h, launches, sampler, nccl_ablation,
                        sustained)
@@ -570,7 +581,7 @@ def finish_ours(args, D, K, W, dims, blocks, g, label, scaling, pts, pts_gpu, pe
         if paper_style is not None:
             line["paper_style_per_block"] = paper_style
         if nccl_ablation is not None:
-            line["ablation_nccl_sendrecv"] = nccl_ablation
+            line["exchange_ablations"] = nccl_ablation
         print(json.dumps(line), flush=True)
     D.finish()
 

@@ -28,8 +28,9 @@ def main():
         e = {k: d.get(k) for k in ("value", "unit", "ms_per_step", "n_gpus", "scaling", "config", "gpu_launches",
                                    "clocks", "exchange")}
         e["roofline_frac"] = (d.get("roofline") or {}).get("frac")
-        if d.get("ablation_nccl_sendrecv"):
-            e["ablation_nccl_sendrecv"] = d["ablation_nccl_sendrecv"]
+        for key in ("exchange_ablations", "ablation_nccl_sendrecv"):
+            if d.get(key):
+                e[key] = d[key]
         if base:
             sp = d["value"] / base["value"]
             e["speedup_vs_1gpu"] = sp
