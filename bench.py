@@ -435,8 +435,10 @@ def run_ours(args, D):
         # exchange share: exposed exchange = t(default) - t(skip);
         # no-overlap = faces packed by the sweep, pulled by a ghost-fill pass after a
         # cross-rank barrier (JAC_F_UNFUSED_PACK)
-        for name, fl in (("skip_exchange_WRONG", JB.JAC_F_SKIP_EXCHANGE),
-                         ("unfused_pack_no_overlap", JB.JAC_F_UNFUSED_PACK)):
+        abl = [("skip_exchange_WRONG", JB.JAC_F_SKIP_EXCHANGE)]
+        if not MODE_2D[0]:  # JAC_F_2D runs the fused TMA path only
+            abl.append(("unfused_pack_no_overlap", JB.JAC_F_UNFUSED_PACK))
+        for name, fl in abl:
             Ja = make_ctx(dims, blocks, g, D, flags=fl)
             Ja.set_init_hash(1)
             ms_a, _ = time_ctx(Ja, K, W, D)
