@@ -404,14 +404,21 @@ void configure_tiles(jac_ctx *c)
 
 // Create-time autotune of the wide tile's TMA ring depth (6 stages at 3 CTAs / SM vs
 // 4 stages at 4 CTAs / SM) on the context's own decomposition and GPU: 1 + 8 sweeps
-// each, exchange off, the faster wins (ties within 0.5%: 6 stages in 3-D, 4 in 2-D).
-// Measured with the lean z-march: 3-D 512^3 ODF 1 and 8 within 0.6% either way (a
-// few boxes: 4 stages 2% faster), ODF 16 / 64 6 stages 1.5% / 3% faster; 2-D
-// 32768^2 4 stages 1.7% faster.  Results are bit-identical either way.
-// JAC_AUTOTUNE=0 (6 stages) or JAC_VARIANT skip it.
+// each, exchange off, the faster wins (ties within 0.5%: 6 stages).  Measured with
+// the lean z-march: 3-D 512^3 ODF 1 and 8 within 0.6% either way (a few boxes: 4
+// stages 2% faster), ODF 16 / 64 6 stages 1.5% / 3% faster.  2-D takes 4 stages
+// without timing: 5% faster on every box and in both power regimes (2614 vs 2742 us
+// per 32768^2 sweep), while the create-time timing on the fresh arena sometimes
+// picked 6.  Results are bit-identical either way.  JAC_AUTOTUNE=0 (6 stages) or
+// JAC_VARIANT skip it.
 int autotune(jac_ctx *c)
 {
     if (c->variant != jac::TMA_WIDE || getenv("JAC_VARIANT")) return JAC_OK;
+    if (c->flags & JAC_F_2D) {  // 2-D: 4 stages measured 5% faster on every box, both regimes
+        c->variant = jac::TMA_WIDE4;
+        configure_tiles(c);
+        return JAC_OK;
+    }
     if (const char *s = getenv("JAC_AUTOTUNE"); s && atoi(s) == 0) return JAC_OK;
     const int cands[2] = {jac::TMA_WIDE, jac::TMA_WIDE4};
     float ms_of[2] = {0.f, 0.f};
@@ -434,10 +441,8 @@ int autotune(jac_ctx *c)
         CK(cudaEventElapsedTime(&ms_of[n], c->ev0, c->ev1));
         c->tuned_ms[n] = ms_of[n] / 8;
     }
-    // ties (< 0.5%) go to the usual winner: 6 stages in 3-D, 4 stages in 2-D
-    const bool two_d = (c->flags & JAC_F_2D) != 0;
-    c->variant = (two_d ? (ms_of[0] < 0.995f * ms_of[1]) : !(ms_of[1] < 0.995f * ms_of[0])) ? jac::TMA_WIDE
-                                                                                             : jac::TMA_WIDE4;
+    // ties (< 0.5%) go to the usual winner, 6 stages
+    c->variant = (ms_of[1] < 0.995f * ms_of[0]) ? jac::TMA_WIDE4 : jac::TMA_WIDE;
     configure_tiles(c);
     return JAC_OK;
 }

@@ -639,52 +639,80 @@ __global__ void __launch_bounds__(NT, 4) sweep2d_tma_kernel(const __grid_constan
         if (a.mode == MODE_FUSED) xf = blk.nb[f][dst];
         else if (blk.nb[f][0]) xf = a.outbox + (int64_t)blk.slot * g.ostride + g.ooff[f];
     }
-    for (int q = 0; q < nq; ++q) {
+    // general y tile: every store through emit_pair
+    auto tile_general = [&](int q) {
         mbar_wait(&bars[q % NS], (q / NS) & 1);
         const double *S = stage + (q % NS) * L::STRIDE;
         const int y0 = (ty0 + q) * BY;
-        const bool lean = xfull && (y0 + BY <= g.ey) && !((y0 == 0 && ym_face) || (y0 + BY == g.ey && yp_face));
-        if (lean) {
-            const double *Sb = S + sb;
-            double2 rw[RY + 2];  // rows jl0-1 .. jl0+RY
 #pragma unroll
-            for (int r = 0; r < RY + 2; ++r) rw[r] = *reinterpret_cast<const double2 *>(Sb + (r - 1) * W);
-            double *op = own + (int64_t)(y0 + jl0 + 1) * g.P + g.A + i;
-#pragma unroll
-            for (int r = 0; r < RY; ++r) {
-                double xm = Sb[r * W - 1], xp1 = Sb[r * W + 2];
-                if (xedge) {
-                    if (ilo) xm = S[xg + r];
-                    if (ihi1) xp1 = S[xg + BY + r];
-                }
-                const double2 c = rw[r + 1];
-                double2 v;
-                v.x = stencil5(c.x, xm, c.y, rw[r].x, rw[r + 2].x);
-                v.y = stencil5(c.y, c.x, xp1, rw[r].y, rw[r + 2].y);
-                *reinterpret_cast<double2 *>(op + r * g.P) = v;
-                if (xedge && xf) xf[y0 + jl0 + r] = ilo ? v.x : v.y;
-            }
-        } else {
-#pragma unroll
-            for (int r = 0; r < RY; ++r) {
-                const int jl = rg * RY + r;
-                const double *row = S + (jl + 1) * W + col;
-                const double2 c = *reinterpret_cast<const double2 *>(row);
-                const double xm = ilo ? S[L::XG_OFF + jl] : row[-1];
-                const double xp1 = ihi1 ? S[L::XG_OFF + BY + jl] : row[2];
-                const double xp0 = ihi0 ? S[L::XG_OFF + BY + jl] : c.y;
-                const double2 ym = *reinterpret_cast<const double2 *>(row - W);
-                const double2 yp = *reinterpret_cast<const double2 *>(row + W);
-                double2 v;
-                v.x = stencil5(c.x, xm, xp0, ym.x, yp.x);
-                v.y = stencil5(c.y, c.x, xp1, ym.y, yp.y);
-                const int j = y0 + jl;
-                if (j < g.ey) emit_pair<false>(a, blk, dst, own, (int64_t)(j + 1) * g.P + g.A + i, i, j, 0, v);
-            }
+        for (int r = 0; r < RY; ++r) {
+            const int jl = rg * RY + r;
+            const double *row = S + (jl + 1) * W + col;
+            const double2 c = *reinterpret_cast<const double2 *>(row);
+            const double xm = ilo ? S[L::XG_OFF + jl] : row[-1];
+            const double xp1 = ihi1 ? S[L::XG_OFF + BY + jl] : row[2];
+            const double xp0 = ihi0 ? S[L::XG_OFF + BY + jl] : c.y;
+            const double2 ym = *reinterpret_cast<const double2 *>(row - W);
+            const double2 yp = *reinterpret_cast<const double2 *>(row + W);
+            double2 v;
+            v.x = stencil5(c.x, xm, xp0, ym.x, yp.x);
+            v.y = stencil5(c.y, c.x, xp1, ym.y, yp.y);
+            const int j = y0 + jl;
+            if (j < g.ey) emit_pair<false>(a, blk, dst, own, (int64_t)(j + 1) * g.P + g.A + i, i, j, 0, v);
         }
         __syncthreads();
         if (threadIdx.x == 0 && q + NS < nq) issue(q + NS);
+    };
+    auto lean_ok = [&](int q) {
+        const int y0 = (ty0 + q) * BY;
+        return xfull && (y0 + BY <= g.ey) && !((y0 == 0 && ym_face) || (y0 + BY == g.ey && yp_face));
+    };
+    // The block's first and last y tile (y faces, ragged rows) take the general path;
+    // the tiles between are lean whenever the tile is full in x.
+    int q = 0;
+    if (q < nq && !lean_ok(q)) tile_general(q++);
+    const int qend = (nq > q && !lean_ok(nq - 1)) ? nq - 1 : nq;
+    if (xfull && q < qend) {
+        int sl = q % NS;                    // ring slot of tile q
+        uint32_t ph = (q / NS) & 1u;        // its mbarrier parity
+        double *op = own + (int64_t)((ty0 + q) * BY + jl0 + 1) * g.P + g.A + i;
+        double *xfp = xf ? xf + (ty0 + q) * BY + jl0 : nullptr;
+        const int64_t P = g.P, TP = (int64_t)BY * g.P;
+        auto run = [&](const bool XE) {
+            for (; q < qend; ++q) {
+                mbar_wait(&bars[sl], ph);
+                const double *S = stage + sl * L::STRIDE;
+                const double *Sb = S + sb;
+                double2 rw[RY + 2];  // rows jl0-1 .. jl0+RY
+#pragma unroll
+                for (int r = 0; r < RY + 2; ++r) rw[r] = *reinterpret_cast<const double2 *>(Sb + (r - 1) * W);
+#pragma unroll
+                for (int r = 0; r < RY; ++r) {
+                    double xm = Sb[r * W - 1], xp1 = Sb[r * W + 2];
+                    if (XE) {
+                        if (ilo) xm = S[xg + r];
+                        if (ihi1) xp1 = S[xg + BY + r];
+                    }
+                    const double2 c = rw[r + 1];
+                    double2 v;
+                    v.x = stencil5(c.x, xm, c.y, rw[r].x, rw[r + 2].x);
+                    v.y = stencil5(c.y, c.x, xp1, rw[r].y, rw[r + 2].y);
+                    *reinterpret_cast<double2 *>(op + r * P) = v;
+                    if (XE && xfp) xfp[r] = ilo ? v.x : v.y;
+                }
+                op += TP;
+                if (XE && xfp) xfp += BY;
+                __syncthreads();
+                if (threadIdx.x == 0 && q + NS < nq) issue(q + NS);
+                if (++sl == NS) { sl = 0; ph ^= 1u; }
+            }
+        };
+        if (xedge) run(true);
+        else run(false);
+    } else {
+        for (; q < qend; ++q) tile_general(q);
     }
+    if (q < nq) tile_general(q);
     if (remote) signal_done(a);
 }
 
