@@ -397,6 +397,7 @@ def run_ours(args, D):
     # per-launch sweep duration (CUDA events around each sweep launch, same stream)
     cool(D)
     sweep_ms = D.max(J.profile_sweep(min(max(K, 10), 50)))
+    gap_us = 1e3 * D.max(J.profile_gap_ms())  # end of sweep i -> start of sweep i+1 (device clock)
     achieved = BYTES_PER_LUP * pts_gpu / (sweep_ms * 1e-3) / 1e9
     traffic = ncu_traffic(label)
 
@@ -447,7 +448,7 @@ def run_ours(args, D):
         nccl_ablation["exposed_exchange_ms_per_iter"] = ms_iter - nccl_ablation["skip_exchange_WRONG"]["ms_per_iter"]
     return finish_ours(args, D, K, W, dims, blocks, g, label, scaling, pts, pts_gpu, peak, peak_src, value, ms_iter,
                        st, sweep_ms, achieved, traffic, e2e_val, h2d, d2h, launches, sampler, nccl_ablation,
-                       sustained)
+                       sustained, gap_us)
 
 
 def run_e2e(J, D, dims, origin, extent, pts, pts_gpu, K):
@@ -476,7 +477,8 @@ def run_e2e(J, D, dims, origin, extent, pts, pts_gpu, K):
 
 
 def finish_ours(args, D, K, W, dims, blocks, g, label, scaling, pts, pts_gpu, peak, peak_src, value, ms_iter, st,
-                sweep_ms, achieved, traffic, e2e_val, h2d, d2h, launches, sampler, nccl_ablation, sustained=None):
+                sweep_ms, achieved, traffic, e2e_val, h2d, d2h, launches, sampler, nccl_ablation, sustained=None,
+                gap_us=None):
     from paper_2605_12734_b200 import jacobi3d as JB
 
     # ---- ODF sweep + ablations (N = 1, c2)
@@ -493,13 +495,13 @@ def finish_ours(args, D, K, W, dims, blocks, g, label, scaling, pts, pts_gpu, pe
                 ms, _ = time_ctx(Jo, K, W, D)
                 cool(D)
                 sw = Jo.profile_sweep(20)
-                runs.append((ms, sw))
+                runs.append((ms, sw, Jo.profile_gap_ms()))
                 close_ctx(Jo, D)
             runs.sort()
-            ms, sw = runs[1]
+            ms, sw, gp = runs[1]
             sweep[str(odf)] = {"blocks": b2, "ms_per_iter": ms / K, "glups": pts * K / (ms * 1e-3) / 1e9,
                                "hbm_frac": BYTES_PER_LUP * pts / (ms / K * 1e-3) / 1e9 / peak,
-                               "sweep_kernel_us": 1e3 * sw, "allocations": 3,
+                               "sweep_kernel_us": 1e3 * sw, "inter_launch_gap_us": 1e3 * gp, "allocations": 3,
                                "ms_per_iter_min_max": [runs[0][0] / K, runs[2][0] / K]}
         base = sweep["1"]["ms_per_iter"]
         for v in sweep.values():
@@ -561,6 +563,7 @@ def finish_ours(args, D, K, W, dims, blocks, g, label, scaling, pts, pts_gpu, pe
                          "kernel": "sweep2d_tma_kernel" if MODE_2D[0] else "sweep_tma_kernel",
                          "algorithmic_bytes_per_launch": BYTES_PER_LUP * pts_gpu,
                          "avg_launch_us": 1e3 * sweep_ms,
+                         "inter_launch_gap_us": gap_us,
                          "sweep_share_of_step": sweep_ms / ms_iter},
             "hbm_frac_step": BYTES_PER_LUP * pts_gpu / (ms_iter * 1e-3) / 1e9 / peak,
             "hbm_frac_step_vs_8TBs": BYTES_PER_LUP * pts_gpu / (ms_iter * 1e-3) / 1e9 / 8000.0,

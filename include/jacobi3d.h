@@ -214,6 +214,13 @@ int jac_last_step_ms(const jac_ctx *c, double *ms);
  * median sweep-kernel duration in ms (the roofline's per-launch figure).  Advances
  * the state like jac_step. */
 int jac_profile_sweep(jac_ctx *c, int32_t n_iters, double *avg_sweep_ms);
+/* Median device-time gap, in ms, between the end of one sweep launch and the start
+ * of the next inside the last jac_profile_sweep graph (n_iters >= 2): the per-
+ * iteration launch / dependency cost of the graph-replayed iteration (in the fused
+ * mode nothing else runs between sweeps; the event-record nodes are included).
+ * JAC_ESTATE before such a profile.  The launch/sync-gap evidence SURVEY.md §8(d.1)
+ * asks of an nsys timeline, on the device clock. */
+int jac_last_profile_gap_ms(const jac_ctx *c, double *gap_ms);
 
 enum jac_stat {
     JAC_STAT_KERNEL_LAUNCHES = 0, /* our kernels launched so far (graph nodes counted) */

@@ -150,6 +150,7 @@ struct jac_ctx {
     int ntx = 1, nty = 1, ntz = 1, zc = 1;
     int nzc = 1, ncols = 1, nitems = 1, gcols = 1;
     float tuned_ms[2] = {0.f, 0.f};  // autotune: sweep ms for the 6- and 4-stage wide tiles
+    double last_gap_ms = -1.0;       // jac_profile_sweep: median gap between consecutive sweeps
 
     // cross-rank exchange
     std::vector<int32_t> peer_ranks;     // face-adjacent ranks
@@ -1121,14 +1122,33 @@ int jac_profile_sweep(jac_ctx *c, int32_t n, double *avg_ms)
     if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
     cudaGraphExecDestroy(exec);
     if (e != cudaSuccess) return fail(JAC_ECUDA, "profile graph: %s", cudaGetErrorString(e));
-    std::vector<float> dur(n);
+    std::vector<float> dur(n), gap(n > 1 ? n - 1 : 0);
     for (int it = 0; it < n; ++it) CK(cudaEventElapsedTime(&dur[it], ev[2 * it], ev[2 * it + 1]));
+    // end of sweep i -> start of sweep i+1: the graph's launch / dependency gap
+    // (plus whatever the iteration enqueues after the sweep: nothing in the fused
+    // mode; the ghost-fill kernel / NCCL calls in the ablation modes)
+    for (int it = 0; it + 1 < n; ++it) CK(cudaEventElapsedTime(&gap[it], ev[2 * it + 1], ev[2 * it + 2]));
+    if (!gap.empty()) {
+        std::sort(gap.begin(), gap.end());
+        const size_t m = gap.size();
+        c->last_gap_ms = (m & 1) ? gap[m / 2] : 0.5 * ((double)gap[m / 2 - 1] + gap[m / 2]);
+    } else {
+        c->last_gap_ms = -1.0;
+    }
     c->iters += n;
     c->kernel_launches += (int64_t)n * c->kernels_per_iter();
     // median: robust to the first launches of a multi-rank run, whose remote items may
     // wait for a neighbour rank that started its profiling graph a little later
     std::sort(dur.begin(), dur.end());
     *avg_ms = (n & 1) ? dur[n / 2] : 0.5 * ((double)dur[n / 2 - 1] + dur[n / 2]);
+    return JAC_OK;
+}
+
+int jac_last_profile_gap_ms(const jac_ctx *c, double *ms)
+{
+    if (!c || !ms) return fail(JAC_EINVAL, "ctx/ms is NULL");
+    if (c->last_gap_ms < 0) return fail(JAC_ESTATE, "no jac_profile_sweep with n_iters >= 2 yet");
+    *ms = c->last_gap_ms;
     return JAC_OK;
 }
 

@@ -36,7 +36,8 @@ STAT_NAMES = ["kernel_launches", "graph_launches", "kernels_per_iter", "local_bl
 EXPORTED = ["jac_plan", "jac_plan_face", "jac_create", "jac_create_rank", "jac_ipc_handle_bytes",
             "jac_export_ipc", "jac_import_ipc", "jac_set_init", "jac_set_init_hash", "jac_step",
             "jac_get_block", "jac_get_block_padded", "jac_get_field", "jac_get_layout",
-            "jac_block_owner", "jac_last_step_ms", "jac_set_init_box", "jac_get_field_box", "jac_local_box", "jac_profile_sweep", "jac_get_stats",
+            "jac_block_owner", "jac_last_step_ms", "jac_set_init_box", "jac_get_field_box", "jac_local_box",
+            "jac_profile_sweep", "jac_last_profile_gap_ms", "jac_get_stats",
             "jac_destroy", "jac_last_error", "jac_version", "jac_set_option", "jac_nccl_id_bytes",
             "jac_nccl_get_unique_id", "jac_nccl_init", "jac_get_region"]
 MICROBENCH_EXPORTED = ["jac_mb_launch_latency", "jac_mb_overlap", "jac_mb_launch_rate", "jac_mb_pipeline",
@@ -92,6 +93,7 @@ def load() -> ctypes.CDLL:
         "jac_block_owner": [vp, i32, i32, i32, P(i32)],
         "jac_last_step_ms": [vp, P(ctypes.c_double)],
         "jac_profile_sweep": [vp, i32, P(ctypes.c_double)],
+        "jac_last_profile_gap_ms": [vp, P(ctypes.c_double)],
         "jac_get_stats": [vp, P(i64)],
         "jac_destroy": [vp],
         "jac_set_option": [vp, i32, i64],
@@ -279,6 +281,12 @@ def jac_profile_sweep(ctx, n_iters: int) -> float:
     return v.value
 
 
+def jac_last_profile_gap_ms(ctx) -> float:
+    v = ctypes.c_double()
+    _check(load().jac_last_profile_gap_ms(ctx, ctypes.byref(v)), "jac_last_profile_gap_ms")
+    return v.value
+
+
 def jac_get_stats(ctx) -> dict:
     st = (ctypes.c_int64 * len(STAT_NAMES))()
     _check(load().jac_get_stats(ctx, st), "jac_get_stats")
@@ -400,6 +408,10 @@ class Jacobi3D:
 
     def profile_sweep(self, n: int) -> float:
         return jac_profile_sweep(self.ctx, n)
+
+    def profile_gap_ms(self) -> float:
+        """Median gap between consecutive sweeps of the last profile_sweep (n >= 2)."""
+        return jac_last_profile_gap_ms(self.ctx)
 
     def set_option(self, option: int, value: int) -> None:
         jac_set_option(self.ctx, option, value)

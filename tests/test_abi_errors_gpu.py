@@ -96,3 +96,17 @@ def test_rank_context_needs_ipc_before_init(lib):
         _expect(lib, lib.jac_nccl_init(c, None), J.JAC_EINVAL)
     finally:
         assert lib.jac_destroy(c) == J.JAC_OK
+
+
+def test_profile_gap(lib, ctx):
+    """jac_last_profile_gap_ms: JAC_ESTATE before a profile; afterwards the median
+    end-of-sweep -> next-sweep gap of the graph, a few microseconds (one kernel per
+    iteration, no host round trip)."""
+    g = dbl()
+    _expect(lib, lib.jac_last_profile_gap_ms(ctx, ctypes.byref(g)), J.JAC_ESTATE)
+    _expect(lib, lib.jac_last_profile_gap_ms(ctx, None), J.JAC_EINVAL)
+    assert lib.jac_set_init_hash(ctx, 1) == J.JAC_OK
+    d = dbl()
+    assert lib.jac_profile_sweep(ctx, 12, ctypes.byref(d)) == J.JAC_OK
+    assert lib.jac_last_profile_gap_ms(ctx, ctypes.byref(g)) == J.JAC_OK
+    assert 0.0 <= g.value < 0.05, g.value
