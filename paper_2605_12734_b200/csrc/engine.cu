@@ -151,6 +151,7 @@ struct jac_ctx {
     int nzc = 1, ncols = 1, nitems = 1, gcols = 1;
     float tuned_ms[2] = {0.f, 0.f};  // autotune: sweep ms for the 6- and 4-stage wide tiles
     double last_gap_ms = -1.0;       // jac_profile_sweep: median gap between consecutive sweeps
+    bool pdl = true;                 // sweeps use programmatic dependent launch (JAC_PDL=0: off)
 
     // cross-rank exchange
     std::vector<int32_t> peer_ranks;     // face-adjacent ranks
@@ -246,8 +247,8 @@ int enqueue_sweep(jac_ctx *c, int src)
 {
     const jac::SweepArgs a = sweep_args(c, src, sweep_mode(c));
     if (c->variant == kPlain) CK(jac::launch_sweep_plain(a, c->stream));
-    else if (c->flags & JAC_F_2D) CK(jac::launch_sweep2d_tma(c->tmap, a, c->variant, c->stream));
-    else CK(jac::launch_sweep_tma(c->tmap, a, c->variant, c->stream));
+    else if (c->flags & JAC_F_2D) CK(jac::launch_sweep2d_tma(c->tmap, a, c->variant, c->stream, c->pdl));
+    else CK(jac::launch_sweep_tma(c->tmap, a, c->variant, c->stream, c->pdl));
     return JAC_OK;
 }
 
@@ -534,6 +535,7 @@ int create_common(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, in
     }
     configure_tiles(c);
     if (const char *s = getenv("JAC_UNROLL")) c->unroll = std::max(2, atoi(s) & ~1);
+    if (const char *s = getenv("JAC_PDL")) c->pdl = atoi(s) != 0;
     if ((int64_t)c->nslots * c->ntx * c->nty * c->ntz > 0x7fffffffLL) {
         delete c;
         return fail(JAC_EINVAL, "too many tiles for one launch");

@@ -149,6 +149,19 @@ __device__ __forceinline__ void emit_pair(const SweepArgs &a, const DevBlock &bl
     }
 }
 
+// ------------------------------------------------------------------ programmatic dependent launch
+// Sweeps are launched with programmatic stream serialization: every CTA lets the
+// next sweep be scheduled early (its CTAs fill SMs freed during this sweep's last
+// wave) and then waits, before touching any buffer, until the previous grid has
+// completed and its memory is visible.  Only the read-only descriptor table and the
+// kernel parameters are read before the wait, so the result is that of serialized
+// launches.  Without the launch attribute both instructions are no-ops.
+__device__ __forceinline__ void pdl_launch_dependents_then_wait()
+{
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 // ------------------------------------------------------------------ TMA / mbarrier
 __device__ __forceinline__ uint32_t smem_u32(const void *p)
 {
@@ -321,6 +334,7 @@ __global__ void __launch_bounds__(NT, min_ctas_per_sm(NT, NS))
     const bool remote = a.fused_sync && (int)blockIdx.x < a.nremote;  // item_map puts them first
     __shared__ DevBlock blk;  // this item's descriptor, read once from the table
     if (threadIdx.x == 0) blk = a.blocks[t.b];
+    pdl_launch_dependents_then_wait();
     const int soff = tile_soff<BX, W>(g, t.x0);  // staged column of point i = x0 (0, 2 or 4)
     const int c0 = g.A + t.x0 - soff;
     const bool xlo = (t.x0 == 0);                 // tile touches the x- block face
@@ -588,6 +602,7 @@ __global__ void __launch_bounds__(NT, 4) sweep2d_tma_kernel(const __grid_constan
     const int x0 = t.x0;
     __shared__ DevBlock blk;
     if (threadIdx.x == 0) blk = a.blocks[b];
+    pdl_launch_dependents_then_wait();
     const int soff = tile_soff<BX, W>(g, x0);
     const int c0 = g.A + x0 - soff;
     const bool xlo = (x0 == 0), xhi = (x0 + BX >= g.ex);
@@ -963,8 +978,26 @@ static cudaError_t prepare_tma_t()
                                 (int)smem);
 }
 
+// <<<grid, block, smem, s>>>(args...) with programmatic stream serialization when pdl
+template <typename... Args>
+static cudaError_t launch_maybe_pdl(void (*kernel)(Args...), unsigned grid, unsigned block, size_t smem,
+                                    cudaStream_t s, bool pdl, const Args &...args)
+{
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
 template <int BX, int BY, int W, int NT, int NS>
-static cudaError_t launch_tma_t(const CUtensorMap &tm, const SweepArgs &a, cudaStream_t s)
+static cudaError_t launch_tma_t(const CUtensorMap &tm, const SweepArgs &a, cudaStream_t s, bool pdl)
 {
     constexpr size_t smem = tma_smem_bytes(BX, BY, W, NS);
     // One CTA per item: the hardware launches CTAs in index order as slots free up,
@@ -972,8 +1005,7 @@ static cudaError_t launch_tma_t(const CUtensorMap &tm, const SweepArgs &a, cudaS
     // close, so their shared halo planes are L2 hits.  A persistent grid with static
     // striding lets CTAs drift apart and turns halos into DRAM re-reads (measured
     // 359 -> 454 us per 512^3 sweep).
-    sweep_tma_kernel<BX, BY, W, NT, NS><<<(unsigned)a.nitems, NT, smem, s>>>(tm, a);
-    return cudaGetLastError();
+    return launch_maybe_pdl(sweep_tma_kernel<BX, BY, W, NT, NS>, (unsigned)a.nitems, NT, smem, s, pdl, tm, a);
 }
 
 // Ring depth, measured on several B200 boxes: for the wide tile a 6-stage ring (3 CTAs
@@ -1021,30 +1053,30 @@ cudaError_t prepare_sweep_tma(int variant)
     return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_sweep_tma(const CUtensorMap &tm, const SweepArgs &a, int variant, cudaStream_t s)
+cudaError_t launch_sweep_tma(const CUtensorMap &tm, const SweepArgs &a, int variant, cudaStream_t s, bool pdl)
 {
 #define X(V, BX, BY, W, NT, NS) \
-    if (variant == V) return launch_tma_t<BX, BY, W, NT, NS>(tm, a, s);
+    if (variant == V) return launch_tma_t<BX, BY, W, NT, NS>(tm, a, s, pdl);
     JAC_TMA_VARIANTS(X)
 #undef X
     return cudaErrorInvalidValue;
 }
 
 template <int BX, int BY, int W, int NT, int NS>
-static cudaError_t launch2d_t(const CUtensorMap &tm, const SweepArgs &a, cudaStream_t s, bool prepare_only)
+static cudaError_t launch2d_t(const CUtensorMap &tm, const SweepArgs &a, cudaStream_t s, bool prepare_only,
+                              bool pdl = false)
 {
     constexpr size_t smem = tma_smem_bytes(BX, BY, W, NS);
     if (prepare_only)
         return cudaFuncSetAttribute(sweep2d_tma_kernel<BX, BY, W, NT, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)smem);
-    sweep2d_tma_kernel<BX, BY, W, NT, NS><<<(unsigned)a.nitems, NT, smem, s>>>(tm, a);
-    return cudaGetLastError();
+    return launch_maybe_pdl(sweep2d_tma_kernel<BX, BY, W, NT, NS>, (unsigned)a.nitems, NT, smem, s, pdl, tm, a);
 }
 
-cudaError_t launch_sweep2d_tma(const CUtensorMap &tm, const SweepArgs &a, int variant, cudaStream_t s)
+cudaError_t launch_sweep2d_tma(const CUtensorMap &tm, const SweepArgs &a, int variant, cudaStream_t s, bool pdl)
 {
 #define X(V, BX, BY, W, NT, NS) \
-    if (variant == V) return launch2d_t<BX, BY, W, NT, NS>(tm, a, s, false);
+    if (variant == V) return launch2d_t<BX, BY, W, NT, NS>(tm, a, s, false, pdl);
     JAC_TMA_VARIANTS(X)
 #undef X
     return cudaErrorInvalidValue;

@@ -20,8 +20,12 @@ struct TileShape { int bx, by, w; };
 TileShape tma_tile_shape(int variant);
 cudaError_t prepare_sweep_tma(int variant);   // sets the dynamic-smem attribute (current device)
 int sweep_resident_ctas(int variant);         // SMs x resident CTAs of the TMA sweep (current device)
-cudaError_t launch_sweep_tma(const CUtensorMap &tm, const SweepArgs &a, int variant, cudaStream_t s);
-cudaError_t launch_sweep2d_tma(const CUtensorMap &tm, const SweepArgs &a, int variant, cudaStream_t s);
+// pdl: launch with programmatic stream serialization (the next sweep's CTAs may be
+// scheduled during this one's tail; they wait for its completion before any access)
+cudaError_t launch_sweep_tma(const CUtensorMap &tm, const SweepArgs &a, int variant, cudaStream_t s,
+                             bool pdl = false);
+cudaError_t launch_sweep2d_tma(const CUtensorMap &tm, const SweepArgs &a, int variant, cudaStream_t s,
+                               bool pdl = false);
 cudaError_t prepare_sweep2d_tma(int variant);
 cudaError_t launch_sweep_plain(const SweepArgs &a, cudaStream_t s);  // 64 x 8 tiles
 cudaError_t launch_sweep_plain_one(const SweepArgs &a, cudaStream_t s);  // a.blocks = one block

@@ -1,4 +1,3 @@
-F=gpurun_out/final4; mkdir -p $F
-R="python -m torch.distributed.run --nnodes 1 --master-addr 127.0.0.1"
-CUDA_VISIBLE_DEVICES=0 python bench.py --config j2d --no-sweep --no-cpu > $F/bench_j2d_n1.json 2> $F/bench_j2d_n1.err
-for n in 2 4; do $R --nproc-per-node $n --master-port $((29500 + RANDOM % 400)) bench.py --gpus $n --config j2d > $F/bench_j2d_n$n.json 2> $F/bench_j2d_n$n.err; done
+F=gpurun_out/pdl; mkdir -p $F
+CUDA_VISIBLE_DEVICES=0 timeout 600 python tools/pdl_probe.py > $F/probe.log 2>&1
+timeout 2400 python -m pytest tests -m gpu -q 2>&1 | tail -5 > $F/pytest_gpu.log
