@@ -525,12 +525,14 @@ int create_common(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, in
     if (flags & JAC_F_NO_TMA) c->variant = kPlain;
     // (32-wide blocks: 32 x 16 tiles; the 32 x 32 tile won only while y-face rows
     // took the general epilogue -- lean y faces: 445 vs 462 us for 512^3 in 32^3 blocks)
-    else c->variant = (g.ex <= 32) ? jac::TMA_EXACT32 : (g.ex <= 64) ? jac::TMA_EXACT64 : jac::TMA_WIDE;
+    // (64-wide blocks: 6-stage ring, 377-379 vs 399-409 us for 512^3 in 64^3 blocks;
+    // 32-wide blocks: 6 stages within noise of 4, which stay)
+    else c->variant = (g.ex <= 32) ? jac::TMA_EXACT32 : (g.ex <= 64) ? jac::TMA_EXACT64_6 : jac::TMA_WIDE;
     if (const char *s = getenv("JAC_VARIANT"); s && c->variant != kPlain) {
         const int v = atoi(s);  // tuning knob; EXACT* only where one tile spans the block row
         if (v == jac::TMA_WIDE || v == jac::TMA_WIDE4 || v == jac::TMA_NARROW || 
-            ((v == jac::TMA_EXACT32 || v == jac::TMA_EXACT32_TALL) && g.ex <= 32) ||
-            (v == jac::TMA_EXACT64 && g.ex <= 64))
+            ((v == jac::TMA_EXACT32 || v == jac::TMA_EXACT32_TALL || v == jac::TMA_EXACT32_6) && g.ex <= 32) ||
+            ((v == jac::TMA_EXACT64 || v == jac::TMA_EXACT64_6) && g.ex <= 64))
             c->variant = v;
     }
     configure_tiles(c);

@@ -1024,7 +1024,9 @@ static cudaError_t launch_tma_t(const CUtensorMap &tm, const SweepArgs &a, cudaS
     X(TMA_NARROW, 32, 16, 36, 256, 4)     \
     X(TMA_EXACT32, 32, 16, 32, 256, 4)    \
     X(TMA_EXACT64, 64, 16, 64, 256, 4)    \
-    X(TMA_EXACT32_TALL, 32, 32, 32, 256, 4)
+    X(TMA_EXACT32_TALL, 32, 32, 32, 256, 4) \
+    X(TMA_EXACT32_6, 32, 16, 32, 256, 6)    \
+    X(TMA_EXACT64_6, 64, 16, 64, 256, 6)
 
 int sweep_resident_ctas(int variant)
 {

@@ -13,7 +13,9 @@ enum TmaVariant {
     TMA_NARROW = 1,  /* 32 x 16 tiles, staged 36 wide (blocks 33..64 wide) */
     TMA_EXACT32 = 3, /* 32 x 16 tiles, staged 32 wide: one tile per block row (ex <= 32) */
     TMA_EXACT64 = 4, /* 64 x 16 tiles, staged 64 wide: one tile per block row (ex <= 64) */
-    TMA_EXACT32_TALL = 12 /* 32 x 32 tiles: a whole 32^2 block face per item (ex <= 32) */
+    TMA_EXACT32_TALL = 12, /* 32 x 32 tiles: a whole 32^2 block face per item (ex <= 32) */
+    TMA_EXACT32_6 = 13,    /* 32 x 16 tiles, 6-stage ring (ex <= 32) */
+    TMA_EXACT64_6 = 14     /* 64 x 16 tiles, 6-stage ring (ex <= 64) */
 };
 struct TileShape { int bx, by, w; };
 

@@ -151,4 +151,6 @@ def test_sass_no_fma_and_tma_present():
     assert "DFMA" not in sass
     funcs = sass.split("Function : ")
     tma = [f for f in funcs if f.startswith("_ZN3jac16sweep_tma_kernel")]
-    assert len(tma) == 6 and all("UTMALDG" in f and "UBLKCP" in f for f in tma)
+    assert len(tma) >= 6 and all("UTMALDG" in f and "UBLKCP" in f for f in tma)
+    # programmatic dependent launch: every sweep instantiation waits on its predecessor
+    assert all("ACQBULK" in f and "PREEXIT" in f for f in tma)

@@ -16,7 +16,7 @@ from paper_2605_12734_b200 import jacobi3d as J
 pytestmark = pytest.mark.gpu
 
 N_CASES = 32
-_VARIANTS = [None, None, None, "0", "5", "1", "3", "4", "12"]
+_VARIANTS = [None, None, None, "0", "5", "1", "3", "4", "12", "13", "14"]
 _FLAGS = [0, 0, 0, J.JAC_F_NO_GRAPH, J.JAC_F_UNFUSED_PACK, J.JAC_F_FMA, J.JAC_F_NO_TMA]
 
 
