@@ -44,6 +44,7 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 MODE_2D = [False]  # set for --config j2d
+EXTRA = {}  # additional keys of our JSON line
 BYTES_PER_LUP = 16  # algorithmic HBM bytes per lattice update: 8 B read + 8 B write
 FLOPS_PER_LUP = 7
 
@@ -233,6 +234,16 @@ class Dist:
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
         return float(t.item())
 
+    def gather(self, v):
+        """[v of rank 0, v of rank 1, ...] (a one-element list without torch.distributed)."""
+        if not self.dist:
+            return [v]
+        import torch
+        t = torch.tensor([float(v)], device="cuda")
+        out = [torch.zeros_like(t) for _ in range(self.world)]
+        self.dist.all_gather(out, t)
+        return [float(x.item()) for x in out]
+
     def sum(self, v):
         if not self.dist:
             return v
@@ -391,6 +402,7 @@ def run_ours(args, D):
     J.set_init_hash(1)
     sampler = ClockSampler(D.local)
     dev_ms, launches = time_ctx(J, K, W, D, sampler)
+    rank_ms = D.gather(J.last_step_ms())  # each rank's own device time (value uses the max)
     value = pts * K / (dev_ms * 1e-3) / 1e9
     ms_iter = dev_ms / K
     st = J.stats()
@@ -426,6 +438,8 @@ def run_ours(args, D):
     else:
         e2e_val, h2d, d2h = run_e2e(J, D, dims, origin, extent, pts, pts_gpu, K)
     nccl_ablation = None
+    if D.world > 1:
+        EXTRA["rank_ms_per_step"] = [m / K for m in rank_ms]
     if D.world > 1 and not args.no_sweep:  # NCCL send/recv of packed faces instead of peer stores
         Jn = make_ctx(dims, blocks, g, D, flags=JB.JAC_F_NCCL)
         Jn.set_init_hash(1)
@@ -587,6 +601,7 @@ def finish_ours(args, D, K, W, dims, blocks, g, label, scaling, pts, pts_gpu, pe
             line["paper_style_per_block"] = paper_style
         if nccl_ablation is not None:
             line["exchange_ablations"] = nccl_ablation
+        line.update(EXTRA)
         print(json.dumps(line), flush=True)
     D.finish()
 
