@@ -1,9 +1,6 @@
-F=gpurun_out/ranks2; mkdir -p $F
-R="python -m torch.distributed.run --nnodes 1 --master-addr 127.0.0.1"
-for rep in 1 2; do
-  # four independent 1-GPU runs at the same time (no communication at all)
-  for g in 0 1 2 3; do CUDA_VISIBLE_DEVICES=$g python bench.py --no-sweep --no-e2e --no-sustained --no-cpu --steps 2000 > $F/conc_${rep}_gpu$g.json 2>/dev/null & done; wait
-  for g in 0 1 2 3; do CUDA_VISIBLE_DEVICES=$g python bench.py --no-sweep --no-e2e --no-sustained --no-cpu --steps 2000 > $F/solo_${rep}_gpu$g.json 2>/dev/null; done
-  $R --nproc-per-node 4 --master-port $((29500 + RANDOM % 400)) bench.py --gpus 4 --no-sweep --no-e2e --no-sustained --steps 2000 > $F/n4_${rep}.json 2> /dev/null
-  JAC_NO_FUSED_SYNC=1 $R --nproc-per-node 4 --master-port $((29500 + RANDOM % 400)) bench.py --gpus 4 --no-sweep --no-e2e --no-sustained --steps 2000 > $F/n4nofused_${rep}.json 2> /dev/null
-done
+F=gpurun_out/final6; mkdir -p $F
+timeout 2400 python -m pytest tests -m gpu -q 2>&1 | tail -5 > $F/pytest_gpu.log
+python -c "import __graft_entry__ as g; g.build(); g.smoke(); print('smoke ok')" > $F/smoke.log 2>&1
+export CUDA_VISIBLE_DEVICES=0
+python tools/profile_sweep.py --blocks 8 8 8 --iters 3 > $F/pre.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:sweep -c 1 -o $F/r01b_sweep_blocks888 -f python tools/profile_sweep.py --blocks 8 8 8 --iters 2 > /dev/null 2>&1
