@@ -25,6 +25,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/jacobi3d.h"
@@ -222,6 +223,7 @@ jac::SweepArgs sweep_args(const jac_ctx *c, int src, int mode)
     a.mode = mode;
     a.ntx = c->ntx; a.nty = c->nty; a.ntz = c->ntz; a.zc = c->zc;
     a.nzc = c->nzc; a.ncols = c->ncols; a.nitems = c->nitems; a.gcols = c->gcols;
+    if (c->ditem_map && !c->fused) a.item_map = c->ditem_map;  // JAC_ORDER_EXP
     if (c->fused && mode == jac::MODE_FUSED) {
         a.fused_sync = 1;
         a.nremote = c->nremote;
@@ -449,6 +451,56 @@ int autotune(jac_ctx *c)
     return JAC_OK;
 }
 
+// Launch order for the fused cross-rank sync: the items touching a face in mask[b]
+// first (their completion releases the neighbour ranks), then -- partners -- the 3-D
+// items sharing a staged halo (x/y neighbour column, z neighbour chunk) with one of
+// them, then the rest, each class in the natural order.  *n_first = first class size.
+std::vector<int32_t> remote_first_order(jac_ctx *c, const std::vector<uint32_t> &mask, bool partners,
+                                        int32_t *n_first)
+{
+    const jac::SweepArgs a0 = sweep_args(c, 0, jac::MODE_NOEXCHANGE);
+    const jac::TileShape ts = jac::tma_tile_shape(c->variant);
+    const bool two_d = (c->flags & JAC_F_2D) != 0;
+    std::vector<jac::TileItem> items(c->nitems);
+    std::vector<char> cls(c->nitems, 2);
+    for (int32_t it = 0; it < c->nitems; ++it) {
+        items[it] = two_d ? jac::decode_item2d(a0, it, ts.bx, ts.by) : jac::decode_item3d(a0, it, ts.bx, ts.by);
+        if (jac::item_touches(a0, items[it], mask[items[it].b], ts.bx, ts.by, two_d)) cls[it] = 0;
+    }
+    if (partners && !two_d) {
+        auto key = [](int64_t b, int64_t x0, int64_t y0, int64_t z) {
+            return (uint64_t)((b << 48) | (x0 << 32) | (y0 << 16) | z);
+        };
+        std::unordered_map<uint64_t, int32_t> by_start, by_end;
+        for (int32_t it = 0; it < c->nitems; ++it) {
+            const jac::TileItem &t = items[it];
+            by_start[key(t.b, t.x0, t.y0, t.zs)] = it;
+            by_end[key(t.b, t.x0, t.y0, t.ze)] = it;
+        }
+        auto mark = [&](std::unordered_map<uint64_t, int32_t> &m, uint64_t k) {
+            auto f = m.find(k);
+            if (f != m.end() && cls[f->second] == 2) cls[f->second] = 1;
+        };
+        for (int32_t it = 0; it < c->nitems; ++it) {
+            if (cls[it] != 0) continue;
+            const jac::TileItem &t = items[it];
+            mark(by_start, key(t.b, t.x0, t.y0, t.ze));  // z+ neighbour chunk
+            mark(by_end, key(t.b, t.x0, t.y0, t.zs));    // z- neighbour chunk
+            if (t.x0 >= ts.bx) mark(by_start, key(t.b, t.x0 - ts.bx, t.y0, t.zs));
+            mark(by_start, key(t.b, t.x0 + ts.bx, t.y0, t.zs));
+            if (t.y0 >= ts.by) mark(by_start, key(t.b, t.x0, t.y0 - ts.by, t.zs));
+            mark(by_start, key(t.b, t.x0, t.y0 + ts.by, t.zs));
+        }
+    }
+    std::vector<int32_t> order;
+    order.reserve(c->nitems);
+    for (char k = 0; k < 3; ++k)
+        for (int32_t it = 0; it < c->nitems; ++it)
+            if (cls[it] == k) order.push_back(it);
+    *n_first = (int32_t)std::count(cls.begin(), cls.end(), (char)0);
+    return order;
+}
+
 int create_common(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, int32_t bz,
                   int32_t n_gpus, const int32_t *gpu_grid, bool rank_mode, int32_t rank,
                   int32_t device, uint32_t flags, jac_ctx **out)
@@ -648,23 +700,26 @@ int create_common(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, in
     if ((rc = autotune(c))) return bail(rc);  // fixes the variant: the item map depends on it
     c->fused = rank_mode && !c->peer_ranks.empty() && sweep_mode(c) == jac::MODE_FUSED && c->variant != kPlain &&
                !(flags & JAC_F_NCCL) && !getenv("JAC_NO_FUSED_SYNC");
-    if (c->fused) {
-        const jac::SweepArgs a0 = sweep_args(c, 0, jac::MODE_NOEXCHANGE);
-        const jac::TileShape ts = jac::tma_tile_shape(c->variant);
-        const bool two_d = (flags & JAC_F_2D) != 0;
-        std::vector<int32_t> first, last;
-        for (int32_t it = 0; it < c->nitems; ++it) {
-            const jac::TileItem t = two_d ? jac::decode_item2d(a0, it, ts.bx, ts.by) : jac::decode_item3d(a0, it, ts.bx, ts.by);
-            (jac::item_touches(a0, t, c->hblocks[t.b].remote_mask, ts.bx, ts.by, two_d) ? last : first).push_back(it);
-        }
+    // experiment knob (single-GPU contexts): the remote-first launch order of a rank
+    // whose z- and y- faces were remote, without any sync -- isolates the cost of the
+    // order itself.  1 = remote-first, 2 = remote-first + halo partners.
+    const int order_exp = (!rank_mode && getenv("JAC_ORDER_EXP")) ? atoi(getenv("JAC_ORDER_EXP")) : 0;
+    if (c->fused || (order_exp && c->variant != kPlain)) {
+        std::vector<uint32_t> mask(c->nslots);
+        for (int32_t sl = 0; sl < c->nslots; ++sl)
+            mask[sl] = c->fused ? c->hblocks[sl].remote_mask
+                                : (((c->hblocks[sl].org[2] == 0) ? 1u << jac::ZM : 0u) |
+                                   ((c->hblocks[sl].org[1] == 0) ? 1u << jac::YM : 0u));
         // remote-touching items first: their signal leaves early in the sweep, so the
         // next sweep's remote items (which wait for it) find it already set
-        c->nremote = (int32_t)last.size();
-        last.insert(last.end(), first.begin(), first.end());
-        if (cudaMalloc(&c->ditem_map, sizeof(int32_t) * last.size()) != cudaSuccess ||
-            cudaMemcpy(c->ditem_map, last.data(), sizeof(int32_t) * last.size(), cudaMemcpyHostToDevice) != cudaSuccess)
+        int32_t nfirst = 0;
+        const std::vector<int32_t> order =
+            remote_first_order(c, mask, order_exp == 2, &nfirst);
+        if (c->fused) c->nremote = nfirst;
+        if (cudaMalloc(&c->ditem_map, sizeof(int32_t) * order.size()) != cudaSuccess ||
+            cudaMemcpy(c->ditem_map, order.data(), sizeof(int32_t) * order.size(), cudaMemcpyHostToDevice) != cudaSuccess)
             return bail(fail(JAC_ENOMEM, "item map"));
-        if (c->nremote == 0) c->fused = false;
+        if (c->fused && c->nremote == 0) c->fused = false;
     }
     // barrier args (peer slots filled at import)
     c->bar.ctrl = c->ctrl;

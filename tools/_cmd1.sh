@@ -1,2 +1,2 @@
-F=gpurun_out/w8; mkdir -p $F
-VARS=0,5,15 BLOCKS=1x1x1,2x2x2,2x2x4,4x4x4 timeout 600 python tools/var_probe.py > $F/probe.log 2>&1
+F=gpurun_out/order; mkdir -p $F
+KNOB=JAC_ORDER_EXP VALUES=0,1,2 BLOCKS=2x2x2,2x2x4 timeout 600 python tools/env_probe.py > $F/probe.log 2>&1
