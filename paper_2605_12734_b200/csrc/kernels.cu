@@ -57,6 +57,13 @@ __device__ __forceinline__ void st_pair(double *p, double2 v, bool both)
     else p[0] = v.x;
 }
 
+// Does face f of `blk` have a store target in this sweep's mode (neighbour ghosts of
+// output buffer dst in the fused mode, the outbox in the pack mode)?
+__device__ __forceinline__ bool has_target(const SweepArgs &a, const DevBlock &blk, int dst, int f)
+{
+    return (a.mode == MODE_FUSED ? blk.nb[f][dst] : blk.nb[f][0]) != nullptr;
+}
+
 // Stores the new values of points (i, j, k) and (i+1, j, k) of block `blk` into the
 // output buffer `dst` (own_plane = the block's output array + (k+1)*Q, rowoff =
 // (j+1)*P + A + i), plus the face traffic of the chosen mode.  Caller guarantees
@@ -404,7 +411,7 @@ __global__ void __launch_bounds__(NT, min_ctas_per_sm(NT, NS))
     for (int r = 0; r < RY; ++r) c[r] = *reinterpret_cast<const double2 *>(plane(1) + sb + r * W);
 
     // One z-plane of the march: wait for plane q+1, update centre plane q (k), store.
-    auto update = [&](int q, double2 (&v)[RY], bool full) {
+    auto update = [&](int q, double2 (&v)[RY]) {
         wait(q + 1);
         const double *Sn = plane(q + 1);
 #pragma unroll
@@ -414,7 +421,7 @@ __global__ void __launch_bounds__(NT, min_ctas_per_sm(NT, NS))
         for (int r = 0; r < RY; ++r) {
             const double xm = ilo ? S[xg + r] : S[sb + r * W - 1];
             const double xp1 = ihi1 ? S[xg + BY + r] : S[sb + r * W + 2];
-            const double xp0 = (!full && ihi0) ? S[xg + BY + r] : c[r].y;  // full tiles: never
+            const double xp0 = ihi0 ? S[xg + BY + r] : c[r].y;
             const double2 ym = (r == 0) ? *reinterpret_cast<const double2 *>(S + sb - W) : c[r - 1];
             const double2 yp = (r == RY - 1) ? *reinterpret_cast<const double2 *>(S + sb + RY * W) : c[r + 1];
             v[r].x = stencil7(c[r].x, xm, xp0, ym.x, yp.x, zm[r].x, zp[r].x);
@@ -431,7 +438,7 @@ __global__ void __launch_bounds__(NT, min_ctas_per_sm(NT, NS))
     auto plane_general = [&](int q) {
         const int k = t.zs - 1 + q;
         double2 v[RY];
-        update(q, v, false);
+        update(q, v);
         double *const own_k = own + (int64_t)(k + 1) * g.Q;
 #pragma unroll
         for (int r = 0; r < RY; ++r) {
@@ -459,7 +466,7 @@ __global__ void __launch_bounds__(NT, min_ctas_per_sm(NT, NS))
     const int qlean_end = (exch && t.ze == g.ez) ? qlast - 1 : qlast;
     if (lean && q <= qlean_end) {
         // edge instantiation: x-ghost lanes, or a y-face row with a target
-        auto has = [&](int f) { return (a.mode == MODE_FUSED ? blk.nb[f][dst] : blk.nb[f][0]) != nullptr; };
+        auto has = [&](int f) { return has_target(a, blk, dst, f); };
         const bool edge = (t.x0 == 0) || (t.x0 + BX >= g.ex) ||
                           (exch && ((t.y0 == 0 && has(YM)) || (t.y0 + BY >= g.ey && has(YP))));
         double *xf = nullptr;  // x-face target of this lane (row 0 of the thread, plane q)
@@ -641,7 +648,7 @@ __global__ void __launch_bounds__(NT, 4) sweep2d_tma_kernel(const __grid_constan
     // store per pair (+ the x-face value on x-edge lanes), rows shared between a
     // thread's RY rows instead of reloaded.  Other tiles take emit_pair.
     const bool exch = (a.mode != MODE_NOEXCHANGE);
-    auto has = [&](int f) { return (a.mode == MODE_FUSED ? blk.nb[f][dst] : blk.nb[f][0]) != nullptr; };
+    auto has = [&](int f) { return has_target(a, blk, dst, f); };
     const bool xfull = (x0 + BX <= g.ex) && g.ex > 2;
     const bool xedge = xlo || xhi;
     const bool ym_face = exch && has(YM), yp_face = exch && has(YP);  // loop-invariant
