@@ -968,6 +968,10 @@ static int resident_tma_t()
     static int resident = 0;  // SMs x CTAs per SM (per process; one device per process)
     if (!resident) {
         constexpr size_t smem = tma_smem_bytes(BX, BY, W, NS);
+        // the occupancy query needs the kernel's dynamic shared-memory limit raised
+        // first (above 48 KB it would report 0 CTAs per SM)
+        cudaFuncSetAttribute(sweep_tma_kernel<BX, BY, W, NT, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
         int dev = 0, sms = 0, per_sm = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
