@@ -1,3 +1,6 @@
-F=gpurun_out/resid; mkdir -p $F
-timeout 1500 python -m pytest tests/test_parity_gpu.py tests/test_parity_fuzz_gpu.py tests/test_fullsize_gpu.py -m gpu -q 2>&1 | tail -2 > $F/pytest.log
-CASES=64x64x64:2x2x2,128x128x128:2x2x2,512x512x512:1x1x1,512x512x512:2x2x2,512x512x512:2x2x4,512x512x512:4x4x4,512x512x512:8x8x8,512x512x512:16x16x16,768x768x768:2x2x2 REPS=2 timeout 1500 python tools/ab_probe.py > $F/ab.log 2>&1
+F=gpurun_out/ncu2; mkdir -p $F
+python tools/profile_sweep.py --blocks 16 16 16 --iters 3 > $F/pre.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:sweep -c 1 -o $F/r01b_sweep_blocks161616 -f python tools/profile_sweep.py --blocks 16 16 16 --iters 2 > /dev/null 2>&1
+python tools/profile_sweep.py --dims 32768 32768 1 --blocks 2 4 1 --flags 512 --iters 3 >> $F/pre.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:sweep -c 1 -o $F/r01b_sweep2d_32768sq_odf8 -f python tools/profile_sweep.py --dims 32768 32768 1 --blocks 2 4 1 --flags 512 --iters 2 > /dev/null 2>&1
+ls $F >> $F/pre.log
