@@ -33,9 +33,26 @@ def _inputs():
     return files
 
 
+STAMP = LIB + ".stamp"  # sha256 of the inputs + flags the .so was built from
+
+
+def _digest() -> str:
+    import hashlib
+    h = hashlib.sha256(" ".join(NVCC_FLAGS).encode())
+    for f in _inputs():
+        with open(f, "rb") as fh:
+            h.update(os.path.basename(f).encode() + b"\0" + fh.read())
+    return h.hexdigest()
+
+
 def needs_build() -> bool:
+    """Content-based: a copied tree (new mtimes, e.g. the gpurun snapshot) reuses a
+    .so built from the same sources; without a stamp, fall back to mtimes."""
     if not os.path.exists(LIB):
         return True
+    if os.path.exists(STAMP):
+        with open(STAMP) as fh:
+            return fh.read().strip() != _digest()
     t = os.path.getmtime(LIB)
     return any(os.path.getmtime(f) > t for f in _inputs())
 
@@ -49,8 +66,12 @@ def build(force: bool = False, verbose: bool = False) -> str:
            *[os.path.join(CSRC, s) for s in SOURCES]]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
+    digest = _digest()
     subprocess.check_call(cmd)
     os.replace(tmp, LIB)
+    with open(STAMP + f".tmp{os.getpid()}", "w") as fh:
+        fh.write(digest + "\n")
+    os.replace(STAMP + f".tmp{os.getpid()}", STAMP)
     return LIB
 
 
