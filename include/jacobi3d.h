@@ -209,15 +209,16 @@ int jac_block_owner(const jac_ctx *c, int32_t ix, int32_t iy, int32_t iz, int32_
 /* Device time of the last jac_step (CUDA events recorded on the launching
  * stream(s) around its launches; max over this context's devices), in ms. */
 int jac_last_step_ms(const jac_ctx *c, double *ms);
-/* Runs n_iters iterations as one captured graph with CUDA event-record nodes around
- * every sweep-kernel launch (same stream, same kernels as jac_step); returns the
- * median sweep-kernel duration in ms (the roofline's per-launch figure).  Advances
- * the state like jac_step. */
+/* Runs n_iters iterations as one captured graph (same stream, same kernels and launch
+ * attributes as jac_step); returns the median sweep-kernel duration in ms (the
+ * roofline's per-launch figure): each TMA sweep records its span on the device clock
+ * (first CTA start after the dependency wait, last CTA end); the plain-load ablation
+ * kernel is bracketed by CUDA event-record nodes.  Advances the state like jac_step. */
 int jac_profile_sweep(jac_ctx *c, int32_t n_iters, double *avg_sweep_ms);
 /* Median device-time gap, in ms, between the end of one sweep launch and the start
  * of the next inside the last jac_profile_sweep graph (n_iters >= 2): the per-
  * iteration launch / dependency cost of the graph-replayed iteration (in the fused
- * mode nothing else runs between sweeps; the event-record nodes are included).
+ * mode nothing else runs between sweeps).
  * JAC_ESTATE before such a profile.  The launch/sync-gap evidence SURVEY.md §8(d.1)
  * asks of an nsys timeline, on the device clock. */
 int jac_last_profile_gap_ms(const jac_ctx *c, double *gap_ms);

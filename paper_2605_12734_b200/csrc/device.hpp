@@ -98,6 +98,9 @@ struct SweepArgs {
     int32_t fused_sync;
     int32_t nremote;         // items touching a remote face (the first nremote of item_map)
     int32_t pad2_;
+    // jac_profile_sweep: when set, every CTA atomicMin's %globaltimer into span[0] after
+    // the dependency wait and atomicMax's it into span[1] when done (ns)
+    unsigned long long *span;
 };
 
 struct TileItem {

@@ -152,6 +152,8 @@ struct jac_ctx {
     int nzc = 1, ncols = 1, nitems = 1, gcols = 1;
     float tuned_ms[2] = {0.f, 0.f};  // autotune: sweep ms for the 6- and 4-stage wide tiles
     double last_gap_ms = -1.0;       // jac_profile_sweep: median gap between consecutive sweeps
+    unsigned long long *prof_span = nullptr;  // jac_profile_sweep capture: per-iteration [start, end]
+    int prof_it = 0;
     bool pdl = true;                 // sweeps use programmatic dependent launch (JAC_PDL=0: off)
 
     // cross-rank exchange
@@ -224,6 +226,7 @@ jac::SweepArgs sweep_args(const jac_ctx *c, int src, int mode)
     a.ntx = c->ntx; a.nty = c->nty; a.ntz = c->ntz; a.zc = c->zc;
     a.nzc = c->nzc; a.ncols = c->ncols; a.nitems = c->nitems; a.gcols = c->gcols;
     if (c->ditem_map && !c->fused) a.item_map = c->ditem_map;  // JAC_ORDER_EXP
+    if (c->prof_span) a.span = c->prof_span + 2 * (int64_t)c->prof_it;
     if (c->fused && mode == jac::MODE_FUSED) {
         a.fused_sync = 1;
         a.nremote = c->nremote;
@@ -1166,18 +1169,38 @@ int jac_profile_sweep(jac_ctx *c, int32_t n, double *avg_ms)
         std::vector<cudaEvent_t> v;
         ~Events() { for (cudaEvent_t e : v) if (e) cudaEventDestroy(e); }
     } evs;
-    evs.v.assign(2 * (size_t)n, nullptr);
+    // TMA sweeps time themselves (first CTA start after the dependency wait, last CTA
+    // end, %globaltimer) so the profile graph keeps the programmatic-dependent-launch
+    // overlap of jac_step; the plain-load kernel is bracketed by event-record nodes.
+    const bool use_span = c->variant != kPlain;
+    struct Span {  // freed on every return path
+        unsigned long long *d = nullptr;
+        jac_ctx *c;
+        ~Span() { if (d) cudaFree(d); c->prof_span = nullptr; }
+    } span{nullptr, c};
+    std::vector<unsigned long long> hspan(2 * (size_t)n);
+    for (int it = 0; it < n; ++it) { hspan[2 * it] = ~0ull; hspan[2 * it + 1] = 0ull; }
+    if (use_span) {
+        CK(cudaMalloc(&span.d, sizeof(unsigned long long) * hspan.size()));
+        CK(cudaMemcpy(span.d, hspan.data(), sizeof(unsigned long long) * hspan.size(), cudaMemcpyHostToDevice));
+    } else {
+        evs.v.assign(2 * (size_t)n, nullptr);
+        for (auto &e : evs.v) CK(cudaEventCreate(&e));
+    }
     std::vector<cudaEvent_t> &ev = evs.v;
-    for (auto &e : ev) CK(cudaEventCreate(&e));
     int src = (int)(c->iters & 1);
-    // The n iterations are captured into one graph with event-record nodes around
-    // every sweep launch, so the sweep is timed exactly as jac_step runs it.
+    // The n iterations are captured into one graph, so the sweep is timed exactly as
+    // jac_step runs it.
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
     CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
     rc = JAC_OK;
-    for (int it = 0; it < n && rc == JAC_OK; ++it, src ^= 1)
-        rc = enqueue_iteration(c, src, ev[2 * it], ev[2 * it + 1]);
+    c->prof_span = span.d;
+    for (int it = 0; it < n && rc == JAC_OK; ++it, src ^= 1) {
+        c->prof_it = it;
+        rc = use_span ? enqueue_iteration(c, src) : enqueue_iteration(c, src, ev[2 * it], ev[2 * it + 1]);
+    }
+    c->prof_span = nullptr;
     cudaError_t e = cudaStreamEndCapture(c->stream, &graph);
     if (rc) { if (graph) cudaGraphDestroy(graph); return rc; }
     if (e != cudaSuccess) return fail(JAC_ECUDA, "profile graph capture: %s", cudaGetErrorString(e));
@@ -1189,11 +1212,18 @@ int jac_profile_sweep(jac_ctx *c, int32_t n, double *avg_ms)
     cudaGraphExecDestroy(exec);
     if (e != cudaSuccess) return fail(JAC_ECUDA, "profile graph: %s", cudaGetErrorString(e));
     std::vector<float> dur(n), gap(n > 1 ? n - 1 : 0);
-    for (int it = 0; it < n; ++it) CK(cudaEventElapsedTime(&dur[it], ev[2 * it], ev[2 * it + 1]));
+    if (use_span) {
+        CK(cudaMemcpy(hspan.data(), span.d, sizeof(unsigned long long) * hspan.size(), cudaMemcpyDeviceToHost));
+        for (int it = 0; it < n; ++it) dur[it] = (float)((double)(hspan[2 * it + 1] - hspan[2 * it]) * 1e-6);
+        for (int it = 0; it + 1 < n; ++it)
+            gap[it] = (float)(((double)hspan[2 * it + 2] - (double)hspan[2 * it + 1]) * 1e-6);
+    } else {
+        for (int it = 0; it < n; ++it) CK(cudaEventElapsedTime(&dur[it], ev[2 * it], ev[2 * it + 1]));
+        for (int it = 0; it + 1 < n; ++it) CK(cudaEventElapsedTime(&gap[it], ev[2 * it + 1], ev[2 * it + 2]));
+    }
     // end of sweep i -> start of sweep i+1: the graph's launch / dependency gap
     // (plus whatever the iteration enqueues after the sweep: nothing in the fused
     // mode; the ghost-fill kernel / NCCL calls in the ablation modes)
-    for (int it = 0; it + 1 < n; ++it) CK(cudaEventElapsedTime(&gap[it], ev[2 * it + 1], ev[2 * it + 2]));
     if (!gap.empty()) {
         std::sort(gap.begin(), gap.end());
         const size_t m = gap.size();

@@ -169,6 +169,29 @@ __device__ __forceinline__ void pdl_launch_dependents_then_wait()
     asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
+// Kernel span on the device clock for jac_profile_sweep (a.span set): first CTA start
+// after the dependency wait, last CTA end -- under programmatic dependent launch,
+// where event-record nodes between sweeps would break the launch overlap.
+__device__ __forceinline__ void span_begin(unsigned long long *span)
+{
+    if (span && threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        atomicMin(&span[0], t);
+    }
+}
+__device__ __forceinline__ void span_end(unsigned long long *span)
+{
+    if (span) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            atomicMax(&span[1], t);
+        }
+    }
+}
+
 // ------------------------------------------------------------------ TMA / mbarrier
 __device__ __forceinline__ uint32_t smem_u32(const void *p)
 {
@@ -342,6 +365,7 @@ __global__ void __launch_bounds__(NT, min_ctas_per_sm(NT, NS))
     __shared__ DevBlock blk;  // this item's descriptor, read once from the table
     if (threadIdx.x == 0) blk = a.blocks[t.b];
     pdl_launch_dependents_then_wait();
+    span_begin(a.span);
     const int soff = tile_soff<BX, W>(g, t.x0);  // staged column of point i = x0 (0, 2 or 4)
     const int c0 = g.A + t.x0 - soff;
     const bool xlo = (t.x0 == 0);                 // tile touches the x- block face
@@ -568,6 +592,7 @@ __global__ void __launch_bounds__(NT, min_ctas_per_sm(NT, NS))
     }
     if (q <= qlast) plane_general(q);  // z+ face plane
     if (remote) signal_done(a);
+    span_end(a.span);
 }
 
 // ------------------------------------------------------------------ Jacobi2D sweep
@@ -610,6 +635,7 @@ __global__ void __launch_bounds__(NT, 4) sweep2d_tma_kernel(const __grid_constan
     __shared__ DevBlock blk;
     if (threadIdx.x == 0) blk = a.blocks[b];
     pdl_launch_dependents_then_wait();
+    span_begin(a.span);
     const int soff = tile_soff<BX, W>(g, x0);
     const int c0 = g.A + x0 - soff;
     const bool xlo = (x0 == 0), xhi = (x0 + BX >= g.ex);
@@ -736,6 +762,7 @@ __global__ void __launch_bounds__(NT, 4) sweep2d_tma_kernel(const __grid_constan
     }
     if (q < nq) tile_general(q);
     if (remote) signal_done(a);
+    span_end(a.span);
 }
 
 // ------------------------------------------------------------------ plain sweep

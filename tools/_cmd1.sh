@@ -1,6 +1,5 @@
-F=gpurun_out/ncu2; mkdir -p $F
-python tools/profile_sweep.py --blocks 16 16 16 --iters 3 > $F/pre.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:sweep -c 1 -o $F/r01b_sweep_blocks161616 -f python tools/profile_sweep.py --blocks 16 16 16 --iters 2 > /dev/null 2>&1
-python tools/profile_sweep.py --dims 32768 32768 1 --blocks 2 4 1 --flags 512 --iters 3 >> $F/pre.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:sweep -c 1 -o $F/r01b_sweep2d_32768sq_odf8 -f python tools/profile_sweep.py --dims 32768 32768 1 --blocks 2 4 1 --flags 512 --iters 2 > /dev/null 2>&1
-ls $F >> $F/pre.log
+F=gpurun_out/span; mkdir -p $F
+timeout 1500 python -m pytest tests/test_abi_errors_gpu.py tests/test_parity_gpu.py tests/test_parity2d_gpu.py -m gpu -q 2>&1 | tail -2 > $F/pytest.log
+python bench.py --no-cpu --no-e2e --no-sustained > $F/bench.json 2> $F/bench.err
+python bench.py --config j2d --no-cpu --no-e2e --no-sustained --no-sweep > $F/bench_j2d.json 2> $F/bench_j2d.err
+for b in "1 1 1" "2 2 2"; do python tools/profile_sweep.py --blocks $b --iters 20 >> $F/pytest.log 2>&1; done
