@@ -44,6 +44,22 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 MODE_2D = [False]  # set for --config j2d
+_JSON_OUT = [None]  # the process's original stdout: the JSON line goes there, nothing else
+
+
+def quiet_stdout():
+    """Keep stdout for the one JSON line: duplicate fd 1 for it, then point fd 1 (C and
+    Python writes alike, e.g. NCCL's version banner) at stderr."""
+    if _JSON_OUT[0] is None:
+        sys.stdout.flush()
+        _JSON_OUT[0] = os.fdopen(os.dup(1), "w")
+        os.dup2(2, 1)
+
+
+def emit(line):
+    out = _JSON_OUT[0] or sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
 EXTRA = {}  # additional keys of our JSON line
 BYTES_PER_LUP = 16  # algorithmic HBM bytes per lattice update: 8 B read + 8 B write (SURVEY §8(d.3))
 FLOPS_PER_LUP = 7
@@ -325,7 +341,7 @@ def run_reference(args, D):
             "cpu_baseline": {"kind": "oracle", "cores": cb["cores"], "sample": cb["sample"], "value": cb["value"],
                              "unit": "GLUP/s"},
             "e2e": {"value": cb["value"], "unit": "GLUP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit(line)
     D.finish()
 
 
@@ -602,7 +618,7 @@ def finish_ours(args, D, K, W, dims, blocks, g, label, scaling, pts, pts_gpu, pe
         if nccl_ablation is not None:
             line["exchange_ablations"] = nccl_ablation
         line.update(EXTRA)
-        print(json.dumps(line), flush=True)
+        emit(line)
     D.finish()
 
 
@@ -620,6 +636,7 @@ def main():
     ap.add_argument("--no-sustained", action="store_true", help="skip the ~2 s power-capped steady-state leg")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     args = ap.parse_args()
+    quiet_stdout()
     D = Dist()
     if D.world != args.gpus:
         if D.world > 1:
