@@ -982,6 +982,14 @@ __global__ void hash_init_kernel(const SweepArgs a, int64_t nx, int64_t ny, uint
         const uint64_t px = blk.org[0] + ii, py = blk.org[1] + jj, pz = blk.org[2] + kk;
         const uint64_t p = (pz * (uint64_t)(ny + 2) + py) * (uint64_t)(nx + 2) + px;
         const double v = r11_value(seed, p);
+        if (g.A == 0 && (ii == 0 || ii == sx - 1)) {  // dense rows: x ghosts -> x-ghost arrays
+            if (jj >= 1 && jj <= g.ey && kk >= g.zg && kk < g.ez + g.zg) {
+                const int64_t xi = (kk - g.zg) * g.eyp + (jj - 1);
+                xg_array(a.xg, g, 0, blk.slot, ii ? 1 : 0)[xi] = v;
+                xg_array(a.xg, g, 1, blk.slot, ii ? 1 : 0)[xi] = v;
+            }
+            continue;
+        }
         const int64_t off = kk * g.Q + jj * g.P + (g.A - 1) + ii;
         b0[off] = v;
         b1[off] = v;

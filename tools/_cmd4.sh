@@ -1,4 +1,3 @@
-F=gpurun_out/driverlike2; mkdir -p $F
-python bench.py --gpus 1 --steps 20 --warmup 3 --no-sweep > $F/n1.json 2> $F/n1.err; echo "n1 rc=$?" >> $F/rc.log
-python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29611 bench.py --gpus 2 --steps 20 --warmup 3 > $F/n2.json 2> $F/n2.err; echo "n2 rc=$?" >> $F/rc.log
-python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29612 bench.py --impl reference --gpus 2 --steps 2 --warmup 3 > $F/ref2.json 2> $F/ref2.err; echo "ref2 rc=$?" >> $F/rc.log
+F=gpurun_out/densefull; mkdir -p $F
+timeout 2400 python -m pytest tests -m gpu -q 2>&1 | tail -8 > $F/pytest_gpu.log
+CUDA_VISIBLE_DEVICES=0 CASES=64x64x64:2x2x2,512x512x512:16x16x16,512x512x512:8x8x8,512x512x512:2x2x2,1024x1024x1024:32x32x32 REPS=2 timeout 1200 python tools/ab_probe.py > $F/ab.log 2>&1
