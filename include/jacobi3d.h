@@ -186,8 +186,8 @@ int jac_step(jac_ctx *c, int32_t n_iters);
  * into caller-owned host `out`.  The block must be local to this context. */
 int jac_get_block(jac_ctx *c, int32_t ix, int32_t iy, int32_t iz, double *out);
 /* Debug (pin P11): the whole ghosted block of the current buffer,
- * (ex+2)*(ey+2)*(ez+2) doubles, x fastest.  In the dense narrow-block layout (3-D,
- * ex <= 64, ex % 8 == 0) the x-edge cells of the ghost rows and planes (x ghost
+ * (ex+2)*(ey+2)*(ez+2) doubles, x fastest.  In the dense row layout (3-D blocks with
+ * ex % 8 == 0) the x-edge cells of the ghost rows and planes (x ghost
  * column with a y or z ghost index) are not stored -- the stencil never reads them --
  * and are returned as NaN. */
 int jac_get_block_padded(jac_ctx *c, int32_t ix, int32_t iy, int32_t iz, double *out);

@@ -571,12 +571,14 @@ int create_common(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, in
     int palign = narrow ? 8 : 4;
     if (const char *s = getenv("JAC_PALIGN")) palign = std::max(4, atoi(s) & ~3);  // layout experiment knob
     g.P = round_up(g.A + g.ex + 4, palign);  // room for the 32-byte +x ghost sector (A % 4 == 0)
-    // Dense narrow rows (3-D, ex <= 64, ex % 8 == 0): no padding and no inline ghost
-    // columns at all -- A = 0, P = ex -- so a block's rows are back to back and the
+    // Dense rows (3-D, ex % 8 == 0): no padding and no inline ghost columns at all --
+    // A = 0, P = ex -- so a block's rows are back to back, 64-byte aligned, and the
     // staged boxes are contiguous DRAM runs.  The x ghosts live in the x-ghost arrays
-    // anyway; init fills them directly (jac_set_init_box, hash_init_kernel).  512^3 in
-    // 32^3 blocks: 441.6 -> 411.4 us per sweep.  JAC_NO_DENSE=1 keeps the padded rows.
-    if (!(flags & JAC_F_2D) && g.ex <= 64 && g.ex % 8 == 0 && !getenv("JAC_NO_DENSE")) {
+    // anyway; init fills them directly (jac_set_init_box, hash_init_kernel).  Same-box
+    // A/B per sweep: 512^3 in 32^3 blocks 441.6 -> 411.4 us; ODF 1 336 -> 330 us;
+    // ODF 8 -2%; ODF 64 365 -> 350 us; 1536^3 ODF 16 -2.6..4.7%.  JAC_NO_DENSE=1 keeps
+    // the padded rows.
+    if (!(flags & JAC_F_2D) && g.ex % 8 == 0 && !getenv("JAC_NO_DENSE")) {
         g.A = 0;
         g.P = g.ex;
     }
