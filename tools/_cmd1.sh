@@ -1,4 +1,2 @@
-F=gpurun_out/lastcheck; mkdir -p $F
-python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > $F/smoke.log 2>&1; echo "smoke rc=$?" >> $F/rc.log
-python bench.py > $F/bench.json 2> $F/bench.err; echo "bench rc=$?" >> $F/rc.log
-python bench.py --impl reference > $F/ref.json 2> $F/ref.err; echo "ref rc=$?" >> $F/rc.log
+F=gpurun_out/layouts; mkdir -p $F
+timeout 900 python -m pytest tests/test_layouts_gpu.py -m gpu -q 2>&1 | tail -15 > $F/pytest.log
