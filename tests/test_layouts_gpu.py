@@ -56,3 +56,26 @@ def test_block_padded_corners():
     assert _bits_equal(xcols, want[1:-1, 1:-1, [0, -1]])
     corners = np.concatenate([b[[0, -1], :, :][:, :, [0, -1]].ravel(), b[:, [0, -1], :][:, :, [0, -1]].ravel()])
     assert np.isnan(corners).all()
+
+
+@pytest.mark.parametrize("pdl", ["0", "1"])
+@pytest.mark.parametrize("dims,blocks,flags", [((64, 64, 64), (2, 2, 2), 0), ((128, 128, 128), (2, 2, 4), 0),
+                                               ((256, 192, 1), (2, 2, 1), 1 << 9)])
+def test_programmatic_dependent_launch_on_off(monkeypatch, pdl, dims, blocks, flags):
+    """Sweeps with and without programmatic dependent launch (JAC_PDL) give the same
+    bits: every CTA waits on griddepcontrol before touching a buffer."""
+    monkeypatch.setenv("JAC_PDL", pdl)
+    if flags:
+        u0 = JI.hash_field2d(dims[0], dims[1], seed=3)
+        with jb.Jacobi2D(dims[:2], blocks[:2]) as s:
+            s.set_init(u0)
+            s.step(9)
+            got = s.field(u0)
+        assert _bits_equal(got, oracle.jacobi2d(u0, 9))
+        return
+    u0 = JI.hash_field(*dims, seed=3)
+    with jb.Jacobi3D(dims, blocks) as s:
+        s.set_init(u0)
+        s.step(9)
+        got = s.field(u0)
+    assert _bits_equal(got, oracle.jacobi3d(u0, 9))
