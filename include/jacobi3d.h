@@ -66,14 +66,24 @@ enum jac_flags {
                                      sweep packs REMOTE faces into send buffers, grouped
                                      ncclSend / ncclRecv move them (one per face), the
                                      batched ghost kernel unpacks (north-star subsystem 4,
-                                     "NCCL send/recv").  Bootstrap with jac_nccl_* below. */
+                                     "NCCL send/recv").  Bootstrap with jac_nccl_* below.
+                                     With JAC_F_VIRTUAL_GPUS: the same packed layout, moved
+                                     by an on-device copy kernel standing in for NCCL. */
     JAC_F_UNFUSED_PACK = 1u << 4, /* north-star layout: the sweep packs faces into an
                                      outbox and a separate batched ghost-copy kernel
                                      fills the ghosts (PAPER.md:90 pack/unpack kernels) */
     JAC_F_NO_TMA = 1u << 5,       /* plain per-point global-load sweep (no TMA staging) */
-    JAC_F_VIRTUAL_GPUS = 1u << 6, /* test-only: all n_gpus partitions live on device 0 and
-                                     are swept by ONE kernel (no cross-partition waits);
-                                     exercises the partition / REMOTE-face logic */
+    JAC_F_VIRTUAL_GPUS = 1u << 6, /* test-only: all n_gpus partitions live on device 0 in one
+                                     context and are swept by ONE kernel per iteration, but
+                                     faces between partitions take the REMOTE path of a
+                                     multi-GPU run: per-partition remote masks, the
+                                     remote-first item order, per-partition epoch / flag /
+                                     count words with the in-sweep wait and signal, the
+                                     barrier kernel, and (with JAC_F_NCCL) packed send /
+                                     receive buffers.  Inside one kernel the previous sweep
+                                     has completed, so the waits are satisfied on entry (they
+                                     check the epoch bookkeeping, not timing): kernels that
+                                     wait on one another never share a GPU. */
     JAC_F_SKIP_EXCHANGE = 1u << 7, /* timing-only ablation: no face writes. WRONG results */
     JAC_F_PER_BLOCK = 1u << 8,     /* paper-style execution: one stream per
                                       block ("non-blocking per-chare streams")
@@ -81,8 +91,8 @@ enum jac_flags {
                                       face, one stencil launch, one pack launch per face
                                       (SPEC.md:474), ordered by per-block events; no graph.
                                       Launching host threads (the paper's PEs per process,
-                                      PAPER.md:95) via jac_set_option.  One GPU only
-                                      (n_gpus == 1 or JAC_F_VIRTUAL_GPUS); 3-D or 2-D. */
+                                      PAPER.md:95) via jac_set_option.  One GPU, one
+                                      partition (n_gpus == 1); 3-D or 2-D. */
     JAC_F_2D = 1u << 9             /* Jacobi2D (the paper's evaluated app,
                                       PAPER.md:280-294): nz == 1, bz == 1; 5-point mean
                                       u' = ((((c + x-) + x+) + y-) + y+) * fl(1/5)
@@ -94,8 +104,15 @@ enum jac_flags {
 
 /* Options for jac_set_option. */
 enum jac_option {
-    JAC_OPT_LAUNCH_THREADS = 1 /* JAC_F_PER_BLOCK: host threads enqueueing the blocks'
+    JAC_OPT_LAUNCH_THREADS = 1, /* JAC_F_PER_BLOCK: host threads enqueueing the blocks'
                                   work (1..64, default 1); blocks are dealt round-robin */
+    JAC_OPT_WATCHDOG_MS = 2     /* cross-partition wait limit in ms (default 60000; 0 = wait
+                                  forever).  A sweep or barrier whose neighbour partition
+                                  has not signalled within the limit stops waiting, the
+                                  call returns JAC_ECUDA ("peer watchdog") and that call's
+                                  results are invalid; the CUDA context stays usable.  Rank
+                                  contexts: every rank starts its next collective call
+                                  within this limit of its neighbours. */
 };
 
 /* Face kinds of the block-descriptor table (the analog of the paper's pre-filled
@@ -120,10 +137,16 @@ int jac_plan_face(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, in
                   int32_t iz, int32_t f, int32_t *kind, int32_t *owner);
 
 /* ---------------------------------------------------------------- lifecycle
- * jac_create: one process drives all n_gpus partitions.  Partition g runs on CUDA
- * device g, or on device 0 for every g under JAC_F_VIRTUAL_GPUS.  Multi-device
- * single-process contexts are not supported this round (use jac_create_rank, one
- * process per GPU); n_gpus > 1 without JAC_F_VIRTUAL_GPUS returns JAC_EINVAL.
+ * jac_create: one process drives all n_gpus partitions.
+ * Partition g runs on CUDA device g: the context holds one sub-context per device,
+ * neighbour devices get peer access (cudaDeviceEnablePeerAccess) and faces to another
+ * GPU are stored into its ghost cells over NVLink by the sweep kernel, ordered by the
+ * device-flag handshake -- the same path as jac_create_rank, with plain peer pointers
+ * instead of IPC.  jac_step launches every device's iterations and returns after all
+ * devices finish; the other calls fan out to the devices.  JAC_EDEVICE if fewer than
+ * n_gpus devices are visible or two neighbour devices lack P2P access; JAC_EINVAL for
+ * JAC_F_NCCL / JAC_F_PER_BLOCK with n_gpus > 1 (rank contexts only).  Under
+ * JAC_F_VIRTUAL_GPUS every partition lives on device 0 (test mode, see the flag).
  * Allocates everything (two ghosted arrays per block, descriptor table, control
  * words, streams, events); nothing is allocated inside jac_step (PAPER.md:190-194
  * "persistent Views ... preallocated buffers"). *out receives the context. */
@@ -185,7 +208,11 @@ int jac_step(jac_ctx *c, int32_t n_iters);
 /* Interior of block (ix,iy,iz) after the sweeps so far, ex*ey*ez doubles, x fastest,
  * into caller-owned host `out`.  The block must be local to this context. */
 int jac_get_block(jac_ctx *c, int32_t ix, int32_t iy, int32_t iz, double *out);
-/* Debug (pin P11): the whole ghosted block of the current buffer,
+/* Debug (pin P11): the whole ghosted block of the current buffer.  Rank contexts: a
+ * neighbour rank may still be storing into this block's ghosts until every rank has
+ * returned from its jac_step -- call it after a collective barrier for valid ghosts
+ * (interiors are always valid).  Single-process contexts synchronise all devices in
+ * jac_step, so no barrier is needed.
  * (ex+2)*(ey+2)*(ez+2) doubles, x fastest.  In the dense row layout (3-D blocks with
  * ex % 8 == 0) the x-edge cells of the ghost rows and planes (x ghost
  * column with a y or z ghost index) are not stored -- the stencil never reads them --
@@ -206,6 +233,9 @@ int jac_get_region(jac_ctx *c, const int64_t *lo, const int64_t *ext, double *ou
 
 int jac_get_layout(const jac_ctx *c, int32_t *gpu_grid, int64_t *block_extent,
                    int64_t *iterations_done);
+/* The creation arguments: interior dims n[3] (x, y, z), global blocks[3] and flags
+ * (any pointer may be NULL).  Lets a caller size host arrays for a context it holds. */
+int jac_get_grid(const jac_ctx *c, int64_t *n, int32_t *blocks, uint32_t *flags);
 /* Partition (GPU) owning block (ix,iy,iz). */
 int jac_block_owner(const jac_ctx *c, int32_t ix, int32_t iy, int32_t iz, int32_t *gpu);
 
@@ -231,12 +261,19 @@ enum jac_stat {
     JAC_STAT_GRAPH_LAUNCHES = 1,
     JAC_STAT_KERNELS_PER_ITER = 2,
     JAC_STAT_LOCAL_BLOCKS = 3,
-    JAC_STAT_LOCAL_FACES = 4,     /* exchanged LOCAL faces per iteration */
-    JAC_STAT_REMOTE_FACES = 5,    /* exchanged REMOTE faces per iteration */
-    JAC_STAT_REMOTE_BYTES = 6,    /* bytes stored to peers per iteration */
+    JAC_STAT_LOCAL_FACES = 4,     /* exchanged faces inside a partition per iteration */
+    JAC_STAT_REMOTE_FACES = 5,    /* exchanged faces between partitions per iteration */
+    JAC_STAT_REMOTE_BYTES = 6,    /* bytes stored to other partitions per iteration */
     JAC_STAT_ARENA_BYTES = 7,     /* device bytes of the ghosted block arena */
     JAC_STAT_SWEEP_VARIANT = 8,   /* sweep tile variant (kernels.hpp TmaVariant; 2 = plain loads) */
-    JAC_STAT_N = 9
+    JAC_STAT_PARTITIONS = 9,      /* partitions hosted (1 per device; n_gpus when virtual) */
+    JAC_STAT_REMOTE_ITEMS = 10,   /* sweep work items that wait / signal (fused sync), per iteration */
+    JAC_STAT_FUSED_SYNC = 11,     /* 1: cross-partition ordering runs inside the sweep */
+    JAC_STAT_EPOCH_MIN = 12,      /* min / max over hosted partitions of the epoch word: the */
+    JAC_STAT_EPOCH_MAX = 13,      /* synchronised phases (sweeps + barriers) completed */
+    JAC_STAT_EXPERIMENT = 14,     /* bit mask of active experiment knobs (JAC_EXPERIMENT=1);
+                                     0 in production: no environment variable changes the library */
+    JAC_STAT_N = 15
 };
 int jac_get_stats(const jac_ctx *c, int64_t *stats /* [JAC_STAT_N] */);
 

@@ -38,14 +38,15 @@ JAC_HD inline constexpr int opposite(int f) { return f ^ 1; }
 constexpr int kA = 4;        // x offset of interior column 0 inside a row
 constexpr int kXgPad = 32;   // doubles of slack after each x-ghost array (bulk-copy overrun)
 
-constexpr int kCtrlCounter = 8191;  // ctrl word: CTAs of the current sweep that finished
-
 struct DevBlock {
     int32_t slot;            // own slot in this GPU's arena
     int32_t org[3];          // global interior origin of the block (x, y, z)
-    uint32_t remote_mask;    // bit f: face f's neighbour lives on another rank (process)
+    uint32_t remote_mask;    // bit f: face f's neighbour lives in another partition (another
+                             // GPU, or another virtual partition under JAC_F_VIRTUAL_GPUS)
     uint32_t pack_mask;      // bit f: nb[f][*] is a packed send buffer (JAC_F_NCCL), layout
                              // x: [k][eyp] (x-ghost layout), y: [k][ex], z: [j][ex]
+    int32_t part;            // index of the owning partition in the context's PartSync table
+    int32_t pad_;
     double *nb[6][2];        // per face and buffer, where this block's boundary layer
                              // goes: y/z faces -> the neighbour block's array base;
                              // x faces -> the neighbour's x-ghost array (side
@@ -71,6 +72,30 @@ struct Geom {
 
 enum SweepMode { MODE_FUSED = 0, MODE_PACK = 1, MODE_NOEXCHANGE = 2 };
 
+// Cross-partition ordering state of one partition hosted by a context (one per rank
+// context; one per virtual partition under JAC_F_VIRTUAL_GPUS).  Its control words
+// live in the hosting context's ctrl area: [0] = epoch (phases completed here),
+// [1 + q] = the flag word partition q stores its epoch into (st.release.sys, over
+// NVLink for a peer GPU), [1 + n_gpus] = count of this sweep's finished remote CTAs.
+struct PartSync {
+    uint64_t *ctrl;
+    unsigned long long *count;
+    uint64_t *peer_slot[6];  // per neighbour partition: &its_ctrl[1 + this partition]
+    int32_t peer_id[6];      // neighbour partition ids
+    int32_t npeers;
+    int32_t nremote;         // items of one sweep touching a remote face of this partition
+};
+
+// Watchdog of the cross-partition waits (wait_peers, barrier_kernel): a wait longer
+// than spin_limit_ns (0 = forever) gives up, ORs kStatusPeerTimeout into *status (a
+// mapped host word the engine checks after every call) and continues -- the results of
+// that sweep are then wrong and the call returns JAC_ECUDA; the CUDA context survives.
+constexpr uint32_t kStatusPeerTimeout = 1u;
+struct Watchdog {
+    uint32_t *status;        // mapped pinned host word, or nullptr
+    uint64_t spin_limit_ns;
+};
+
 struct SweepArgs {
     Geom g;
     const DevBlock *blocks;  // [nslots]
@@ -86,21 +111,29 @@ struct SweepArgs {
     // group, z-chunk-major inside a group: item = g*gcols*nzc + zi*gsize + (col - g*gcols).
     // z-chunk zi of a column covers planes [zi*ez/nzc, (zi+1)*ez/nzc).
     int32_t nzc, ncols, nitems, gcols;
-    // Fused cross-rank ordering (rank contexts with remote faces, fused mode).  Only
-    // the items that touch a remote face share memory with a neighbour rank: they
+    // Fused cross-partition ordering (contexts with remote faces, fused mode).  Only
+    // the items that touch a remote face share memory with a neighbour partition: they
     // launch first (item_map), wait for the neighbours' signal of the previous sweep,
-    // and the last of them (nremote) signals this sweep's.  Other items never wait.
+    // and the last of them per partition (PartSync::nremote) signals this sweep's.
+    // Other items never wait.
     const int32_t *item_map; // launch order -> item, or nullptr
-    uint64_t *ctrl;          // own control block ([0] epoch, [1+rank] flags, [kCtrlCounter])
-    uint64_t *peer_slot[6];  // &peer_ctrl[1 + my_rank] per neighbour rank
-    int32_t peer_id[6];
-    int32_t npeers;
+    const PartSync *sync;    // [partitions hosted], indexed by DevBlock::part
+    Watchdog wd;
     int32_t fused_sync;
-    int32_t nremote;         // items touching a remote face (the first nremote of item_map)
-    int32_t pad2_;
+    int32_t nremote;         // remote-touching items of all hosted partitions (the first
+                             // nremote entries of item_map)
     // jac_profile_sweep: when set, every CTA atomicMin's %globaltimer into span[0] after
     // the dependency wait and atomicMax's it into span[1] when done (ns)
     unsigned long long *span;
+};
+
+// One contiguous face copy of the virtual transport (JAC_F_VIRTUAL_GPUS | JAC_F_NCCL):
+// a packed send buffer of one partition into the matching receive buffer of another,
+// standing in for one ncclSend / ncclRecv pair.
+struct FaceCopy {
+    const double *src;
+    double *dst;
+    int64_t count;           // doubles
 };
 
 struct TileItem {
@@ -167,13 +200,14 @@ JAC_HD inline double *xg_array(double *xg, const Geom &g, int buf, int slot, int
     return xg + ((int64_t)(buf * g.nslots + slot) * 2 + side) * g.xgstride;
 }
 
-// Neighbour barrier between ranks (one process per GPU): one flag word per sender
-// in the receiver's control block, monotonically increasing epochs.
+// Neighbour barrier between partitions: every hosted partition bumps its epoch and
+// stores it into each neighbour's flag word, then waits until every neighbour's flag
+// in its own control block has reached it (monotonically increasing epochs).
 struct BarrierArgs {
-    uint64_t *ctrl;          // own control block: [0] = epoch, [1 + sender] = flags
-    uint64_t *peer_slot[6];  // for each face-adjacent rank (<= 6): &peer_ctrl[1 + my_rank]
-    int32_t peer_id[6];      // neighbour rank ids
-    int32_t npeers;
+    const PartSync *sync;    // device table [nparts]
+    int32_t nparts;
+    int32_t pad_;
+    Watchdog wd;
 };
 
 }  // namespace jac

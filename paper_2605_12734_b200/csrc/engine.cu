@@ -134,15 +134,22 @@ struct jac_ctx {
     jac::Plan plan{};
     uint32_t flags = 0;
     bool rank_mode = false;
+    bool virtual_parts = false;  // JAC_F_VIRTUAL_GPUS: every partition on one device, one kernel
     int32_t rank = 0;         // partition owned in rank mode
     int device = 0;
     std::vector<int32_t> parts;  // partitions hosted by this context
     int32_t nslots = 0;
 
+    // group context (jac_create with n_gpus > 1): one rank-mode sub-context per device,
+    // connected by plain peer pointers; every call fans out to them
+    bool group = false;
+    std::vector<jac_ctx *> subs;
+
     jac::Geom geom{};
-    char *alloc = nullptr;    // single allocation: [ctrl][arena][outbox]
+    char *alloc = nullptr;    // single allocation: [ctrl][arena][x ghosts][outbox]
     size_t alloc_bytes = 0, ctrl_off = 0, arena_off = 0, xg_off = 0, outbox_off = 0;
     uint64_t *ctrl = nullptr;
+    int64_t ctrl_stride = 0;  // control words per hosted partition (PartSync)
     double *arena = nullptr, *xg = nullptr, *outbox = nullptr;
     std::vector<jac::DevBlock> hblocks;
     jac::DevBlock *dblocks = nullptr;
@@ -157,14 +164,20 @@ struct jac_ctx {
     int prof_it = 0;
     bool pdl = true;                 // sweeps use programmatic dependent launch (JAC_PDL=0: off)
 
-    // cross-rank exchange
-    std::vector<int32_t> peer_ranks;     // face-adjacent ranks
+    // cross-partition exchange
+    std::vector<std::vector<int32_t>> part_peers;  // [hosted partition] -> neighbour partitions
+    std::vector<jac::PartSync> hsync;              // [hosted partition]
+    jac::PartSync *dsync = nullptr;
+    uint32_t *status_h = nullptr, *status_d = nullptr;  // watchdog word (mapped pinned host)
+    uint64_t watchdog_ns = 60ull * 1000 * 1000 * 1000;
     std::vector<void *> ipc_opened;
     bool ipc_done = false;
-    jac::BarrierArgs bar{};
-    bool fused = false;                 // fused cross-rank ordering inside the sweep
+    bool fused = false;                 // fused cross-partition ordering inside the sweep
     std::vector<NcclFace> nccl_faces;   // JAC_F_NCCL: remote faces, sorted (peer, key)
     void *nccl_comm = nullptr;
+    std::vector<jac::FaceCopy> vcopies; // JAC_F_VIRTUAL_GPUS | JAC_F_NCCL: the virtual transport
+    jac::FaceCopy *dvcopies = nullptr;
+    int64_t vcopy_max = 0;
     int32_t *ditem_map = nullptr;       // launch order -> item (remote-touching items first)
     int32_t nremote = 0;
 
@@ -176,6 +189,7 @@ struct jac_ctx {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     cudaGraphExec_t g1[2] = {nullptr, nullptr}, gU[2] = {nullptr, nullptr};
     int unroll = 10;
+    uint64_t exp_mask = 0;  // experiment knobs this context read (JAC_STAT_EXPERIMENT)
 
     bool inited = false;
     int64_t iters = 0;
@@ -183,12 +197,18 @@ struct jac_ctx {
     int64_t kernel_launches = 0, graph_launches = 0;
     int64_t local_faces = 0, remote_faces = 0, remote_bytes = 0;
 
-    bool has_remote() const { return !peer_ranks.empty(); }
+    bool has_remote() const
+    {
+        for (const auto &p : part_peers)
+            if (!p.empty()) return true;
+        return false;
+    }
+    bool virtual_copy() const { return virtual_parts && (flags & JAC_F_NCCL); }
     int kernels_per_iter() const
     {
         if (flags & JAC_F_PER_BLOCK) return (int)(nslots + 2 * local_faces + 2 * remote_faces);
         if (fused) return 1;
-        if (flags & JAC_F_NCCL) return 2;  // sweep + unpack (NCCL's own kernels not counted)
+        if (flags & JAC_F_NCCL) return virtual_copy() ? 3 : 2;  // sweep + [copy] + unpack (NCCL's own kernels not counted)
         int k = 1;
         if (flags & JAC_F_UNFUSED_PACK) k += 1 + (has_remote() ? 2 : 0);
         else if (has_remote()) k += 1;
@@ -198,6 +218,7 @@ struct jac_ctx {
     {
         return arena + (int64_t)(buf * nslots + slot) * geom.bstride;
     }
+    jac::Watchdog wd() const { return {status_d, watchdog_ns}; }
 };
 
 namespace {
@@ -214,6 +235,28 @@ uint64_t fingerprint(const jac_ctx *c)
     return h;
 }
 
+// Experiment knobs: environment variables that select a tile variant,
+// layout or launch detail for same-box A/B measurements.  They are read only when
+// JAC_EXPERIMENT=1, and every knob a context saw is recorded in its
+// JAC_STAT_EXPERIMENT mask, so no stray variable silently changes a production run.
+const char *const kKnobs[] = {"JAC_L2PROMO", "JAC_ZC",     "JAC_ZCHUNK", "JAC_GCOLS",   "JAC_VARIANT",
+                              "JAC_AUTOTUNE", "JAC_A",      "JAC_PALIGN", "JAC_NO_DENSE", "JAC_UNROLL",
+                              "JAC_PDL",     "JAC_NO_FUSED_SYNC", "JAC_ORDER_EXP", "JAC_DROP_REMOTE",
+                              "JAC_HOLD_SIGNAL"};
+
+const char *knob(jac_ctx *c, const char *name)
+{
+    const char *on = getenv("JAC_EXPERIMENT");
+    if (!on || strcmp(on, "1") != 0) return nullptr;
+    const char *v = getenv(name);
+    if (v)
+        for (size_t i = 0; i < sizeof kKnobs / sizeof kKnobs[0]; ++i)
+            if (!strcmp(kKnobs[i], name)) c->exp_mask |= 1ull << i;
+    return v;
+}
+
+int64_t experiment_mask(const jac_ctx *c) { return (int64_t)c->exp_mask; }
+
 jac::SweepArgs sweep_args(const jac_ctx *c, int src, int mode)
 {
     jac::SweepArgs a{};
@@ -228,16 +271,12 @@ jac::SweepArgs sweep_args(const jac_ctx *c, int src, int mode)
     a.nzc = c->nzc; a.ncols = c->ncols; a.nitems = c->nitems; a.gcols = c->gcols;
     if (c->ditem_map && !c->fused) a.item_map = c->ditem_map;  // JAC_ORDER_EXP
     if (c->prof_span) a.span = c->prof_span + 2 * (int64_t)c->prof_it;
+    a.wd = c->wd();
     if (c->fused && mode == jac::MODE_FUSED) {
         a.fused_sync = 1;
         a.nremote = c->nremote;
         a.item_map = c->ditem_map;
-        a.ctrl = c->ctrl;
-        a.npeers = c->bar.npeers;
-        for (int n = 0; n < c->bar.npeers; ++n) {
-            a.peer_slot[n] = c->bar.peer_slot[n];
-            a.peer_id[n] = c->bar.peer_id[n];
-        }
+        a.sync = c->dsync;
     }
     return a;
 }
@@ -260,9 +299,26 @@ int enqueue_sweep(jac_ctx *c, int src)
 
 int enqueue_barrier(jac_ctx *c)
 {
-    // NCCL contexts share no memory with their peers: NCCL orders the exchange
+    // NCCL contexts share no memory with their peers: NCCL (or, for virtual
+    // partitions, the copy kernel in stream order) orders the exchange
     if (!c->has_remote() || (c->flags & JAC_F_NCCL)) return JAC_OK;
-    CK(jac::launch_barrier(c->bar, c->stream));
+    jac::BarrierArgs ba{};
+    ba.sync = c->dsync;
+    ba.nparts = (int32_t)c->parts.size();
+    ba.wd = c->wd();
+    CK(jac::launch_barrier(ba, c->stream));
+    return JAC_OK;
+}
+
+// The watchdog word the cross-partition waits set when a neighbour never signalled.
+int check_status(jac_ctx *c)
+{
+    if (c->status_h && *reinterpret_cast<volatile uint32_t *>(c->status_h)) {
+        *reinterpret_cast<volatile uint32_t *>(c->status_h) = 0;
+        return fail(JAC_ECUDA, "peer watchdog: a neighbour partition did not signal within %.1f s (rank skew, "
+                               "dead peer or unequal call sequences); this call's results are invalid",
+                    (double)c->watchdog_ns * 1e-9);
+    }
     return JAC_OK;
 }
 
@@ -274,6 +330,11 @@ int enqueue_iteration(jac_ctx *c, int src, cudaEvent_t evs = nullptr, cudaEvent_
     if (evs) CK(cudaEventRecordWithFlags(evs, c->stream, cudaEventRecordExternal));
     if ((rc = enqueue_sweep(c, src))) return rc;
     if (eve) CK(cudaEventRecordWithFlags(eve, c->stream, cudaEventRecordExternal));
+    if (c->virtual_copy()) {  // virtual partitions: packed faces moved by a copy kernel
+        CK(jac::launch_face_copy(c->dvcopies, (int)c->vcopies.size(), c->vcopy_max, c->stream));
+        CK(jac::launch_ghost_fill(sweep_args(c, src, jac::MODE_FUSED), 1 - src, c->stream));
+        return JAC_OK;
+    }
     if (c->flags & JAC_F_NCCL) {  // ablation: library point-to-point instead of peer stores
         const NcclApi *N = nccl_api();
         ncclComm_t comm = (ncclComm_t)c->nccl_comm;
@@ -331,7 +392,7 @@ int encode_tmap(jac_ctx *c)
     const cuuint32_t box[4] = {(cuuint32_t)ts.w, (cuuint32_t)(ts.by + 2), 1, 1};
     const cuuint32_t estr[4] = {1, 1, 1, 1};
     CUtensorMapL2promotion promo = g.ex <= 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
-    if (const char *s = getenv("JAC_L2PROMO")) {  // experiment knob: 0, 64, 128, 256
+    if (const char *s = knob(c, "JAC_L2PROMO")) {  // experiment knob: 0, 64, 128, 256
         const int v = atoi(s);
         promo = v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE : v == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
               : v == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
@@ -374,7 +435,7 @@ void configure_tiles(jac_ctx *c)
     int zc = g.ez;
     const int64_t target = 148 * 4 * 4;
     while ((int64_t)c->nslots * c->ntx * c->nty * ((g.ez + zc - 1) / zc) < target && zc > 16) zc = (zc + 1) / 2;
-    if (const char *s = getenv("JAC_ZC")) zc = std::max(1, std::min(g.ez, atoi(s)));
+    if (const char *s = knob(c, "JAC_ZC")) zc = std::max(1, std::min(g.ez, atoi(s)));
     c->zc = zc;
     c->ntz = (g.ez + zc - 1) / zc;
     // TMA kernel work list: columns cut into z-chunks of ~16 planes.  Short
@@ -394,7 +455,7 @@ void configure_tiles(jac_ctx *c)
         // small grids (C1: 64^3): shorter chunks until the launch fills ~3/4 of a wave
         // (measured 24.5 -> 5.2 us per C1 iteration)
         while (zchunk > 2 && 4 * (int64_t)c->ncols * ((g.ez + zchunk - 1) / zchunk) < 3 * (int64_t)resident) zchunk /= 2;
-        if (const char *s = getenv("JAC_ZCHUNK")) zchunk = std::max(1, atoi(s));
+        if (const char *s = knob(c, "JAC_ZCHUNK")) zchunk = std::max(1, atoi(s));
         c->nzc = std::max(1, (g.ez + zchunk - 1) / zchunk);
         c->nitems = c->ncols * c->nzc;
         // Column groups of 2 x SM-count columns: inside a group the chunk k+1 item of a
@@ -408,7 +469,7 @@ void configure_tiles(jac_ctx *c)
             if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         }
         int gcols = 2 * sms;
-        if (const char *s = getenv("JAC_GCOLS")) gcols = atoi(s);
+        if (const char *s = knob(c, "JAC_GCOLS")) gcols = atoi(s);
         c->gcols = std::max(1, std::min(c->ncols, gcols > 0 ? gcols : c->ncols));
         if (flags & JAC_F_2D) {  // 2-D: items = (block, x tile, chunk of 8 y tiles), nzc = y chunks
             c->nzc = std::max(1, (c->nty + 7) / 8);
@@ -428,13 +489,13 @@ void configure_tiles(jac_ctx *c)
 // JAC_VARIANT skip it.
 int autotune(jac_ctx *c)
 {
-    if (c->variant != jac::TMA_WIDE || getenv("JAC_VARIANT")) return JAC_OK;
+    if (c->variant != jac::TMA_WIDE || knob(c, "JAC_VARIANT")) return JAC_OK;
     if (c->flags & JAC_F_2D) {  // 2-D: 4 stages measured 5% faster on every box, both regimes
         c->variant = jac::TMA_WIDE4;
         configure_tiles(c);
         return JAC_OK;
     }
-    if (const char *s = getenv("JAC_AUTOTUNE"); s && atoi(s) == 0) return JAC_OK;
+    if (const char *s = knob(c, "JAC_AUTOTUNE"); s && atoi(s) == 0) return JAC_OK;
     const int cands[2] = {jac::TMA_WIDE, jac::TMA_WIDE4};
     float ms_of[2] = {0.f, 0.f};
     for (int n = 0; n < 2; ++n) {
@@ -467,7 +528,7 @@ int autotune(jac_ctx *c)
 // items sharing a staged halo (x/y neighbour column, z neighbour chunk) with one of
 // them, then the rest, each class in the natural order.  *n_first = first class size.
 std::vector<int32_t> remote_first_order(jac_ctx *c, const std::vector<uint32_t> &mask, bool partners,
-                                        int32_t *n_first)
+                                        int32_t *n_first, std::vector<int32_t> *first_per_part = nullptr)
 {
     const jac::SweepArgs a0 = sweep_args(c, 0, jac::MODE_NOEXCHANGE);
     const jac::TileShape ts = jac::tma_tile_shape(c->variant);
@@ -509,6 +570,11 @@ std::vector<int32_t> remote_first_order(jac_ctx *c, const std::vector<uint32_t> 
         for (int32_t it = 0; it < c->nitems; ++it)
             if (cls[it] == k) order.push_back(it);
     *n_first = (int32_t)std::count(cls.begin(), cls.end(), (char)0);
+    if (first_per_part) {  // class-0 items per hosted partition (PartSync::nremote)
+        first_per_part->assign(c->parts.size(), 0);
+        for (int32_t it = 0; it < c->nitems; ++it)
+            if (cls[it] == 0) (*first_per_part)[c->hblocks[items[it].b].part]++;
+    }
     return order;
 }
 
@@ -522,8 +588,10 @@ int create_common(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, in
     std::string err;
     int rc = jac::make_plan(nx, ny, nz, bx, by, bz, n_gpus, gpu_grid, &plan, &err);
     if (rc) return fail(rc, "%s", err.c_str());
-    if ((flags & JAC_F_NCCL) && (!rank_mode || (flags & (JAC_F_UNFUSED_PACK | JAC_F_PER_BLOCK | JAC_F_SKIP_EXCHANGE))))
-        return fail(JAC_EINVAL, "flags: JAC_F_NCCL needs a rank context (jac_create_rank) and the fused sweep");
+    if ((flags & JAC_F_NCCL) && (!(rank_mode || (flags & JAC_F_VIRTUAL_GPUS)) ||
+                                 (flags & (JAC_F_UNFUSED_PACK | JAC_F_PER_BLOCK | JAC_F_SKIP_EXCHANGE | JAC_F_NO_TMA))))
+        return fail(JAC_EINVAL, "flags: JAC_F_NCCL needs a rank context (jac_create_rank) or JAC_F_VIRTUAL_GPUS, "
+                                "and the fused TMA sweep");
     if ((flags & JAC_F_2D) && (nz != 1 || bz != 1))
         return fail(JAC_EINVAL, "flags: JAC_F_2D needs nz == 1 and bz == 1 (the 2-D grid is nx x ny)");
     if ((flags & JAC_F_2D) && (flags & (JAC_F_UNFUSED_PACK | JAC_F_NO_TMA)))
@@ -531,12 +599,15 @@ int create_common(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, in
     if ((flags & JAC_F_PER_BLOCK) && (rank_mode || (flags & (JAC_F_UNFUSED_PACK | JAC_F_SKIP_EXCHANGE))))
         return fail(JAC_EINVAL, "flags: JAC_F_PER_BLOCK runs on one GPU (not a rank context) and excludes "
                                 "JAC_F_UNFUSED_PACK / JAC_F_SKIP_EXCHANGE");
+    const bool virt = (flags & JAC_F_VIRTUAL_GPUS) != 0;
     if (rank_mode) {
         if (rank < 0 || rank >= n_gpus) return fail(JAC_EINVAL, "rank %d out of [0,%d)", rank, n_gpus);
-        if (flags & JAC_F_VIRTUAL_GPUS) return fail(JAC_EINVAL, "flags: JAC_F_VIRTUAL_GPUS is not valid for rank contexts");
-    } else if (n_gpus > 1 && !(flags & JAC_F_VIRTUAL_GPUS)) {
-        return fail(JAC_EINVAL, "n_gpus > 1 in one process needs JAC_F_VIRTUAL_GPUS; use jac_create_rank (one process per GPU)");
+        if (virt) return fail(JAC_EINVAL, "flags: JAC_F_VIRTUAL_GPUS is not valid for rank contexts");
+    } else if (n_gpus > 1 && !virt) {
+        return fail(JAC_EINVAL, "internal: multi-device contexts are groups of rank contexts");
     }
+    if ((flags & JAC_F_PER_BLOCK) && n_gpus > 1)
+        return fail(JAC_EINVAL, "flags: JAC_F_PER_BLOCK runs one partition on one GPU (n_gpus == 1)");
     int ndev = 0;
     cudaError_t e = cudaGetDeviceCount(&ndev);
     if (e != cudaSuccess || ndev < 1) return fail(JAC_EDEVICE, "no CUDA device (%s)", cudaGetErrorString(e));
@@ -550,6 +621,7 @@ int create_common(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, in
     c->plan = plan;
     c->flags = flags;
     c->rank_mode = rank_mode;
+    c->virtual_parts = virt && n_gpus > 1;
     c->rank = rank;
     c->device = device;
     if (rank_mode) c->parts = {rank};
@@ -567,9 +639,9 @@ int create_common(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, in
     // (the padding is a few percent of a row; measured equal or better).
     const bool narrow = g.ex <= 64;
     g.A = narrow ? 2 * jac::kA : jac::kA;
-    if (const char *s = getenv("JAC_A")) g.A = std::max(2, atoi(s) & ~1);  // layout experiment knob
+    if (const char *s = knob(c, "JAC_A")) g.A = std::max(2, atoi(s) & ~1);  // layout experiment knob
     int palign = narrow ? 8 : 4;
-    if (const char *s = getenv("JAC_PALIGN")) palign = std::max(4, atoi(s) & ~3);  // layout experiment knob
+    if (const char *s = knob(c, "JAC_PALIGN")) palign = std::max(4, atoi(s) & ~3);  // layout experiment knob
     g.P = round_up(g.A + g.ex + 4, palign);  // room for the 32-byte +x ghost sector (A % 4 == 0)
     // Dense rows (3-D, ex % 8 == 0): no padding and no inline ghost columns at all --
     // A = 0, P = ex -- so a block's rows are back to back, 64-byte aligned, and the
@@ -578,7 +650,7 @@ int create_common(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, in
     // A/B per sweep: 512^3 in 32^3 blocks 441.6 -> 411.4 us; ODF 1 336 -> 330 us;
     // ODF 8 -2%; ODF 64 365 -> 350 us; 1536^3 ODF 16 -2.6..4.7%.  JAC_NO_DENSE=1 keeps
     // the padded rows.
-    if (!(flags & JAC_F_2D) && g.ex % 8 == 0 && !getenv("JAC_NO_DENSE")) {
+    if (!(flags & JAC_F_2D) && g.ex % 8 == 0 && !knob(c, "JAC_NO_DENSE")) {
         g.A = 0;
         g.P = g.ex;
     }
@@ -602,7 +674,7 @@ int create_common(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, in
     // (64-wide blocks: 6-stage ring, 377-379 vs 399-409 us for 512^3 in 64^3 blocks;
     // 32-wide blocks: 6 stages within noise of 4, which stay)
     else c->variant = (g.ex <= 32) ? jac::TMA_EXACT32 : (g.ex <= 64) ? jac::TMA_EXACT64_6 : jac::TMA_WIDE;
-    if (const char *s = getenv("JAC_VARIANT"); s && c->variant != kPlain) {
+    if (const char *s = knob(c, "JAC_VARIANT"); s && c->variant != kPlain) {
         const int v = atoi(s);  // tuning knob; EXACT* only where one tile spans the block row
         if (v == jac::TMA_WIDE || v == jac::TMA_WIDE4 || v == jac::TMA_NARROW ||
             ((v == jac::TMA_EXACT32 || v == jac::TMA_EXACT32_TALL || v == jac::TMA_EXACT32_6) && g.ex <= 32) ||
@@ -610,16 +682,18 @@ int create_common(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, in
             c->variant = v;
     }
     configure_tiles(c);
-    if (const char *s = getenv("JAC_UNROLL")) c->unroll = std::max(2, atoi(s) & ~1);
-    if (const char *s = getenv("JAC_PDL")) c->pdl = atoi(s) != 0;
+    if (const char *s = knob(c, "JAC_UNROLL")) c->unroll = std::max(2, atoi(s) & ~1);
+    if (const char *s = knob(c, "JAC_PDL")) c->pdl = atoi(s) != 0;
     if ((int64_t)c->nslots * c->ntx * c->nty * c->ntz > 0x7fffffffLL) {
         delete c;
         return fail(JAC_EINVAL, "too many tiles for one launch");
     }
 
-    // allocation: [ctrl 64 KiB][arena][x-ghost arrays][outbox]
+    // allocation: [ctrl: one PartSync word block per hosted partition][arena][x-ghost
+    // arrays][outbox]
     c->ctrl_off = 0;
-    c->arena_off = 65536;
+    c->ctrl_stride = round_up((int64_t)n_gpus + 2, 16);
+    c->arena_off = (size_t)round_up(std::max<int64_t>(65536, (int64_t)c->parts.size() * c->ctrl_stride * 8), 65536);
     const size_t arena_bytes = (size_t)2 * c->nslots * g.bstride * sizeof(double);
     c->xg_off = c->arena_off + arena_bytes;
     const size_t xg_bytes = (size_t)2 * c->nslots * 2 * g.xgstride * sizeof(double);
@@ -627,6 +701,7 @@ int create_common(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, in
     // outbox: one set of faces per block; JAC_F_PER_BLOCK double-buffers it by parity
     // (JAC_F_NCCL: send buffers then receive buffers)
     const size_t outbox_bytes = (size_t)((flags & (JAC_F_PER_BLOCK | JAC_F_NCCL)) ? 2 : 1) * c->nslots * g.ostride * sizeof(double);
+    c->part_peers.assign(c->parts.size(), {});
     c->alloc_bytes = c->outbox_off + outbox_bytes;
     e = cudaMalloc(&c->alloc, c->alloc_bytes);
     if (e != cudaSuccess) {
@@ -642,60 +717,86 @@ int create_common(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, in
 
     // descriptor table
     c->hblocks.resize(c->nslots);
+    auto hosted = [&](int32_t part) {  // index of a partition among the hosted ones, or -1
+        const auto it = std::find(c->parts.begin(), c->parts.end(), part);
+        return it == c->parts.end() ? -1 : (int32_t)(it - c->parts.begin());
+    };
     for (int32_t s = 0; s < c->nslots; ++s) {
-        const int32_t part = c->parts[s / bpp], ls = s % bpp;
+        const int32_t h = s / bpp, part = c->parts[h], ls = s % bpp;
         int32_t blk[3];
         plan.block_of(part, ls, blk);
         jac::DevBlock &d = c->hblocks[s];
         memset(&d, 0, sizeof d);
         d.slot = s;
+        d.part = h;
         for (int k = 0; k < 3; ++k) d.org[k] = (int32_t)(blk[k] * plan.e[k]);
         for (int f = 0; f < 6; ++f) {
             int32_t nb[3];
             if (!plan.neighbor(blk, f, nb)) continue;
             const int32_t owner = plan.owner(nb[0], nb[1], nb[2]);
-            const bool local = std::find(c->parts.begin(), c->parts.end(), owner) != c->parts.end();
+            const int32_t oh = hosted(owner);
             const bool same_part = owner == part;
             if (same_part) c->local_faces++;
             else c->remote_faces++;
-            if (!same_part) c->remote_bytes += 8 * ((f >> 1) == 0 ? fx : (f >> 1) == 1 ? fy : fz);
-            if (local) {
-                d.nb[f][0] = block_ptr_local(c, nb, 0, f);
-                d.nb[f][1] = block_ptr_local(c, nb, 1, f);
-                if (c->outbox && (flags & JAC_F_UNFUSED_PACK)) {
-                    int32_t h = (int32_t)(std::find(c->parts.begin(), c->parts.end(), owner) - c->parts.begin());
-                    const int32_t ns = h * bpp + plan.local_slot(nb[0], nb[1], nb[2]);
-                    d.nb_out[f] = c->outbox + (int64_t)ns * g.ostride + g.ooff[jac::opposite(f)];
-                }
-            } else if (flags & JAC_F_NCCL) {
-                // pack into this block's send buffer; the batched ghost kernel unpacks the
-                // receive buffer after the grouped ncclSend / ncclRecv
+            const int64_t count = (f >> 1) == 0 ? fx : (f >> 1) == 1 ? fy : fz;
+            if (!same_part) {
+                c->remote_bytes += 8 * count;
                 d.remote_mask |= 1u << f;
+                auto &pp = c->part_peers[h];
+                if (std::find(pp.begin(), pp.end(), owner) == pp.end()) pp.push_back(owner);
+            }
+            if (!same_part && (flags & JAC_F_NCCL)) {
+                // pack into this block's send buffer; the batched ghost kernel unpacks the
+                // receive buffer after the transport (grouped ncclSend / ncclRecv, or the
+                // copy kernel between virtual partitions)
                 d.pack_mask |= 1u << f;
                 double *sendb = c->outbox + (int64_t)s * g.ostride + g.ooff[f];
                 double *recvb = c->outbox + (int64_t)(c->nslots + s) * g.ostride + g.ooff[f];
                 d.nb[f][0] = d.nb[f][1] = sendb;
                 d.nb_out[f] = recvb;
-                const int64_t gb = ((int64_t)blk[2] * plan.b[1] + blk[1]) * plan.b[0] + blk[0];
-                const int64_t gn = ((int64_t)nb[2] * plan.b[1] + nb[1]) * plan.b[0] + nb[0];
-                const int64_t count = (f >> 1) == 0 ? fx : (f >> 1) == 1 ? fy : fz;
-                c->nccl_faces.push_back({owner, std::min(gb, gn) * 3 + (f >> 1), count, sendb, recvb});
-                if (std::find(c->peer_ranks.begin(), c->peer_ranks.end(), owner) == c->peer_ranks.end())
-                    c->peer_ranks.push_back(owner);
-            } else {
-                d.remote_mask |= 1u << f;  // pointers filled by jac_import_ipc
-                if (std::find(c->peer_ranks.begin(), c->peer_ranks.end(), owner) == c->peer_ranks.end())
-                    c->peer_ranks.push_back(owner);
+                if (oh >= 0) {  // virtual: into the neighbour block's receive buffer
+                    const int32_t ns = oh * bpp + plan.local_slot(nb[0], nb[1], nb[2]);
+                    c->vcopies.push_back({sendb, c->outbox + (int64_t)(c->nslots + ns) * g.ostride +
+                                                     g.ooff[jac::opposite(f)], count});
+                    c->vcopy_max = std::max(c->vcopy_max, count);
+                } else {
+                    const int64_t gb = ((int64_t)blk[2] * plan.b[1] + blk[1]) * plan.b[0] + blk[0];
+                    const int64_t gn = ((int64_t)nb[2] * plan.b[1] + nb[1]) * plan.b[0] + nb[0];
+                    c->nccl_faces.push_back({owner, std::min(gb, gn) * 3 + (f >> 1), count, sendb, recvb});
+                }
+            } else if (oh >= 0) {
+                // the neighbour's memory is in this allocation (same partition, or another
+                // virtual partition): direct-to-ghost stores
+                d.nb[f][0] = block_ptr_local(c, nb, 0, f);
+                d.nb[f][1] = block_ptr_local(c, nb, 1, f);
+                if (c->outbox && (flags & JAC_F_UNFUSED_PACK)) {
+                    const int32_t ns = oh * bpp + plan.local_slot(nb[0], nb[1], nb[2]);
+                    d.nb_out[f] = c->outbox + (int64_t)ns * g.ostride + g.ooff[jac::opposite(f)];
+                }
             }
+            // else: another rank's memory; pointers filled when the peers are connected
         }
     }
-    if (c->peer_ranks.size() > 6) return bail(fail(JAC_EINVAL, "more than 6 neighbour ranks"));
-    if (n_gpus >= jac::kCtrlCounter) return bail(fail(JAC_EINVAL, "n_gpus too large for the control block"));
-    // Fused cross-rank ordering: remote-touching work items launch last and wait for
-    // the neighbours' end-of-sweep signal; everything else starts at once.
+    for (const auto &pp : c->part_peers)
+        if (pp.size() > 6) return bail(fail(JAC_EINVAL, "more than 6 neighbour partitions"));
+    // negative-control experiment (tests): faces between virtual partitions get no store
+    // target, so a neighbour partition's ghosts go stale -- the result must differ
+    if (c->virtual_parts && knob(c, "JAC_DROP_REMOTE"))
+        for (jac::DevBlock &d : c->hblocks)
+            for (int f = 0; f < 6; ++f)
+                if ((d.remote_mask >> f) & 1u) d.nb[f][0] = d.nb[f][1] = nullptr;
+    if ((int64_t)c->parts.size() * c->ctrl_stride > (int64_t)(c->arena_off / 8))
+        return bail(fail(JAC_EINVAL, "n_gpus too large for the control block"));
     std::sort(c->nccl_faces.begin(), c->nccl_faces.end(), [](const NcclFace &x, const NcclFace &y) {
         return x.peer != y.peer ? x.peer < y.peer : x.key < y.key;  // same order on both sides
     });
+    if (!c->vcopies.empty()) {
+        if (c->vcopies.size() > 65535) return bail(fail(JAC_EINVAL, "too many virtual remote faces"));
+        if (cudaMalloc(&c->dvcopies, sizeof(jac::FaceCopy) * c->vcopies.size()) != cudaSuccess ||
+            cudaMemcpy(c->dvcopies, c->vcopies.data(), sizeof(jac::FaceCopy) * c->vcopies.size(),
+                       cudaMemcpyHostToDevice) != cudaSuccess)
+            return bail(fail(JAC_ENOMEM, "virtual transport list"));
+    }
     if (cudaMalloc(&c->dblocks, sizeof(jac::DevBlock) * c->nslots) != cudaSuccess)
         return bail(fail(JAC_ENOMEM, "cudaMalloc descriptor table"));
     if (cudaMemcpy(c->dblocks, c->hblocks.data(), sizeof(jac::DevBlock) * c->nslots, cudaMemcpyHostToDevice) != cudaSuccess)
@@ -720,12 +821,13 @@ int create_common(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, in
                 return bail(fail(JAC_ECUDA, "per-block event creation"));
     }
     if ((rc = autotune(c))) return bail(rc);  // fixes the variant: the item map depends on it
-    c->fused = rank_mode && !c->peer_ranks.empty() && sweep_mode(c) == jac::MODE_FUSED && c->variant != kPlain &&
-               !(flags & JAC_F_NCCL) && !getenv("JAC_NO_FUSED_SYNC");
+    c->fused = (rank_mode || c->virtual_parts) && c->has_remote() && sweep_mode(c) == jac::MODE_FUSED &&
+               c->variant != kPlain && !(flags & (JAC_F_NCCL | JAC_F_PER_BLOCK)) && !knob(c, "JAC_NO_FUSED_SYNC");
     // experiment knob (single-GPU contexts): the remote-first launch order of a rank
     // whose z- and y- faces were remote, without any sync -- isolates the cost of the
     // order itself.  1 = remote-first, 2 = remote-first + halo partners.
-    const int order_exp = (!rank_mode && getenv("JAC_ORDER_EXP")) ? atoi(getenv("JAC_ORDER_EXP")) : 0;
+    const int order_exp = (!rank_mode && !c->virtual_parts && knob(c, "JAC_ORDER_EXP")) ? atoi(knob(c, "JAC_ORDER_EXP")) : 0;
+    std::vector<int32_t> nremote_part(c->parts.size(), 0);
     if (c->fused || (order_exp && c->variant != kPlain)) {
         std::vector<uint32_t> mask(c->nslots);
         for (int32_t sl = 0; sl < c->nslots; ++sl)
@@ -736,18 +838,41 @@ int create_common(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, in
         // next sweep's remote items (which wait for it) find it already set
         int32_t nfirst = 0;
         const std::vector<int32_t> order =
-            remote_first_order(c, mask, order_exp == 2, &nfirst);
+            remote_first_order(c, mask, order_exp == 2, &nfirst, &nremote_part);
         if (c->fused) c->nremote = nfirst;
         if (cudaMalloc(&c->ditem_map, sizeof(int32_t) * order.size()) != cudaSuccess ||
             cudaMemcpy(c->ditem_map, order.data(), sizeof(int32_t) * order.size(), cudaMemcpyHostToDevice) != cudaSuccess)
             return bail(fail(JAC_ENOMEM, "item map"));
         if (c->fused && c->nremote == 0) c->fused = false;
     }
-    // barrier args (peer slots filled at import)
-    c->bar.ctrl = c->ctrl;
-    c->bar.npeers = (int32_t)c->peer_ranks.size();
-    for (int n = 0; n < c->bar.npeers; ++n) c->bar.peer_id[n] = c->peer_ranks[n];
-    c->ipc_done = !c->has_remote() && !rank_mode;
+    // watchdog word of the cross-partition waits: mapped pinned host memory, read after
+    // every synchronising call
+    if (cudaHostAlloc(&c->status_h, sizeof(uint32_t), cudaHostAllocMapped) != cudaSuccess ||
+        cudaHostGetDevicePointer(&c->status_d, c->status_h, 0) != cudaSuccess)
+        return bail(fail(JAC_ENOMEM, "watchdog status word"));
+    *c->status_h = 0;
+    // per-partition sync table: own control words; neighbours' flag slots are local
+    // for virtual partitions, filled when the peers are connected for a rank context
+    c->hsync.assign(c->parts.size(), jac::PartSync{});
+    for (size_t h = 0; h < c->parts.size(); ++h) {
+        jac::PartSync &ps = c->hsync[h];
+        ps.ctrl = c->ctrl + (int64_t)h * c->ctrl_stride;
+        ps.count = reinterpret_cast<unsigned long long *>(ps.ctrl + 1 + n_gpus);
+        ps.npeers = (int32_t)c->part_peers[h].size();
+        ps.nremote = nremote_part[h];
+        // watchdog experiment (tests): partition 0 never signals its sweeps
+        if (h == 0 && knob(c, "JAC_HOLD_SIGNAL")) ps.nremote = 0x7fffffff;
+        for (int n = 0; n < ps.npeers; ++n) {
+            const int32_t q = c->part_peers[h][n];
+            ps.peer_id[n] = q;
+            const int32_t qh = hosted(q);
+            if (qh >= 0) ps.peer_slot[n] = c->ctrl + (int64_t)qh * c->ctrl_stride + 1 + c->parts[h];
+        }
+    }
+    if (cudaMalloc(&c->dsync, sizeof(jac::PartSync) * c->hsync.size()) != cudaSuccess ||
+        cudaMemcpy(c->dsync, c->hsync.data(), sizeof(jac::PartSync) * c->hsync.size(), cudaMemcpyHostToDevice) != cudaSuccess)
+        return bail(fail(JAC_ENOMEM, "partition sync table"));
+    c->ipc_done = !rank_mode;
     *out = c;
     return JAC_OK;
 }
@@ -877,9 +1002,257 @@ int finish_init(jac_ctx *c)
     int rc;
     if ((rc = enqueue_barrier(c))) return rc;  // neighbours may write our ghosts only after this
     CK(cudaStreamSynchronize(c->stream));
+    if ((rc = check_status(c))) return rc;
     c->inited = true;
     c->iters = 0;
     return JAC_OK;
+}
+
+// ---------------------------------------------------------------- jac_step phases
+// jac_step = check, begin (graphs, start event), launches in chunks, end (stop event,
+// synchronise, watchdog).  A group context runs the phases of its sub-contexts
+// interleaved, chunk by chunk, so every device has its share queued before any host
+// wait (the devices' sweeps wait on one another's flags).
+int step_check(jac_ctx *c, int32_t n)
+{
+    int rc;
+    if ((rc = require_ready(c))) return rc;
+    if (n < 0) return fail(JAC_EINVAL, "n_iters = %d < 0", n);
+    if (!c->inited) return fail(JAC_ESTATE, "jac_step before jac_set_init / jac_set_init_hash");
+    return JAC_OK;
+}
+
+bool use_graphs(const jac_ctx *c) { return !(c->flags & (JAC_F_NO_GRAPH | JAC_F_PER_BLOCK)); }
+
+int step_begin(jac_ctx *c)
+{
+    int rc;
+    if (use_graphs(c) && !c->g1[0]) {
+        for (int s = 0; s < 2; ++s) {
+            if ((rc = build_graph(c, s, 1, &c->g1[s]))) return rc;
+            if ((rc = build_graph(c, s, c->unroll, &c->gU[s]))) return rc;
+        }
+    }
+    CK(cudaEventRecord(c->ev0, c->stream));
+    return JAC_OK;
+}
+
+// iterations the next launch covers: one unrolled graph, else one iteration
+int32_t step_chunk(const jac_ctx *c, int32_t left) { return (use_graphs(c) && left >= c->unroll) ? c->unroll : 1; }
+
+// Enqueues k iterations (k == unroll: the unrolled graph; k == 1) and advances the
+// context's iteration count (the parity of the next launch).
+int step_launch(jac_ctx *c, int32_t k)
+{
+    const int src = (int)(c->iters & 1);
+    if (use_graphs(c)) {
+        CK(cudaGraphLaunch(k == c->unroll ? c->gU[src] : c->g1[src], c->stream));
+        c->graph_launches++;
+    } else {
+        int rc;
+        if ((rc = enqueue_iteration(c, src))) return rc;
+    }
+    c->iters += k;
+    c->kernel_launches += (int64_t)k * c->kernels_per_iter();
+    return JAC_OK;
+}
+
+int step_end(jac_ctx *c, int32_t n)
+{
+    CK(cudaEventRecord(c->ev1, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+    c->last_ms = ms;
+    if (c->flags & JAC_F_PER_BLOCK) {  // per_block_step enqueued all n iterations
+        c->iters += n;
+        c->kernel_launches += (int64_t)n * c->kernels_per_iter();
+    }
+    return check_status(c);
+}
+
+// Rank context c: fills the REMOTE face pointers of the descriptor table and the
+// neighbours' flag slots from the neighbour ranks' allocation bases (IPC-mapped
+// memory of other processes, or plain peer pointers of a group's sub-contexts) and
+// the layout offsets of their records.
+int connect_peers(jac_ctx *c, const std::vector<char *> &base, const IpcRecord *recs)
+{
+    const jac::Plan &p = c->plan;
+    const int32_t bpp = p.blocks_per_part();
+    const jac::Geom &g = c->geom;
+    for (int32_t s = 0; s < c->nslots; ++s) {
+        int32_t blk[3];
+        p.block_of(c->rank, s, blk);
+        for (int f = 0; f < 6; ++f) {
+            int32_t nb[3];
+            if (!p.neighbor(blk, f, nb)) continue;
+            const int32_t q = p.owner(nb[0], nb[1], nb[2]);
+            if (q == c->rank) continue;
+            const int32_t ns = p.local_slot(nb[0], nb[1], nb[2]);
+            double *arena = reinterpret_cast<double *>(base[q] + recs[q].arena_off);
+            double *xg = reinterpret_cast<double *>(base[q] + recs[q].xg_off);
+            for (int buf = 0; buf < 2; ++buf)
+                c->hblocks[s].nb[f][buf] = (f >> 1) == 0 ? jac::xg_array(xg, g, buf, ns, jac::opposite(f) & 1)
+                                                         : arena + (int64_t)(buf * bpp + ns) * g.bstride;
+            if (c->outbox) {
+                const double *ob = reinterpret_cast<const double *>(base[q] + recs[q].outbox_off);
+                c->hblocks[s].nb_out[f] = ob + (int64_t)ns * g.ostride + g.ooff[jac::opposite(f)];
+            }
+        }
+    }
+    jac::PartSync &ps = c->hsync[0];
+    for (int n = 0; n < ps.npeers; ++n) {
+        const int32_t q = ps.peer_id[n];
+        uint64_t *pc = reinterpret_cast<uint64_t *>(base[q] + recs[q].ctrl_off);  // rank q hosts one partition
+        ps.peer_slot[n] = pc + 1 + c->rank;
+    }
+    CK(cudaMemcpy(c->dblocks, c->hblocks.data(), sizeof(jac::DevBlock) * c->nslots, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->dsync, c->hsync.data(), sizeof(jac::PartSync) * c->hsync.size(), cudaMemcpyHostToDevice));
+    c->ipc_done = true;
+    return JAC_OK;
+}
+
+
+// ---------------------------------------------------------------- group contexts
+// jac_create(n_gpus > 1): one process drives every GPU.  The
+// group holds one rank-mode sub-context per device -- partition g on device g -- and
+// connects them with plain peer pointers (cudaDeviceEnablePeerAccess) instead of IPC
+// records, so every sub-context runs exactly the rank path: in-sweep peer stores over
+// NVLink and the device-flag handshake.  Calls fan out to the sub-contexts.
+
+struct DeviceGuard {  // restores the caller's current device
+    int dev = -1;
+    DeviceGuard() { if (cudaGetDevice(&dev) != cudaSuccess) dev = -1; }
+    ~DeviceGuard() { if (dev >= 0) cudaSetDevice(dev); }
+};
+
+// Runs fn(sub) on every sub-context concurrently, one host thread per device: the
+// collective cold-path calls (init, profiling) contain cross-device barriers, so no
+// device's call may wait for another's to return.  Returns the first error.
+template <class F>
+int for_each_sub(jac_ctx *G, F fn)
+{
+    const size_t n = G->subs.size();
+    std::vector<int> rcs(n, JAC_OK);
+    std::vector<std::string> errs(n);
+    std::vector<std::thread> th;
+    for (size_t i = 0; i < n; ++i)
+        th.emplace_back([&, i] {
+            cudaSetDevice(G->subs[i]->device);
+            rcs[i] = fn(G->subs[i]);
+            if (rcs[i]) errs[i] = g_err;
+        });
+    for (auto &t : th) t.join();
+    for (size_t i = 0; i < n; ++i)
+        if (rcs[i]) { g_err = errs[i]; return rcs[i]; }
+    return JAC_OK;
+}
+
+jac_ctx *owner_sub(const jac_ctx *G, int32_t ix, int32_t iy, int32_t iz)
+{
+    const jac::Plan &p = G->plan;
+    if (ix < 0 || iy < 0 || iz < 0 || ix >= p.b[0] || iy >= p.b[1] || iz >= p.b[2]) return nullptr;
+    return G->subs[p.owner(ix, iy, iz)];
+}
+
+int create_group(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, int32_t bz, int32_t n_gpus,
+                 const int32_t *gpu_grid, uint32_t flags, jac_ctx **out)
+{
+    if (!out) return fail(JAC_EINVAL, "out is NULL");
+    *out = nullptr;
+    jac::Plan plan;
+    std::string err;
+    int rc = jac::make_plan(nx, ny, nz, bx, by, bz, n_gpus, gpu_grid, &plan, &err);
+    if (rc) return fail(rc, "%s", err.c_str());
+    if (flags & (JAC_F_NCCL | JAC_F_PER_BLOCK))
+        return fail(JAC_EINVAL, "flags: JAC_F_NCCL / JAC_F_PER_BLOCK are not available in a multi-GPU "
+                                "single-process context (use jac_create_rank, one process per GPU)");
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev < n_gpus)
+        return fail(JAC_EDEVICE, "n_gpus = %d but %d CUDA devices are visible", n_gpus, e == cudaSuccess ? ndev : 0);
+    DeviceGuard guard;
+    jac_ctx *G = new jac_ctx();
+    G->group = true;
+    G->plan = plan;
+    G->flags = flags;
+    auto bail = [&](int code) { std::string m = g_err; jac_destroy(G); g_err = m; return code; };
+    for (int32_t g = 0; g < n_gpus; ++g) {
+        jac_ctx *sub = nullptr;
+        if ((rc = create_common(nx, ny, nz, bx, by, bz, n_gpus, gpu_grid, true, g, g, flags, &sub))) return bail(rc);
+        G->subs.push_back(sub);
+        G->parts.push_back(g);
+    }
+    // peer access between neighbour devices, then the rank path's connection step with
+    // plain pointers
+    for (jac_ctx *c : G->subs)
+        for (int32_t q : c->part_peers[0]) {
+            int ok = 0;
+            CK(cudaDeviceCanAccessPeer(&ok, c->device, G->subs[q]->device));
+            if (!ok) return bail(fail(JAC_EDEVICE, "device %d cannot access device %d (P2P unavailable)", c->device, q));
+            CK(cudaSetDevice(c->device));
+            const cudaError_t pe = cudaDeviceEnablePeerAccess(G->subs[q]->device, 0);
+            if (pe != cudaSuccess && pe != cudaErrorPeerAccessAlreadyEnabled)
+                return bail(fail(JAC_EDEVICE, "cudaDeviceEnablePeerAccess(%d -> %d): %s", c->device, q,
+                                 cudaGetErrorString(pe)));
+            cudaGetLastError();  // clear cudaErrorPeerAccessAlreadyEnabled
+        }
+    std::vector<char *> base(n_gpus);
+    std::vector<IpcRecord> recs(n_gpus);
+    for (int32_t q = 0; q < n_gpus; ++q) {
+        const jac_ctx *c = G->subs[q];
+        base[q] = c->alloc;
+        memset(&recs[q], 0, sizeof(IpcRecord));
+        recs[q].magic = kIpcMagic;
+        recs[q].rank = q;
+        recs[q].arena_off = c->arena_off;
+        recs[q].outbox_off = c->outbox_off;
+        recs[q].ctrl_off = c->ctrl_off;
+        recs[q].xg_off = c->xg_off;
+    }
+    for (jac_ctx *c : G->subs) {
+        CK(cudaSetDevice(c->device));
+        if ((rc = connect_peers(c, base, recs.data()))) return bail(rc);
+    }
+    G->ipc_done = true;
+    G->nslots = 0;
+    for (jac_ctx *c : G->subs) G->nslots += c->nslots;
+    *out = G;
+    return JAC_OK;
+}
+
+int group_step(jac_ctx *G, int32_t n)
+{
+    int rc;
+    if (n < 0) return fail(JAC_EINVAL, "n_iters = %d < 0", n);
+    DeviceGuard guard;
+    for (jac_ctx *c : G->subs)
+        if ((rc = step_check(c, n))) return rc;
+    for (jac_ctx *c : G->subs) {
+        CK(cudaSetDevice(c->device));
+        if ((rc = step_begin(c))) return rc;
+    }
+    for (int32_t left = n; left > 0;) {  // interleaved: every device's chunk queued in turn
+        const int32_t k = step_chunk(G->subs[0], left);
+        for (jac_ctx *c : G->subs) {
+            CK(cudaSetDevice(c->device));
+            if ((rc = step_launch(c, k))) return rc;
+        }
+        left -= k;
+    }
+    int first = JAC_OK;
+    std::string msg;
+    double ms = 0.0;
+    for (jac_ctx *c : G->subs) {  // every device is synchronised even if one failed
+        cudaSetDevice(c->device);
+        rc = step_end(c, n);
+        if (rc && !first) { first = rc; msg = g_err; }
+        ms = std::max(ms, c->last_ms);
+    }
+    G->last_ms = ms;
+    G->iters = G->subs[0]->iters;
+    if (first) g_err = msg;
+    return first;
 }
 
 }  // namespace
@@ -928,6 +1301,8 @@ int jac_create(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, int32
                const int32_t *gpu_grid, uint32_t flags, jac_ctx **out)
 {
     try {
+        if (n_gpus > 1 && !(flags & JAC_F_VIRTUAL_GPUS))
+            return create_group(nx, ny, nz, bx, by, bz, n_gpus, gpu_grid, flags, out);
         return create_common(nx, ny, nz, bx, by, bz, n_gpus, gpu_grid, false, 0, 0, flags, out);
     } catch (...) { return fail(JAC_ENOMEM, "host allocation failed"); }
 }
@@ -1005,7 +1380,7 @@ int jac_import_ipc(jac_ctx *c, const void *all)
     const jac::Plan &p = c->plan;
     const uint64_t fp = fingerprint(c);
     std::vector<char *> base(p.n_gpus, nullptr);
-    for (int32_t q : c->peer_ranks) {
+    for (int32_t q : c->part_peers[0]) {
         const IpcRecord &r = recs[q];
         if (r.magic != kIpcMagic || r.rank != q) return fail(JAC_EINVAL, "all: record %d is not a jacobi3d IPC record of rank %d", q, q);
         if (r.fingerprint != fp) return fail(JAC_EINVAL, "all: rank %d was created with a different decomposition/flags", q);
@@ -1014,36 +1389,7 @@ int jac_import_ipc(jac_ctx *c, const void *all)
         c->ipc_opened.push_back(ptr);
         base[q] = static_cast<char *>(ptr);
     }
-    const int32_t bpp = p.blocks_per_part();
-    const jac::Geom &g = c->geom;
-    for (int32_t s = 0; s < c->nslots; ++s) {
-        int32_t blk[3];
-        p.block_of(c->rank, s, blk);
-        for (int f = 0; f < 6; ++f) {
-            int32_t nb[3];
-            if (!p.neighbor(blk, f, nb)) continue;
-            const int32_t q = p.owner(nb[0], nb[1], nb[2]);
-            if (q == c->rank) continue;
-            const int32_t ns = p.local_slot(nb[0], nb[1], nb[2]);
-            double *arena = reinterpret_cast<double *>(base[q] + recs[q].arena_off);
-            double *xg = reinterpret_cast<double *>(base[q] + recs[q].xg_off);
-            for (int buf = 0; buf < 2; ++buf)
-                c->hblocks[s].nb[f][buf] = (f >> 1) == 0 ? jac::xg_array(xg, g, buf, ns, jac::opposite(f) & 1)
-                                                         : arena + (int64_t)(buf * bpp + ns) * g.bstride;
-            if (c->outbox) {
-                const double *ob = reinterpret_cast<const double *>(base[q] + recs[q].outbox_off);
-                c->hblocks[s].nb_out[f] = ob + (int64_t)ns * g.ostride + g.ooff[jac::opposite(f)];
-            }
-        }
-    }
-    for (int n = 0; n < c->bar.npeers; ++n) {
-        const int32_t q = c->bar.peer_id[n];
-        uint64_t *pc = reinterpret_cast<uint64_t *>(base[q] + recs[q].ctrl_off);
-        c->bar.peer_slot[n] = pc + 1 + c->rank;
-    }
-    CK(cudaMemcpy(c->dblocks, c->hblocks.data(), sizeof(jac::DevBlock) * c->nslots, cudaMemcpyHostToDevice));
-    c->ipc_done = true;
-    return JAC_OK;
+    return connect_peers(c, base, recs);
 }
 
 int jac_local_box(const jac_ctx *c, int64_t *origin, int64_t *extent)
@@ -1051,6 +1397,15 @@ int jac_local_box(const jac_ctx *c, int64_t *origin, int64_t *extent)
     if (!c || !origin || !extent) return fail(JAC_EINVAL, "ctx/origin/extent is NULL");
     const jac::Plan &p = c->plan;
     int64_t lo[3] = {INT64_MAX, INT64_MAX, INT64_MAX}, hi[3] = {0, 0, 0};
+    if (c->group) {  // the union of the devices' boxes
+        for (const jac_ctx *sc : c->subs) {
+            int64_t o[3], e[3];
+            jac_local_box(sc, o, e);
+            for (int k = 0; k < 3; ++k) { lo[k] = std::min(lo[k], o[k]); hi[k] = std::max(hi[k], o[k] + e[k]); }
+        }
+        for (int k = 0; k < 3; ++k) { origin[k] = lo[k]; extent[k] = hi[k] - lo[k]; }
+        return JAC_OK;
+    }
     for (const jac::DevBlock &d : c->hblocks)
         for (int k = 0; k < 3; ++k) {
             lo[k] = std::min<int64_t>(lo[k], d.org[k]);
@@ -1066,11 +1421,42 @@ int check_box(const jac_ctx *c, const void *box, const int64_t *origin, const in
     if (!box || !origin || !extent) return fail(JAC_EINVAL, "box/origin/extent is NULL");
     int64_t lo[3], ex[3];
     jac_local_box(c, lo, ex);
+    const int zg = c->group ? c->subs[0]->geom.zg : c->geom.zg;
     for (int k = 0; k < 3; ++k)
         if (origin[k] < 0 || extent[k] < 1 || origin[k] > lo[k] || origin[k] + extent[k] < lo[k] + ex[k] ||
-            origin[k] + extent[k] > c->plan.n[k] + (k == 2 ? 2 * c->geom.zg : 2))
+            origin[k] + extent[k] > c->plan.n[k] + (k == 2 ? 2 * zg : 2))
             return fail(JAC_EINVAL, "box origin/extent (dim %d: %lld+%lld) does not cover the local blocks (%lld+%lld)",
                         k, (long long)origin[k], (long long)extent[k], (long long)lo[k], (long long)ex[k]);
+    return JAC_OK;
+}
+// Copies the part of interior sub-box [lo, lo+ext) held by context c into out
+// (x fastest, ext[2] x ext[1] x ext[0]); *covered += the cells copied.
+int region_copy(jac_ctx *c, const int64_t *lo, const int64_t *ext, double *out, int64_t *covered)
+{
+    const jac::Plan &p = c->plan;
+    CK(cudaSetDevice(c->device));
+    const jac::Geom &g = c->geom;
+    for (int32_t s = 0; s < c->nslots; ++s) {
+        const jac::DevBlock &d = c->hblocks[s];
+        int64_t a[3], b[3];
+        bool empty = false;
+        for (int k = 0; k < 3; ++k) {
+            a[k] = std::max<int64_t>(lo[k], d.org[k]);
+            b[k] = std::min<int64_t>(lo[k] + ext[k], d.org[k] + p.e[k]);
+            empty |= a[k] >= b[k];
+        }
+        if (empty) continue;
+        *covered += (b[0] - a[0]) * (b[1] - a[1]) * (b[2] - a[2]);
+        cudaMemcpy3DParms m{};
+        m.srcPtr = make_cudaPitchedPtr(c->slot_ptr((int)(c->iters & 1), s), (size_t)g.P * 8, (size_t)g.P, (size_t)(g.ey + 2));
+        m.srcPos = make_cudaPos((size_t)(g.A + a[0] - d.org[0]) * 8, (size_t)(1 + a[1] - d.org[1]), (size_t)(g.zg + a[2] - d.org[2]));
+        m.dstPtr = make_cudaPitchedPtr(out, (size_t)ext[0] * 8, (size_t)ext[0], (size_t)ext[1]);
+        m.dstPos = make_cudaPos((size_t)(a[0] - lo[0]) * 8, (size_t)(a[1] - lo[1]), (size_t)(a[2] - lo[2]));
+        m.extent = make_cudaExtent((size_t)(b[0] - a[0]) * 8, (size_t)(b[1] - a[1]), (size_t)(b[2] - a[2]));
+        m.kind = cudaMemcpyDeviceToHost;
+        CK(cudaMemcpy3DAsync(&m, c->stream));
+    }
+    CK(cudaStreamSynchronize(c->stream));
     return JAC_OK;
 }
 }  // namespace
@@ -1080,6 +1466,13 @@ int jac_set_init_box(jac_ctx *c, const double *box, const int64_t *origin, const
     int rc;
     if ((rc = require_ready(c))) return rc;
     if ((rc = check_box(c, box, origin, extent))) return rc;
+    if (c->group) {
+        DeviceGuard guard;
+        rc = for_each_sub(c, [&](jac_ctx *sc) { return jac_set_init_box(sc, box, origin, extent); });
+        c->inited = rc == JAC_OK;
+        c->iters = 0;
+        return rc;
+    }
     CK(cudaSetDevice(c->device));
     const jac::Geom &g = c->geom;
     if ((rc = enqueue_barrier(c))) return rc;  // neighbours finished writing our ghosts
@@ -1134,7 +1527,8 @@ int jac_set_init(jac_ctx *c, const double *padded)
     if (!c) return fail(JAC_EINVAL, "ctx is NULL");
     if (!padded) return fail(JAC_EINVAL, "padded is NULL");
     const int64_t o[3] = {0, 0, 0};
-    const int64_t e[3] = {c->plan.n[0] + 2, c->plan.n[1] + 2, c->plan.n[2] + 2 * c->geom.zg};
+    const int zg = c->group ? c->subs[0]->geom.zg : c->geom.zg;
+    const int64_t e[3] = {c->plan.n[0] + 2, c->plan.n[1] + 2, c->plan.n[2] + 2 * zg};
     return jac_set_init_box(c, padded, o, e);
 }
 
@@ -1142,6 +1536,13 @@ int jac_set_init_hash(jac_ctx *c, uint64_t seed)
 {
     int rc;
     if ((rc = require_ready(c))) return rc;
+    if (c->group) {
+        DeviceGuard guard;
+        rc = for_each_sub(c, [&](jac_ctx *sc) { return jac_set_init_hash(sc, seed); });
+        c->inited = rc == JAC_OK;
+        c->iters = 0;
+        return rc;
+    }
     CK(cudaSetDevice(c->device));
     if ((rc = enqueue_barrier(c))) return rc;
     CK(jac::launch_hash_init(sweep_args(c, 0, 0), c->plan.n[0], c->plan.n[1], seed, c->stream));
@@ -1153,48 +1554,20 @@ int jac_set_init_hash(jac_ctx *c, uint64_t seed)
 int jac_step(jac_ctx *c, int32_t n)
 {
     int rc;
-    if ((rc = require_ready(c))) return rc;
-    if (n < 0) return fail(JAC_EINVAL, "n_iters = %d < 0", n);
-    if (!c->inited) return fail(JAC_ESTATE, "jac_step before jac_set_init / jac_set_init_hash");
+    if (c && c->group) return group_step(c, n);
+    if ((rc = step_check(c, n))) return rc;
     CK(cudaSetDevice(c->device));
-    const bool graphs = !(c->flags & (JAC_F_NO_GRAPH | JAC_F_PER_BLOCK));
-    if (graphs && !c->g1[0]) {
-        for (int s = 0; s < 2; ++s) {
-            if ((rc = build_graph(c, s, 1, &c->g1[s]))) return rc;
-            if ((rc = build_graph(c, s, c->unroll, &c->gU[s]))) return rc;
-        }
-    }
-    const int kpi = c->kernels_per_iter();
-    CK(cudaEventRecord(c->ev0, c->stream));
-    int src = (int)(c->iters & 1);
-    int left = n;
+    if ((rc = step_begin(c))) return rc;
     if (c->flags & JAC_F_PER_BLOCK) {
         if ((rc = per_block_step(c, n))) return rc;
-        left = 0;
-    } else if (graphs) {
-        while (left >= c->unroll) {
-            CK(cudaGraphLaunch(c->gU[src], c->stream));
-            c->graph_launches++;
-            left -= c->unroll;  // unroll is even: parity unchanged
-        }
-        while (left > 0) {
-            CK(cudaGraphLaunch(c->g1[src], c->stream));
-            c->graph_launches++;
-            src ^= 1;
-            --left;
-        }
     } else {
-        for (; left > 0; --left, src ^= 1)
-            if ((rc = enqueue_iteration(c, src))) return rc;
+        for (int32_t left = n; left > 0;) {
+            const int32_t k = step_chunk(c, left);
+            if ((rc = step_launch(c, k))) return rc;
+            left -= k;
+        }
     }
-    CK(cudaEventRecord(c->ev1, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
-    float ms = 0.f;
-    CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
-    c->last_ms = ms;
-    c->iters += n;
-    c->kernel_launches += (int64_t)n * kpi;
-    return JAC_OK;
+    return step_end(c, n);
 }
 
 int jac_profile_sweep(jac_ctx *c, int32_t n, double *avg_ms)
@@ -1203,6 +1576,17 @@ int jac_profile_sweep(jac_ctx *c, int32_t n, double *avg_ms)
     if ((rc = require_ready(c))) return rc;
     if (n < 1 || !avg_ms) return fail(JAC_EINVAL, "n_iters must be >= 1 and avg_sweep_ms non-NULL");
     if (!c->inited) return fail(JAC_ESTATE, "jac_profile_sweep before init");
+    if (c->group) {  // every device profiles concurrently; the slowest device's figures
+        DeviceGuard guard;
+        std::vector<double> ms(c->subs.size(), 0.0);
+        rc = for_each_sub(c, [&](jac_ctx *sc) { return jac_profile_sweep(sc, n, &ms[sc->rank]); });
+        if (rc) return rc;
+        *avg_ms = *std::max_element(ms.begin(), ms.end());
+        c->last_gap_ms = -1.0;
+        for (const jac_ctx *sc : c->subs) c->last_gap_ms = std::max(c->last_gap_ms, sc->last_gap_ms);
+        c->iters = c->subs[0]->iters;
+        return JAC_OK;
+    }
     if (c->flags & JAC_F_PER_BLOCK) return fail(JAC_EINVAL, "jac_profile_sweep: not available with JAC_F_PER_BLOCK");
     CK(cudaSetDevice(c->device));
     struct Events {  // destroyed on every return path
@@ -1273,6 +1657,7 @@ int jac_profile_sweep(jac_ctx *c, int32_t n, double *avg_ms)
     }
     c->iters += n;
     c->kernel_launches += (int64_t)n * c->kernels_per_iter();
+    if ((rc = check_status(c))) return rc;
     // median: robust to the first launches of a multi-rank run, whose remote items may
     // wait for a neighbour rank that started its profiling graph a little later
     std::sort(dur.begin(), dur.end());
@@ -1291,6 +1676,12 @@ int jac_last_profile_gap_ms(const jac_ctx *c, double *ms)
 int jac_get_block_padded(jac_ctx *c, int32_t ix, int32_t iy, int32_t iz, double *out)
 {
     if (!c || !out) return fail(JAC_EINVAL, "ctx/out is NULL");
+    if (c->group) {
+        jac_ctx *sc = owner_sub(c, ix, iy, iz);
+        if (!sc) return fail(JAC_EINVAL, "block index (%d,%d,%d) out of range", ix, iy, iz);
+        DeviceGuard guard;
+        return jac_get_block_padded(sc, ix, iy, iz, out);
+    }
     int32_t s;
     int rc;
     if ((rc = local_slot_of(c, ix, iy, iz, &s))) return rc;
@@ -1326,6 +1717,12 @@ int jac_get_block_padded(jac_ctx *c, int32_t ix, int32_t iy, int32_t iz, double 
 int jac_get_block(jac_ctx *c, int32_t ix, int32_t iy, int32_t iz, double *out)
 {
     if (!c || !out) return fail(JAC_EINVAL, "ctx/out is NULL");
+    if (c->group) {
+        jac_ctx *sc = owner_sub(c, ix, iy, iz);
+        if (!sc) return fail(JAC_EINVAL, "block index (%d,%d,%d) out of range", ix, iy, iz);
+        DeviceGuard guard;
+        return jac_get_block(sc, ix, iy, iz, out);
+    }
     int32_t s;
     int rc;
     if ((rc = local_slot_of(c, ix, iy, iz, &s))) return rc;
@@ -1347,6 +1744,12 @@ int jac_get_field_box(jac_ctx *c, double *box, const int64_t *origin, const int6
     if (!c) return fail(JAC_EINVAL, "ctx is NULL");
     int rc;
     if ((rc = check_box(c, box, origin, extent))) return rc;
+    if (c->group) {
+        DeviceGuard guard;
+        for (jac_ctx *sc : c->subs)
+            if ((rc = jac_get_field_box(sc, box, origin, extent))) return rc;
+        return JAC_OK;
+    }
     CK(cudaSetDevice(c->device));
     const jac::Geom &g = c->geom;
     for (int32_t s = 0; s < c->nslots; ++s) {
@@ -1370,7 +1773,8 @@ int jac_get_field(jac_ctx *c, double *padded)
     if (!c) return fail(JAC_EINVAL, "ctx is NULL");
     if (!padded) return fail(JAC_EINVAL, "padded is NULL");
     const int64_t o[3] = {0, 0, 0};
-    const int64_t e[3] = {c->plan.n[0] + 2, c->plan.n[1] + 2, c->plan.n[2] + 2 * c->geom.zg};
+    const int zg = c->group ? c->subs[0]->geom.zg : c->geom.zg;
+    const int64_t e[3] = {c->plan.n[0] + 2, c->plan.n[1] + 2, c->plan.n[2] + 2 * zg};
     return jac_get_field_box(c, padded, o, e);
 }
 
@@ -1381,30 +1785,15 @@ int jac_get_region(jac_ctx *c, const int64_t *lo, const int64_t *ext, double *ou
     for (int k = 0; k < 3; ++k)
         if (lo[k] < 0 || ext[k] < 1 || lo[k] + ext[k] > p.n[k])
             return fail(JAC_EINVAL, "region dim %d [%lld, +%lld) outside the interior", k, (long long)lo[k], (long long)ext[k]);
-    CK(cudaSetDevice(c->device));
-    const jac::Geom &g = c->geom;
+    DeviceGuard guard;
     int64_t covered = 0;
-    for (int32_t s = 0; s < c->nslots; ++s) {
-        const jac::DevBlock &d = c->hblocks[s];
-        int64_t a[3], b[3];
-        bool empty = false;
-        for (int k = 0; k < 3; ++k) {
-            a[k] = std::max<int64_t>(lo[k], d.org[k]);
-            b[k] = std::min<int64_t>(lo[k] + ext[k], d.org[k] + p.e[k]);
-            empty |= a[k] >= b[k];
-        }
-        if (empty) continue;
-        covered += (b[0] - a[0]) * (b[1] - a[1]) * (b[2] - a[2]);
-        cudaMemcpy3DParms m{};
-        m.srcPtr = make_cudaPitchedPtr(c->slot_ptr((int)(c->iters & 1), s), (size_t)g.P * 8, (size_t)g.P, (size_t)(g.ey + 2));
-        m.srcPos = make_cudaPos((size_t)(g.A + a[0] - d.org[0]) * 8, (size_t)(1 + a[1] - d.org[1]), (size_t)(g.zg + a[2] - d.org[2]));
-        m.dstPtr = make_cudaPitchedPtr(out, (size_t)ext[0] * 8, (size_t)ext[0], (size_t)ext[1]);
-        m.dstPos = make_cudaPos((size_t)(a[0] - lo[0]) * 8, (size_t)(a[1] - lo[1]), (size_t)(a[2] - lo[2]));
-        m.extent = make_cudaExtent((size_t)(b[0] - a[0]) * 8, (size_t)(b[1] - a[1]), (size_t)(b[2] - a[2]));
-        m.kind = cudaMemcpyDeviceToHost;
-        CK(cudaMemcpy3DAsync(&m, c->stream));
+    int rc;
+    if (c->group) {
+        for (jac_ctx *sc : c->subs)
+            if ((rc = region_copy(sc, lo, ext, out, &covered))) return rc;
+    } else if ((rc = region_copy(c, lo, ext, out, &covered))) {
+        return rc;
     }
-    CK(cudaStreamSynchronize(c->stream));
     if (covered != ext[0] * ext[1] * ext[2]) return fail(JAC_EINVAL, "region is not entirely local to this context");
     return JAC_OK;
 }
@@ -1417,6 +1806,17 @@ int jac_get_layout(const jac_ctx *c, int32_t *gpu_grid, int64_t *block_extent, i
         if (block_extent) block_extent[d] = c->plan.e[d];
     }
     if (iterations_done) *iterations_done = c->iters;
+    return JAC_OK;
+}
+
+int jac_get_grid(const jac_ctx *c, int64_t *n, int32_t *blocks, uint32_t *flags)
+{
+    if (!c) return fail(JAC_EINVAL, "ctx is NULL");
+    for (int d = 0; d < 3; ++d) {
+        if (n) n[d] = c->plan.n[d];
+        if (blocks) blocks[d] = c->plan.b[d];
+    }
+    if (flags) *flags = c->flags;
     return JAC_OK;
 }
 
@@ -1440,6 +1840,26 @@ int jac_last_step_ms(const jac_ctx *c, double *ms)
 int jac_get_stats(const jac_ctx *c, int64_t *st)
 {
     if (!c || !st) return fail(JAC_EINVAL, "ctx/stats is NULL");
+    if (c->group) {  // totals over the devices; kernels per iteration and variant of device 0
+        int64_t sub[JAC_STAT_N];
+        for (int k = 0; k < JAC_STAT_N; ++k) st[k] = 0;
+        for (const jac_ctx *sc : c->subs) {
+            jac_get_stats(sc, sub);
+            for (int k = 0; k < JAC_STAT_N; ++k) st[k] += sub[k];
+        }
+        st[JAC_STAT_EPOCH_MIN] = INT64_MAX;
+        st[JAC_STAT_EPOCH_MAX] = 0;
+        for (const jac_ctx *sc : c->subs) {
+            jac_get_stats(sc, sub);
+            st[JAC_STAT_EPOCH_MIN] = std::min(st[JAC_STAT_EPOCH_MIN], sub[JAC_STAT_EPOCH_MIN]);
+            st[JAC_STAT_EPOCH_MAX] = std::max(st[JAC_STAT_EPOCH_MAX], sub[JAC_STAT_EPOCH_MAX]);
+        }
+        jac_get_stats(c->subs[0], sub);
+        st[JAC_STAT_KERNELS_PER_ITER] = sub[JAC_STAT_KERNELS_PER_ITER];
+        st[JAC_STAT_SWEEP_VARIANT] = sub[JAC_STAT_SWEEP_VARIANT];
+        st[JAC_STAT_FUSED_SYNC] = sub[JAC_STAT_FUSED_SYNC];
+        return JAC_OK;
+    }
     st[JAC_STAT_KERNEL_LAUNCHES] = c->kernel_launches;
     st[JAC_STAT_GRAPH_LAUNCHES] = c->graph_launches;
     st[JAC_STAT_KERNELS_PER_ITER] = c->kernels_per_iter();
@@ -1449,16 +1869,51 @@ int jac_get_stats(const jac_ctx *c, int64_t *st)
     st[JAC_STAT_REMOTE_BYTES] = c->remote_bytes;
     st[JAC_STAT_ARENA_BYTES] = (int64_t)(2 * (size_t)c->nslots * c->geom.bstride * 8);
     st[JAC_STAT_SWEEP_VARIANT] = c->variant;
+    st[JAC_STAT_PARTITIONS] = (int64_t)c->parts.size();
+    st[JAC_STAT_REMOTE_ITEMS] = c->nremote;
+    st[JAC_STAT_FUSED_SYNC] = c->fused ? 1 : 0;
+    // epochs of the hosted partitions' control words (device read; 0 without peers)
+    st[JAC_STAT_EPOCH_MIN] = 0;
+    st[JAC_STAT_EPOCH_MAX] = 0;
+    if (c->ctrl && !c->hsync.empty()) {
+        int64_t lo = INT64_MAX, hi = 0;
+        cudaSetDevice(c->device);
+        for (const jac::PartSync &ps : c->hsync) {
+            uint64_t e = 0;
+            if (cudaMemcpy(&e, ps.ctrl, sizeof e, cudaMemcpyDeviceToHost) != cudaSuccess)
+                return fail(JAC_ECUDA, "jac_get_stats: control word read");
+            lo = std::min<int64_t>(lo, (int64_t)e);
+            hi = std::max<int64_t>(hi, (int64_t)e);
+        }
+        st[JAC_STAT_EPOCH_MIN] = lo;
+        st[JAC_STAT_EPOCH_MAX] = hi;
+    }
+    st[JAC_STAT_EXPERIMENT] = experiment_mask(c);
     return JAC_OK;
 }
 
 int jac_set_option(jac_ctx *c, int32_t option, int64_t value)
 {
     if (!c) return fail(JAC_EINVAL, "ctx is NULL");
+    if (c->group) {
+        for (jac_ctx *sc : c->subs) {
+            const int rc = jac_set_option(sc, option, value);
+            if (rc) return rc;
+        }
+        return JAC_OK;
+    }
     switch (option) {
     case JAC_OPT_LAUNCH_THREADS:
         if (value < 1 || value > 64) return fail(JAC_EINVAL, "JAC_OPT_LAUNCH_THREADS value %lld not in 1..64", (long long)value);
         c->launch_threads = (int)value;
+        return JAC_OK;
+    case JAC_OPT_WATCHDOG_MS:
+        if (value < 0) return fail(JAC_EINVAL, "JAC_OPT_WATCHDOG_MS value %lld < 0", (long long)value);
+        c->watchdog_ns = (uint64_t)value * 1000000ull;  // captured graphs read it at launch: rebuild them
+        for (int s = 0; s < 2; ++s) {
+            if (c->g1[s]) { cudaGraphExecDestroy(c->g1[s]); c->g1[s] = nullptr; }
+            if (c->gU[s]) { cudaGraphExecDestroy(c->gU[s]); c->gU[s] = nullptr; }
+        }
         return JAC_OK;
     default:
         return fail(JAC_EINVAL, "unknown option %d", option);
@@ -1468,6 +1923,13 @@ int jac_set_option(jac_ctx *c, int32_t option, int64_t value)
 int jac_destroy(jac_ctx *c)
 {
     if (!c) return JAC_OK;
+    if (c->group) {  // no device may still store into a neighbour that is being freed
+        DeviceGuard guard;
+        for (jac_ctx *sc : c->subs) { cudaSetDevice(sc->device); cudaStreamSynchronize(sc->stream); }
+        for (jac_ctx *sc : c->subs) jac_destroy(sc);
+        delete c;
+        return JAC_OK;
+    }
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
     for (cudaStream_t s : c->bstreams) if (s) { cudaStreamSynchronize(s); cudaStreamDestroy(s); }
@@ -1485,6 +1947,9 @@ int jac_destroy(jac_ctx *c)
     if (c->stream) cudaStreamDestroy(c->stream);
     if (c->dblocks) cudaFree(c->dblocks);
     if (c->ditem_map) cudaFree(c->ditem_map);
+    if (c->dsync) cudaFree(c->dsync);
+    if (c->dvcopies) cudaFree(c->dvcopies);
+    if (c->status_h) cudaFreeHost(c->status_h);
     if (c->alloc) cudaFree(c->alloc);
     delete c;
     return JAC_OK;

@@ -209,8 +209,9 @@ __device__ __forceinline__ void mbar_fence_init()
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
 
-// Watchdog: a wait that cannot complete (a TMA that never lands, a peer rank that
-// never signals) traps after ~kSpinLimitNs instead of hanging the GPU.
+// Watchdog of the shared-memory ring: a TMA that never lands (a kernel bug, not a
+// timing condition) traps after ~kSpinLimitNs instead of hanging the GPU.  Waits on
+// other partitions use the softer, configurable Watchdog of device.hpp instead.
 constexpr uint64_t kSpinLimitNs = 20ull * 1000 * 1000 * 1000;
 
 __device__ __forceinline__ uint64_t globaltimer_ns()
@@ -288,38 +289,59 @@ __device__ __forceinline__ TileItem decode_item(const SweepArgs &a, int item)
     return decode_item3d(a, item, BX, BY);
 }
 
-// ---- fused cross-rank ordering (see SweepArgs) --------------------------------
-__device__ __forceinline__ void wait_peers(const SweepArgs &a)
+// ---- fused cross-partition ordering (see SweepArgs, PartSync) -------------------
+// Spins until every neighbour partition of `ps` has stored an epoch >= e into its flag
+// word here.  Watchdog: after wd.spin_limit_ns it records kStatusPeerTimeout in the
+// mapped host status word and gives up (the engine turns that into JAC_ECUDA) instead
+// of trapping, so a skewed or dead peer does not poison this CUDA context.
+__device__ __noinline__ void wait_flags(const PartSync &ps, uint64_t e, const Watchdog &wd)
 {
-    const uint64_t e = *reinterpret_cast<volatile uint64_t *>(a.ctrl);  // phases completed here
-    for (int n = 0; n < a.npeers; ++n) {
-        const uint64_t *f = a.ctrl + 1 + a.peer_id[n];
+    for (int n = 0; n < ps.npeers; ++n) {
+        const uint64_t *f = ps.ctrl + 1 + ps.peer_id[n];
         uint64_t v;
         const uint64_t t0 = globaltimer_ns();
         for (;;) {
             asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(f) : "memory");
             if (v >= e) break;
-            if (globaltimer_ns() - t0 > kSpinLimitNs) __trap();
+            if (wd.spin_limit_ns && globaltimer_ns() - t0 > wd.spin_limit_ns) {
+                if (wd.status) {
+                    *reinterpret_cast<volatile uint32_t *>(wd.status) = kStatusPeerTimeout;
+                    __threadfence_system();
+                }
+                return;
+            }
             __nanosleep(100);
         }
     }
+    // The peers' ghost stores were generic-proxy writes; this CTA reads them next with
+    // TMA / bulk copies (async proxy).  The acquire orders them for the generic proxy;
+    // this fence extends the order to the async proxy (PTX memory model, proxies).
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+// Thread 0 of a remote-touching item, before its first staging copy: wait for the
+// neighbours' signal of the phase this partition completed last.
+__device__ __forceinline__ void wait_peers(const SweepArgs &a, const PartSync &ps)
+{
+    const uint64_t e = *reinterpret_cast<volatile const uint64_t *>(ps.ctrl);  // phases completed here
+    wait_flags(ps, e, a.wd);
 }
 
 // All threads of a remote-touching item: after the CTA's last store.  The last such
-// CTA of the launch bumps the epoch and releases it to every neighbour rank.
-__device__ __forceinline__ void signal_done(const SweepArgs &a)
+// CTA of its partition in this launch bumps the partition's epoch and releases it to
+// every neighbour partition.
+__device__ __forceinline__ void signal_done(const PartSync &ps)
 {
     __syncthreads();
     if (threadIdx.x != 0) return;
     __threadfence_system();  // this CTA's stores (peer stores included) before the count
-    unsigned long long *cnt = reinterpret_cast<unsigned long long *>(a.ctrl + kCtrlCounter);
-    if (atomicAdd(cnt, 1ull) == (unsigned long long)a.nremote - 1) {
-        *cnt = 0;
+    if (atomicAdd(ps.count, 1ull) == (unsigned long long)ps.nremote - 1) {
+        *reinterpret_cast<volatile unsigned long long *>(ps.count) = 0;
         __threadfence_system();
-        const uint64_t e = a.ctrl[0] + 1;
-        a.ctrl[0] = e;
-        for (int n = 0; n < a.npeers; ++n)
-            asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(a.peer_slot[n]), "l"(e) : "memory");
+        const uint64_t e = ps.ctrl[0] + 1;
+        *reinterpret_cast<volatile uint64_t *>(ps.ctrl) = e;
+        for (int n = 0; n < ps.npeers; ++n)
+            asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(ps.peer_slot[n]), "l"(e) : "memory");
     }
 }
 
@@ -393,7 +415,7 @@ __global__ void __launch_bounds__(NT, min_ctas_per_sm(NT, NS))
     if (threadIdx.x == 0) {
         const DevBlock &gb = a.blocks[t.b];
         const int slot = gb.slot;
-        if (remote) wait_peers(a);
+        if (remote) wait_peers(a, a.sync[gb.part]);
         c3 = a.src * g.nslots + slot;
         xg0 = xg_array(a.xg, g, a.src, slot, 0) + t.y0;
         xg1 = xg_array(a.xg, g, a.src, slot, 1) + t.y0;
@@ -591,7 +613,7 @@ __global__ void __launch_bounds__(NT, min_ctas_per_sm(NT, NS))
         for (; q <= qlean_end; ++q) plane_general(q);
     }
     if (q <= qlast) plane_general(q);  // z+ face plane
-    if (remote) signal_done(a);
+    if (remote) signal_done(a.sync[blk.part]);
     span_end(a.span);
 }
 
@@ -653,7 +675,7 @@ __global__ void __launch_bounds__(NT, 4) sweep2d_tma_kernel(const __grid_constan
     if (threadIdx.x == 0) {
         const DevBlock &gb = a.blocks[b];
         const int slot = gb.slot;
-        if (remote) wait_peers(a);
+        if (remote) wait_peers(a, a.sync[gb.part]);
         c3 = a.src * g.nslots + slot;
         xg0 = xg_array(a.xg, g, a.src, slot, 0);
         xg1 = xg_array(a.xg, g, a.src, slot, 1);
@@ -761,7 +783,7 @@ __global__ void __launch_bounds__(NT, 4) sweep2d_tma_kernel(const __grid_constan
         for (; q < qend; ++q) tile_general(q);
     }
     if (q < nq) tile_general(q);
-    if (remote) signal_done(a);
+    if (remote) signal_done(a.sync[blk.part]);
     span_end(a.span);
 }
 
@@ -920,22 +942,30 @@ __global__ void barrier_kernel(const BarrierArgs ba)
 {
     if (threadIdx.x != 0) return;
     __threadfence_system();  // the preceding phase's stores (incl. peer stores) first
-    const uint64_t e = ba.ctrl[0] + 1;
-    ba.ctrl[0] = e;
-    for (int n = 0; n < ba.npeers; ++n)
-        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(ba.peer_slot[n]), "l"(e) : "memory");
-    for (int n = 0; n < ba.npeers; ++n) {
-        const uint64_t *f = ba.ctrl + 1 + ba.peer_id[n];
-        uint64_t v;
-        const uint64_t t0 = globaltimer_ns();
-        for (;;) {
-            asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(f) : "memory");
-            if (v >= e) break;
-            if (globaltimer_ns() - t0 > kSpinLimitNs) __trap();
-            __nanosleep(64);
-        }
+    for (int p = 0; p < ba.nparts; ++p) {
+        const PartSync &ps = ba.sync[p];
+        const uint64_t e = ps.ctrl[0] + 1;
+        *reinterpret_cast<volatile uint64_t *>(ps.ctrl) = e;
+        for (int n = 0; n < ps.npeers; ++n)
+            asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(ps.peer_slot[n]), "l"(e) : "memory");
+    }
+    for (int p = 0; p < ba.nparts; ++p) {
+        const PartSync &ps = ba.sync[p];
+        wait_flags(ps, ps.ctrl[0], ba.wd);
     }
     __threadfence_system();
+}
+
+// ------------------------------------------------------------------ virtual transport
+// JAC_F_VIRTUAL_GPUS | JAC_F_NCCL: the packed REMOTE faces move from each partition's
+// send buffer into its neighbour's receive buffer (one list entry per face, the pair
+// an ncclSend / ncclRecv would move); the batched ghost kernel then unpacks them.
+__global__ void __launch_bounds__(256) face_copy_kernel(const FaceCopy *list)
+{
+    const FaceCopy fc = list[blockIdx.y];
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < fc.count;
+         e += (int64_t)gridDim.x * blockDim.x)
+        fc.dst[e] = fc.src[e];
 }
 
 // ------------------------------------------------------------------ init helpers
@@ -1167,6 +1197,14 @@ cudaError_t launch_ghost_fill(const SweepArgs &a, int dst, cudaStream_t s)
 cudaError_t launch_barrier(const BarrierArgs &ba, cudaStream_t s)
 {
     barrier_kernel<<<1, 32, 0, s>>>(ba);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_face_copy(const FaceCopy *list, int n, int64_t maxcount, cudaStream_t s)
+{
+    if (n <= 0) return cudaSuccess;
+    const int64_t gx = std::max<int64_t>(1, std::min<int64_t>(64, (maxcount + 255) / 256));
+    face_copy_kernel<<<dim3((unsigned)gx, (unsigned)n), 256, 0, s>>>(list);
     return cudaGetLastError();
 }
 

@@ -33,6 +33,8 @@ cudaError_t launch_sweep_plain(const SweepArgs &a, cudaStream_t s);  // 64 x 8 t
 cudaError_t launch_sweep_plain_one(const SweepArgs &a, cudaStream_t s);  // a.blocks = one block
 cudaError_t launch_ghost_fill(const SweepArgs &a, int dst, cudaStream_t s);
 cudaError_t launch_barrier(const BarrierArgs &ba, cudaStream_t s);
+// n copies of the device list (virtual-partition transport); maxcount = largest count
+cudaError_t launch_face_copy(const FaceCopy *list, int n, int64_t maxcount, cudaStream_t s);
 cudaError_t launch_pack_face(const SweepArgs &a, int slot, int f, int buf, int par, cudaStream_t s);
 cudaError_t launch_unpack_face(const SweepArgs &a, int slot, int nslot, int f, int buf, int par, cudaStream_t s);
 cudaError_t launch_xghost_extract(const SweepArgs &a, cudaStream_t s);

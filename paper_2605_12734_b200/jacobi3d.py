@@ -30,16 +30,18 @@ JAC_F_SKIP_EXCHANGE = 1 << 7
 JAC_F_PER_BLOCK = 1 << 8
 JAC_F_2D = 1 << 9
 JAC_OPT_LAUNCH_THREADS = 1
+JAC_OPT_WATCHDOG_MS = 2
 JAC_FACE_BOUNDARY, JAC_FACE_LOCAL, JAC_FACE_REMOTE = 0, 1, 2
 STAT_NAMES = ["kernel_launches", "graph_launches", "kernels_per_iter", "local_blocks",
-              "local_faces", "remote_faces", "remote_bytes", "arena_bytes", "sweep_variant"]
+              "local_faces", "remote_faces", "remote_bytes", "arena_bytes", "sweep_variant",
+              "partitions", "remote_items", "fused_sync", "epoch_min", "epoch_max", "experiment"]
 EXPORTED = ["jac_plan", "jac_plan_face", "jac_create", "jac_create_rank", "jac_ipc_handle_bytes",
             "jac_export_ipc", "jac_import_ipc", "jac_set_init", "jac_set_init_hash", "jac_step",
             "jac_get_block", "jac_get_block_padded", "jac_get_field", "jac_get_layout",
             "jac_block_owner", "jac_last_step_ms", "jac_set_init_box", "jac_get_field_box", "jac_local_box",
             "jac_profile_sweep", "jac_last_profile_gap_ms", "jac_get_stats",
             "jac_destroy", "jac_last_error", "jac_version", "jac_set_option", "jac_nccl_id_bytes",
-            "jac_nccl_get_unique_id", "jac_nccl_init", "jac_get_region"]
+            "jac_nccl_get_unique_id", "jac_nccl_init", "jac_get_region", "jac_get_grid"]
 MICROBENCH_EXPORTED = ["jac_mb_launch_latency", "jac_mb_overlap", "jac_mb_launch_rate", "jac_mb_pipeline",
                        "jac_mb_pipeline_batched"]
 
@@ -100,6 +102,7 @@ def load() -> ctypes.CDLL:
         "jac_nccl_get_unique_id": [vp],
         "jac_nccl_init": [vp, vp],
         "jac_get_region": [vp, P(i64), P(i64), dp],
+        "jac_get_grid": [vp, P(i64), P(i32), P(u32)],
         "jac_mb_launch_latency": [i32, i32, P(ctypes.c_double)],
         "jac_mb_overlap": [i32, i64, i32, i32, P(ctypes.c_double), P(ctypes.c_double)],
         "jac_mb_launch_rate": [i32, i32, i32, ctypes.c_double, P(ctypes.c_double)],
@@ -135,6 +138,45 @@ def _grid(g: Optional[Sequence[int]]):
 
 def _dptr(a: np.ndarray):
     return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+def _checked(a: np.ndarray, shape, what: str):
+    """The C side reads / writes exactly prod(shape) doubles at the pointer: refuse any
+    array that is not C-contiguous float64 of exactly that shape (a wrong dtype, a
+    strided view or a short buffer would otherwise be silent heap corruption)."""
+    if not isinstance(a, np.ndarray):
+        raise TypeError(f"{what} must be a numpy array")
+    if a.dtype != np.float64 or not a.flags.c_contiguous:
+        raise ValueError(f"{what} must be a C-contiguous float64 array (got {a.dtype}, "
+                         f"contiguous={a.flags.c_contiguous})")
+    if tuple(int(v) for v in a.shape) != tuple(int(v) for v in shape):
+        raise ValueError(f"{what} has shape {a.shape}, expected {tuple(shape)}")
+    if what.endswith("(writable)") and not a.flags.writeable:
+        raise ValueError(f"{what} is read-only")
+    return _dptr(a)
+
+
+def _grid_info(ctx):
+    """(n = interior dims (x, y, z), b = global blocks, flags) of a context."""
+    n = (ctypes.c_int64 * 3)()
+    b = (ctypes.c_int32 * 3)()
+    f = ctypes.c_uint32()
+    _check(load().jac_get_grid(ctx, n, b, ctypes.byref(f)), "jac_get_grid")
+    return tuple(n), tuple(b), f.value
+
+
+def _padded_shape(ctx):
+    n, _, flags = _grid_info(ctx)
+    zg = 0 if flags & JAC_F_2D else 1
+    return (n[2] + 2 * zg, n[1] + 2, n[0] + 2)
+
+
+def _block_shape(ctx, padded=False):
+    _, e, _ = jac_get_layout(ctx)
+    _, _, flags = _grid_info(ctx)
+    if not padded:
+        return (e[2], e[1], e[0])
+    return (e[2] + (0 if flags & JAC_F_2D else 2), e[1] + 2, e[0] + 2)
 
 
 # ------------------------------------------------------------------ C-ABI mirrors
@@ -194,9 +236,7 @@ def jac_nccl_init(ctx, uid: bytes) -> None:
 
 
 def jac_set_init(ctx, padded: np.ndarray) -> None:
-    if padded.dtype != np.float64 or not padded.flags.c_contiguous:
-        raise ValueError("padded must be C-contiguous float64")
-    _check(load().jac_set_init(ctx, _dptr(padded)), "jac_set_init")
+    _check(load().jac_set_init(ctx, _checked(padded, _padded_shape(ctx), "padded")), "jac_set_init")
 
 
 def jac_set_init_hash(ctx, seed: int) -> None:
@@ -208,17 +248,20 @@ def jac_step(ctx, n_iters: int) -> None:
 
 
 def jac_get_block(ctx, ix, iy, iz, out: np.ndarray) -> np.ndarray:
-    _check(load().jac_get_block(ctx, ix, iy, iz, _dptr(out)), "jac_get_block")
+    p = _checked(out, _block_shape(ctx), "out (writable)")
+    _check(load().jac_get_block(ctx, ix, iy, iz, p), "jac_get_block")
     return out
 
 
 def jac_get_block_padded(ctx, ix, iy, iz, out: np.ndarray) -> np.ndarray:
-    _check(load().jac_get_block_padded(ctx, ix, iy, iz, _dptr(out)), "jac_get_block_padded")
+    p = _checked(out, _block_shape(ctx, padded=True), "out (writable)")
+    _check(load().jac_get_block_padded(ctx, ix, iy, iz, p), "jac_get_block_padded")
     return out
 
 
 def jac_get_field(ctx, padded: np.ndarray) -> np.ndarray:
-    _check(load().jac_get_field(ctx, _dptr(padded)), "jac_get_field")
+    p = _checked(padded, _padded_shape(ctx), "padded (writable)")
+    _check(load().jac_get_field(ctx, p), "jac_get_field")
     return padded
 
 
@@ -229,15 +272,19 @@ def _i64x3(v):
 def jac_set_init_box(ctx, box: np.ndarray, origin) -> None:
     """``box`` is a [sz, sy, sx] float64 sub-array of the padded grid starting at
     padded cell ``origin`` = (ox, oy, oz)."""
-    if box.dtype != np.float64 or not box.flags.c_contiguous or box.ndim != 3:
-        raise ValueError("box must be a C-contiguous float64 3-D array")
+    if not isinstance(box, np.ndarray) or box.ndim != 3:
+        raise ValueError("box must be a 3-D numpy array [sz, sy, sx]")
+    p = _checked(box, box.shape, "box")
     ext = (box.shape[2], box.shape[1], box.shape[0])
-    _check(load().jac_set_init_box(ctx, _dptr(box), _i64x3(origin), _i64x3(ext)), "jac_set_init_box")
+    _check(load().jac_set_init_box(ctx, p, _i64x3(origin), _i64x3(ext)), "jac_set_init_box")
 
 
 def jac_get_field_box(ctx, box: np.ndarray, origin) -> np.ndarray:
+    if not isinstance(box, np.ndarray) or box.ndim != 3:
+        raise ValueError("box must be a 3-D numpy array [sz, sy, sx]")
+    p = _checked(box, box.shape, "box (writable)")
     ext = (box.shape[2], box.shape[1], box.shape[0])
-    _check(load().jac_get_field_box(ctx, _dptr(box), _i64x3(origin), _i64x3(ext)), "jac_get_field_box")
+    _check(load().jac_get_field_box(ctx, p, _i64x3(origin), _i64x3(ext)), "jac_get_field_box")
     return box
 
 
@@ -380,9 +427,9 @@ class Jacobi3D:
         return jac_get_block_padded(self.ctx, ix, iy, iz, np.empty((ez + 2, ey + 2, ex + 2), dtype=np.float64))
 
     def field(self, like: np.ndarray) -> np.ndarray:
-        """Padded array: shell/non-local cells copied from ``like``, local interiors
-        from the device."""
-        out = np.array(like, dtype=np.float64, copy=True)
+        """Padded array: shell/non-local cells copied from ``like`` (which must have the
+        padded shape), local interiors from the device."""
+        out = np.array(like, dtype=np.float64, copy=True, order="C")
         return jac_get_field(self.ctx, out)
 
     def region(self, lo, ext) -> np.ndarray:

@@ -45,7 +45,13 @@ def test_library_is_in_tree_and_built_for_sm100a():
 
 def test_header_struct_sizes_match_binding():
     assert jb.jac_ipc_handle_bytes() == 256
-    assert len(J.STAT_NAMES) == 9
+    src = open(os.path.join(ROOT, "include", "jacobi3d.h")).read()
+    assert len(J.STAT_NAMES) == int(re.search(r"JAC_STAT_N\s*=\s*(\d+)", src).group(1))
+    # the binding's names follow the header's enum order
+    names = re.findall(r"JAC_STAT_([A-Z_]+)\s*=\s*(\d+)", src)
+    for name, idx in names:
+        if name != "N":
+            assert J.STAT_NAMES[int(idx)] == name.lower(), (name, idx)
 
 
 @pytest.mark.parametrize("args,code", [

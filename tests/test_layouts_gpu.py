@@ -21,6 +21,7 @@ def _bits_equal(a, b):
                                          ((512, 64, 48), (2, 2, 1)), ((48, 40, 24), (3, 1, 2))])
 def test_both_layouts_bit_exact(monkeypatch, dense, dims, blocks):
     if not dense:
+        monkeypatch.setenv("JAC_EXPERIMENT", "1")
         monkeypatch.setenv("JAC_NO_DENSE", "1")
     u0 = JI.hash_field(*dims, seed=2)
     with jb.Jacobi3D(dims, blocks) as s:
@@ -64,6 +65,7 @@ def test_block_padded_corners():
 def test_programmatic_dependent_launch_on_off(monkeypatch, pdl, dims, blocks, flags):
     """Sweeps with and without programmatic dependent launch (JAC_PDL) give the same
     bits: every CTA waits on griddepcontrol before touching a buffer."""
+    monkeypatch.setenv("JAC_EXPERIMENT", "1")
     monkeypatch.setenv("JAC_PDL", pdl)
     if flags:
         u0 = JI.hash_field2d(dims[0], dims[1], seed=3)

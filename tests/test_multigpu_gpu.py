@@ -62,3 +62,69 @@ def test_multi_process_parity(case):
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "OK" in r.stdout
+
+
+# ---------------------------------------------------------------- single process, N GPUs
+# jac_create(n_gpus > 1): one process drives every GPU; the
+# sub-contexts run the rank path with plain peer pointers.
+SP_CASES = [
+    # (n_gpus, dims, blocks, grid, iters, flags, hash)
+    (2, (64, 48, 80), (2, 2, 4), None, 21, 0, False),         # 1x1x2, ODF 8
+    (2, (128, 40, 36), (2, 1, 1), (2, 1, 1), 9, 0, True),     # x split: remote x-ghost arrays
+    (2, (48, 48, 48), (2, 2, 2), None, 11, 1 << 4, False),    # unfused pack + barrier + pull
+    (2, (48, 48, 48), (2, 2, 2), None, 5, 1 << 1, False),     # no graph (interleaved launches)
+    (2, (64, 64, 64), (2, 2, 2), None, 6, 1 << 5, False),     # plain-load sweep + barrier
+    (4, (64, 64, 64), (2, 2, 4), None, 13, 0, False),         # 1x2x2
+    (4, (256, 128, 48), (2, 2, 1), (2, 2, 1), 7, 0, True),    # lean tiles, x and y splits
+    (8, (64, 64, 64), (4, 4, 4), None, 17, 0, False),         # 2x2x2
+]
+
+
+@pytest.mark.parametrize("case", SP_CASES, ids=[f"sp_n{c[0]}_{c[2]}_{c[5]}" for c in SP_CASES])
+def test_single_process_multi_gpu_parity(case):
+    import numpy as np
+
+    sys.path.insert(0, ROOT)
+    import jac_inputs as JI
+    import oracle
+    import paper_2605_12734_b200 as jb
+
+    n, dims, blocks, grid, iters, flags, hashed = case
+    if _ngpu() < n:
+        pytest.skip(f"needs {n} GPUs")
+    u0 = JI.hash_field(*dims, seed=2)
+    with jb.Jacobi3D(dims, blocks, n_gpus=n, gpu_grid=grid, flags=flags) as s:
+        if hashed:
+            s.set_init_hash(2)
+        else:
+            s.set_init(u0)
+        for k in (3, 1, iters - 4):
+            s.step(k)
+        got = s.field(u0)
+        st = s.stats()
+        blk = s.block(blocks[0] - 1, blocks[1] - 1, blocks[2] - 1)  # owned by the last device
+    want = oracle.jacobi3d_omp(u0, iters)[0]
+    assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
+    ex, ey, ez = (dims[d] // blocks[d] for d in range(3))
+    assert np.array_equal(blk, want[-ez - 1:-1, -ey - 1:-1, -ex - 1:-1])
+    assert st["partitions"] == n and st["remote_faces"] > 0
+    if flags == 0:
+        assert st["fused_sync"] == 1 and st["epoch_min"] == st["epoch_max"] == 2 + iters
+
+
+def test_single_process_multi_gpu_2d():
+    import numpy as np
+
+    sys.path.insert(0, ROOT)
+    import jac_inputs as JI
+    import oracle
+    import paper_2605_12734_b200 as jb
+
+    if _ngpu() < 2:
+        pytest.skip("needs 2 GPUs")
+    u0 = JI.hash_field2d(256, 192, seed=1)
+    with jb.Jacobi2D((256, 192), (2, 4), n_gpus=2) as s:
+        s.set_init(u0)
+        s.step(13)
+        got = s.field(u0)
+    assert np.array_equal(got.view(np.uint64), oracle.jacobi2d_omp(u0, 13)[0].view(np.uint64))

@@ -18,6 +18,7 @@ pytestmark = pytest.mark.gpu
 N_CASES = 32
 _VARIANTS = [None, None, None, "0", "5", "1", "3", "4", "12", "13", "14"]
 _FLAGS = [0, 0, 0, J.JAC_F_NO_GRAPH, J.JAC_F_UNFUSED_PACK, J.JAC_F_FMA, J.JAC_F_NO_TMA]
+_VFLAGS = [0, 0, J.JAC_F_NCCL, J.JAC_F_NO_GRAPH, J.JAC_F_UNFUSED_PACK, J.JAC_F_NO_TMA]
 
 
 def make_case(seed):
@@ -45,8 +46,8 @@ def make_case(seed):
                 pass
         n_gpus = int(rng.choice(cands)) if cands else 1
     flags = int(rng.choice(_FLAGS))
-    if n_gpus > 1:
-        flags = (flags & ~J.JAC_F_NO_TMA) | J.JAC_F_VIRTUAL_GPUS
+    if n_gpus > 1:  # virtual partitions: the remote path (virtual NCCL layout included)
+        flags = int(rng.choice(_VFLAGS)) | J.JAC_F_VIRTUAL_GPUS
     variant = _VARIANTS[int(rng.integers(0, len(_VARIANTS)))]
     return tuple(dims), tuple(b), n_gpus, flags, variant, int(rng.integers(1, 12))
 
@@ -55,6 +56,7 @@ def make_case(seed):
 def test_fuzz_parity(monkeypatch, seed):
     dims, blocks, n_gpus, flags, variant, iters = make_case(seed)
     if variant is not None:
+        monkeypatch.setenv("JAC_EXPERIMENT", "1")
         monkeypatch.setenv("JAC_VARIANT", variant)
     u0 = JI.hash_field(*dims, seed=1 + seed % 3)
     with jb.Jacobi3D(dims, blocks, n_gpus=n_gpus, flags=flags) as s:

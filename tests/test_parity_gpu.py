@@ -208,6 +208,7 @@ def test_tma_tile_variants(monkeypatch, variant, dims, blocks):
     """Every TMA tile variant (wide 64+halo, narrow 32+halo, exact 32, exact 64) on
     block widths 32, 64, 29 and 130, forced through JAC_VARIANT (ignored where the
     variant cannot cover the block row)."""
+    monkeypatch.setenv("JAC_EXPERIMENT", "1")
     monkeypatch.setenv("JAC_VARIANT", variant)
     u0 = JI.hash_field(*dims, seed=3)
     assert_bits(run(u0, blocks, 5), ref(u0, 5))
