@@ -294,7 +294,7 @@ __device__ __forceinline__ TileItem decode_item(const SweepArgs &a, int item)
 // word here.  Watchdog: after wd.spin_limit_ns it records kStatusPeerTimeout in the
 // mapped host status word and gives up (the engine turns that into JAC_ECUDA) instead
 // of trapping, so a skewed or dead peer does not poison this CUDA context.
-__device__ __noinline__ void wait_flags(const PartSync &ps, uint64_t e, const Watchdog &wd)
+__device__ __forceinline__ void wait_flags(const PartSync &ps, uint64_t e, const Watchdog &wd)
 {
     for (int n = 0; n < ps.npeers; ++n) {
         const uint64_t *f = ps.ctrl + 1 + ps.peer_id[n];

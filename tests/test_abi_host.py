@@ -43,6 +43,22 @@ def test_library_is_in_tree_and_built_for_sm100a():
     assert "sm_100a" in out
 
 
+def test_tma_kernels_have_no_stack_frame():
+    """Every TMA sweep instantiation runs without a stack frame (STACK:0).  Measured on
+    B200: a non-inlined call inside the 3-D sweep (STACK:240) gave sporadic stale
+    32-point row segments at 512^3 while the same code inlined was bit-exact, so a call
+    or spill that forces a frame is treated as a defect."""
+    import subprocess
+    out = subprocess.run(["cuobjdump", "-res-usage", J.lib_path()], capture_output=True, text=True).stdout
+    lines = out.splitlines()
+    seen = 0
+    for i, ln in enumerate(lines):
+        if "Function" in ln and ("sweep_tma_kernel" in ln or "sweep2d_tma_kernel" in ln):
+            seen += 1
+            assert "STACK:0 " in lines[i + 1], (ln, lines[i + 1])
+    assert seen >= 16
+
+
 def test_header_struct_sizes_match_binding():
     assert jb.jac_ipc_handle_bytes() == 256
     src = open(os.path.join(ROOT, "include", "jacobi3d.h")).read()
