@@ -20,10 +20,13 @@ uniform dense fp64 grid, fixed iteration count, no convergence check, PAPER.md:2
   j2d           NEXT-1: the paper's Jacobi2D, 32768^2 per GPU, ODF --odf, weak.
 Inputs are larger than L2 (>= 2 x 1.07 GB per GPU), so no L2 flush is needed.
 
-N > 1: launched by torchrun, one process per GPU; ranks exchange IPC records once
+N > 1 under torchrun: one process per GPU; ranks exchange IPC records once
 (torch.distributed, plumbing only) and faces move by peer stores inside the sweep
 kernel; the timed region is bracketed by barrier + cuda synchronize, the device
 time (CUDA events on the launching stream) is max-reduced over ranks.
+N > 1 without torchrun (plain ``python bench.py --gpus N``): one process drives all N
+GPUs through ``jac_create(n_gpus=N)`` -- the same sweep kernels and in-kernel peer
+stores, with plain peer pointers; the device time is the max over the N devices.
 
 --impl reference: the CPU oracle (oracle/, OpenMP over z on all host cores) timed
 on a bounded sample of the same workload -- the per-GPU 512^3 box, one iteration
@@ -44,6 +47,7 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 MODE_2D = [False]  # set for --config j2d
+SP_GPUS = [1]  # GPUs driven by this one process (single-process multi-GPU: jac_create(n_gpus))
 _JSON_OUT = [None]  # the process's original stdout: the JSON line goes there, nothing else
 
 
@@ -142,7 +146,7 @@ def workload(cfg, n, odf):
 
 # ------------------------------------------------------------------ clocks (NVML)
 class ClockSampler:
-    """Samples SM clock and clock-event reasons of one GPU every ~2 ms (NVML)."""
+    """Samples SM clock and clock-event reasons of one or more GPUs every ~2 ms (NVML)."""
 
     REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
                0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x2: "applications_clocks_setting",
@@ -152,32 +156,34 @@ class ClockSampler:
         self.ok = False
         self.samples, self.reasons = [], 0
         self.mem_samples, self.temps, self.power = [], [], []
+        idxs = list(cuda_index) if isinstance(cuda_index, (list, tuple)) else [cuda_index]
         try:
             import pynvml as N
             N.nvmlInit()
             vis = os.environ.get("CUDA_VISIBLE_DEVICES")
-            idx = int(vis.split(",")[cuda_index]) if vis else cuda_index
-            self.N, self.h = N, N.nvmlDeviceGetHandleByIndex(idx)
-            self.max_mhz = N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM)
+            phys = [int(vis.split(",")[i]) if vis else i for i in idxs]
+            self.N, self.hs = N, [N.nvmlDeviceGetHandleByIndex(i) for i in phys]
+            self.max_mhz = N.nvmlDeviceGetMaxClockInfo(self.hs[0], N.NVML_CLOCK_SM)
             self.ok = True
         except Exception as e:  # noqa: BLE001
             self.err = str(e)
 
     def _run(self):
-        N, h = self.N, self.h
+        N = self.N
         while not self._stop.is_set():
-            try:
-                self.samples.append(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM))
-                self.mem_samples.append(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_MEM))
-                self.temps.append(N.nvmlDeviceGetTemperature(h, 0))
-                self.power.append(N.nvmlDeviceGetPowerUsage(h) / 1000.0)
+            for h in self.hs:
                 try:
-                    r = N.nvmlDeviceGetCurrentClocksEventReasons(h)
-                except AttributeError:
-                    r = N.nvmlDeviceGetCurrentClocksThrottleReasons(h)
-                self.reasons |= int(r)
-            except Exception:  # noqa: BLE001
-                pass
+                    self.samples.append(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM))
+                    self.mem_samples.append(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_MEM))
+                    self.temps.append(N.nvmlDeviceGetTemperature(h, 0))
+                    self.power.append(N.nvmlDeviceGetPowerUsage(h) / 1000.0)
+                    try:
+                        r = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    except AttributeError:
+                        r = N.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                    self.reasons |= int(r)
+                except Exception:  # noqa: BLE001
+                    pass
             time.sleep(0.002)
 
     def __enter__(self):
@@ -196,7 +202,7 @@ class ClockSampler:
         if not self.ok:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "error": getattr(self, "err", "")}
         return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
-                "sm_max_mhz": self.max_mhz, "samples": len(self.samples),
+                "sm_max_mhz": self.max_mhz, "samples": len(self.samples), "gpus_sampled": len(self.hs),
                 "mem_mhz": statistics.median(self.mem_samples) if self.mem_samples else None,
                 "gpu_temp_c_max": max(self.temps) if self.temps else None,
                 "power_w_max": max(self.power) if self.power else None,
@@ -275,8 +281,44 @@ class Dist:
 
 
 # ------------------------------------------------------------------ CPU oracle timing
-def cpu_oracle(box=(512, 512, 512), n_target=None, budget_s=15.0, steps=None, warmup=0):
-    """Times the oracle as it stands (OpenMP over z, all host cores, iteration loop only)."""
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def cpu_oracle_serial(u0, budget_s=8.0, steps=None):
+    """SURVEY §8(d.4) mode (a): the single-threaded oracle as defined (the serial C loop),
+    pinned to one core (sched_setaffinity, the in-process `taskset -c 0`)."""
+    import oracle
+
+    nz2, ny2, nx2 = u0.shape
+    pts = (nx2 - 2) * (ny2 - 2) * (nz2 - 2)
+    old = os.sched_getaffinity(0)
+    core = min(old)
+    os.sched_setaffinity(0, {core})
+    try:
+        if steps is None:
+            _, t1 = oracle.jacobi3d_timed(u0, 1)
+            n = max(1, min(20, int(budget_s / max(t1, 1e-6))))
+        else:
+            n = steps
+        _, secs = oracle.jacobi3d_timed(u0, n)
+    finally:
+        os.sched_setaffinity(0, old)
+    return {"value": pts * n / secs / 1e9, "unit": "GLUP/s", "cores": 1, "threads": 1, "pinned_core": core,
+            "iterations": n, "ms_per_iter": 1e3 * secs / n,
+            "sample": f"{nx2 - 2}x{ny2 - 2}x{nz2 - 2} grid, {n} iterations, serial oracle on one pinned core"}
+
+
+def cpu_oracle(box=(512, 512, 512), n_target=None, budget_s=15.0, steps=None, warmup=0, serial=True):
+    """Times the oracle as it stands: mode (b) OpenMP over z on all host cores (the
+    headline CPU baseline) and mode (a) the serial oracle on one pinned core (SURVEY
+    §8(d.4)); iteration loops only."""
     import jac_inputs as JI
     import oracle
 
@@ -292,9 +334,13 @@ def cpu_oracle(box=(512, 512, 512), n_target=None, budget_s=15.0, steps=None, wa
         n = steps
     _, threads, secs = oracle.jacobi3d_omp_timed(u0, n, cores)
     glups = nx * ny * nz * n / secs / 1e9
-    return {"value": glups, "unit": "GLUP/s", "cores": threads, "kind": "oracle",
-            "sample": f"{nx}x{ny}x{nz} grid (the per-GPU C2 box), {n} iterations, OpenMP over z on {threads} "
-                      f"threads, iteration loop only", "ms_per_iter": 1e3 * secs / n, "nproc": os.cpu_count()}
+    out = {"value": glups, "unit": "GLUP/s", "cores": threads, "kind": "oracle", "mode": "b: OpenMP over z, all cores",
+           "sample": f"{nx}x{ny}x{nz} grid (the per-GPU C2 box), {n} iterations, OpenMP over z on {threads} "
+                     f"threads, iteration loop only", "ms_per_iter": 1e3 * secs / n, "nproc": os.cpu_count(),
+           "cpu_model": cpu_model(), "threads": threads}
+    if serial:
+        out["single_thread"] = cpu_oracle_serial(u0, budget_s=min(10.0, budget_s))
+    return out
 
 
 def cpu_oracle_2d(box=(8192, 8192), steps=None, warmup=0, budget_s=15.0):
@@ -316,7 +362,7 @@ def cpu_oracle_2d(box=(8192, 8192), steps=None, warmup=0, budget_s=15.0):
     return {"value": nx * ny * n / secs / 1e9, "unit": "GLUP/s", "cores": threads, "kind": "oracle",
             "sample": f"{nx}x{ny} 2-D grid, {n} iterations, OpenMP over y on {threads} threads, "
                       f"iteration loop only", "ms_per_iter": 1e3 * secs / n,
-            "nproc": os.cpu_count()}
+            "nproc": os.cpu_count(), "cpu_model": cpu_model(), "threads": threads}
 
 
 def run_reference(args, D):
@@ -339,7 +385,7 @@ def run_reference(args, D):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (R11 splitmix64 hash, seed 1)",
             "config": {"workload": label, "global_dims": dims, "sample_dims": box},
             "cpu_baseline": {"kind": "oracle", "cores": cb["cores"], "sample": cb["sample"], "value": cb["value"],
-                             "unit": "GLUP/s"},
+                             "unit": "GLUP/s", "cpu_model": cb.get("cpu_model"), "threads": cb.get("threads")},
             "e2e": {"value": cb["value"], "unit": "GLUP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     emit(line)
     D.finish()
@@ -386,7 +432,8 @@ def make_ctx(dims, blocks, g, D, flags=0):
     if D.world > 1:
         from paper_2605_12734_b200.dist import create_rank_context
         return create_rank_context(dims, blocks, gpu_grid=g, flags=flags, device=D.local)
-    return jb.Jacobi3D(dims, blocks, n_gpus=1, gpu_grid=g, flags=flags)
+    # one process: jac_create(n_gpus) drives every GPU (n_gpus = 1: the plain context)
+    return jb.Jacobi3D(dims, blocks, n_gpus=SP_GPUS[0], gpu_grid=g, flags=flags)
 
 
 def close_ctx(J, D):
@@ -416,7 +463,8 @@ def run_ours(args, D):
     # ---- headline: timed region
     J = make_ctx(dims, blocks, g, D)
     J.set_init_hash(1)
-    sampler = ClockSampler(D.local)
+    my_gpus = list(range(SP_GPUS[0])) if SP_GPUS[0] > 1 else D.local
+    sampler = ClockSampler(my_gpus)
     dev_ms, launches = time_ctx(J, K, W, D, sampler)
     rank_ms = D.gather(J.last_step_ms())  # each rank's own device time (value uses the max)
     value = pts * K / (dev_ms * 1e-3) / 1e9
@@ -438,7 +486,7 @@ def run_ours(args, D):
     if not args.no_sustained:
         settle = int(min(20000, max(50, 1500.0 / ms_iter)))
         ks = int(min(5000, max(20, 300.0 / ms_iter)))
-        s_sampler = ClockSampler(D.local)
+        s_sampler = ClockSampler(my_gpus)
         ms_s, _ = time_ctx(J, ks, settle, D, s_sampler, cool_first=False)
         sustained = {"value": pts * ks / (ms_s * 1e-3) / 1e9, "unit": "GLUP/s", "ms_per_step": ms_s / ks,
                      "settle_iters": settle, "timed_iters": ks,
@@ -456,13 +504,15 @@ def run_ours(args, D):
     nccl_ablation = None
     if D.world > 1:
         EXTRA["rank_ms_per_step"] = [m / K for m in rank_ms]
-    if D.world > 1 and not args.no_sweep:  # NCCL send/recv of packed faces instead of peer stores
-        Jn = make_ctx(dims, blocks, g, D, flags=JB.JAC_F_NCCL)
-        Jn.set_init_hash(1)
-        ms_n, _ = time_ctx(Jn, K, W, D)
-        nccl_ablation = {"nccl_sendrecv": {"ms_per_iter": ms_n / K, "glups": pts * K / (ms_n * 1e-3) / 1e9,
-                                           "vs_peer_stores": ms_n / K / ms_iter}}
-        close_ctx(Jn, D)
+    if args.gpus > 1 and not args.no_sweep:
+        nccl_ablation = {}
+        if D.world > 1:  # NCCL send/recv of packed faces instead of peer stores (rank contexts)
+            Jn = make_ctx(dims, blocks, g, D, flags=JB.JAC_F_NCCL)
+            Jn.set_init_hash(1)
+            ms_n, _ = time_ctx(Jn, K, W, D)
+            nccl_ablation["nccl_sendrecv"] = {"ms_per_iter": ms_n / K, "glups": pts * K / (ms_n * 1e-3) / 1e9,
+                                              "vs_peer_stores": ms_n / K / ms_iter}
+            close_ctx(Jn, D)
         # exchange share: exposed exchange = t(default) - t(skip);
         # no-overlap = faces packed by the sweep, pulled by a ghost-fill pass after a
         # cross-rank barrier (JAC_F_UNFUSED_PACK)
@@ -501,7 +551,7 @@ def run_e2e(J, D, dims, origin, extent, pts, pts_gpu, K):
     e2e_s = D.max(time.perf_counter() - t0)
     e2e_val = pts * K / e2e_s / 1e9
     h2d = host_in.nbytes
-    d2h = pts_gpu * 8
+    d2h = (pts if SP_GPUS[0] > 1 else pts_gpu) * 8  # interiors this process reads back
     close_ctx(J, D)
     return e2e_val, h2d, d2h
 
@@ -606,9 +656,14 @@ def finish_ours(args, D, K, W, dims, blocks, g, label, scaling, pts, pts_gpu, pe
             "clocks": sampler.summary(),
             "sustained_power_capped": sustained,
             "cpu_baseline": cpu,
-            "exchange": {"remote_faces_per_gpu": st["remote_faces"], "remote_bytes_per_iter": st["remote_bytes"],
-                         "nvlink_ideal_us": st["remote_bytes"] / 900e9 * 1e6,
-                         "nvlink_share_ideal": st["remote_bytes"] / 900e9 / (ms_iter * 1e-3)},
+            "exchange": {"remote_faces_per_gpu": st["remote_faces"] / SP_GPUS[0],
+                         "remote_bytes_per_iter": st["remote_bytes"] / SP_GPUS[0],
+                         "nvlink_ideal_us": st["remote_bytes"] / SP_GPUS[0] / 900e9 * 1e6,
+                         "nvlink_share_ideal": st["remote_bytes"] / SP_GPUS[0] / 900e9 / (ms_iter * 1e-3)},
+            "launch": ("torchrun: one process per GPU (rank contexts, IPC peer pointers)" if D.world > 1 else
+                       f"one process driving {SP_GPUS[0]} GPU(s) (jac_create n_gpus={SP_GPUS[0]})"),
+            "regime": ("headline = K iterations after W warm-ups and a 0.25 s idle: mostly the uncapped-clock "
+                       "burst; sustained_power_capped = the same context at the 1000 W power-cap equilibrium"),
         }
         if sweep is not None:
             line["odf_sweep"] = sweep
@@ -641,8 +696,8 @@ def main():
     if D.world != args.gpus:
         if D.world > 1:
             raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={D.world}")
-        if args.gpus > 1 and args.impl == "ours":
-            raise SystemExit("--gpus N>1 must be launched with torchrun (one process per GPU)")
+        # plain `python bench.py --gpus N`: this one process drives the N GPUs
+        SP_GPUS[0] = args.gpus
     if args.impl == "reference":
         run_reference(args, D)
     else:

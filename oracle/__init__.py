@@ -49,6 +49,8 @@ def lib() -> ctypes.CDLL:
         i64, dp = ctypes.c_int64, ctypes.POINTER(ctypes.c_double)
         L.oracle_jacobi3d.argtypes = [i64, i64, i64, dp, i64, dp]
         L.oracle_jacobi3d.restype = ctypes.c_int
+        L.oracle_jacobi3d_timed.argtypes = [i64, i64, i64, dp, i64, dp, ctypes.POINTER(ctypes.c_double)]
+        L.oracle_jacobi3d_timed.restype = ctypes.c_int
         L.oracle_jacobi3d_omp.argtypes = [i64, i64, i64, dp, i64, dp, ctypes.c_int]
         L.oracle_jacobi3d_omp.restype = ctypes.c_int
         L.oracle_jacobi3d_omp_timed.argtypes = [i64, i64, i64, dp, i64, dp, ctypes.c_int,
@@ -88,6 +90,18 @@ def jacobi3d(u0: np.ndarray, n: int) -> np.ndarray:
     if rc != 0:
         raise RuntimeError(f"oracle_jacobi3d failed rc={rc}")
     return out
+
+
+def jacobi3d_timed(u0: np.ndarray, n: int):
+    """Single-threaded oracle (as ``jacobi3d``); returns (field, seconds of the
+    iteration loop alone) -- the CPU baseline's mode (a)."""
+    nx, ny, nz = _dims(u0)
+    out = np.empty_like(u0)
+    secs = ctypes.c_double()
+    rc = lib().oracle_jacobi3d_timed(nx, ny, nz, _ptr(u0), int(n), _ptr(out), ctypes.byref(secs))
+    if rc != 0:
+        raise RuntimeError(f"oracle_jacobi3d_timed failed rc={rc}")
+    return out, secs.value
 
 
 def jacobi3d_omp(u0: np.ndarray, n: int, nthreads: int = 0):

@@ -69,9 +69,12 @@ static void sweep(int64_t nx, int64_t ny, int64_t nz, const double *A, double *B
 }
 
 /* Returns 0 on success, -1 on bad arguments, -2 on allocation failure.
- * u0 and out are host arrays of padded size; they may alias. */
-int oracle_jacobi3d(int64_t nx, int64_t ny, int64_t nz, const double *u0, int64_t n,
-                    double *out)
+ * u0 and out are host arrays of padded size; they may alias.  *loop_seconds (if
+ * non-NULL) receives the wall time of the iteration loop alone (the bench's
+ * single-threaded CPU baseline, SURVEY §8(d.4) mode (a)); timing only. */
+static double now_s(void);
+int oracle_jacobi3d_timed(int64_t nx, int64_t ny, int64_t nz, const double *u0, int64_t n,
+                          double *out, double *loop_seconds)
 {
     if (nx < 1 || ny < 1 || nz < 1 || n < 0 || !u0 || !out) return -1;
     const size_t cells = (size_t)(nx + 2) * (size_t)(ny + 2) * (size_t)(nz + 2);
@@ -80,13 +83,21 @@ int oracle_jacobi3d(int64_t nx, int64_t ny, int64_t nz, const double *u0, int64_
     if (!A || !B) { free(A); free(B); return -2; }
     memcpy(A, u0, cells * sizeof(double));
     memcpy(B, u0, cells * sizeof(double)); /* shell identical in both, never written */
+    const double t0 = now_s();
     for (int64_t it = 0; it < n; ++it) {
         sweep(nx, ny, nz, A, B, 1, nz);
         double *t = A; A = B; B = t;
     }
+    if (loop_seconds) *loop_seconds = now_s() - t0;
     memcpy(out, A, cells * sizeof(double));
     free(A); free(B);
     return 0;
+}
+
+int oracle_jacobi3d(int64_t nx, int64_t ny, int64_t nz, const double *u0, int64_t n,
+                    double *out)
+{
+    return oracle_jacobi3d_timed(nx, ny, nz, u0, n, out, 0);
 }
 
 /* Same iteration with the k-loop split over OpenMP threads.

@@ -423,8 +423,8 @@ class Jacobi3D:
         return jac_get_block(self.ctx, ix, iy, iz, np.empty((ez, ey, ex), dtype=np.float64))
 
     def block_padded(self, ix, iy, iz) -> np.ndarray:
-        ex, ey, ez = self.block_extent
-        return jac_get_block_padded(self.ctx, ix, iy, iz, np.empty((ez + 2, ey + 2, ex + 2), dtype=np.float64))
+        shape = _block_shape(self.ctx, padded=True)  # (ez+2, ey+2, ex+2); one plane in 2-D
+        return jac_get_block_padded(self.ctx, ix, iy, iz, np.empty(shape, dtype=np.float64))
 
     def field(self, like: np.ndarray) -> np.ndarray:
         """Padded array: shell/non-local cells copied from ``like`` (which must have the

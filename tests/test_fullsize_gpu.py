@@ -87,3 +87,39 @@ def test_j2d_32768_full_size():
             sub = JI.hash_values(1, ys * np.uint64(nx + 2) + xs)
             res, _ = oracle.jacobi2d_omp(np.ascontiguousarray(sub), n)
             bits(got, res[y0 - a[1] + 1:y0 - a[1] + 1 + s, x0 - a[0] + 1:x0 - a[0] + 1 + s])
+
+
+# ---------------------------------------------------------------- full memcmp
+C2_ODF_BLOCKS = {1: (1, 1, 1), 2: (1, 1, 2), 4: (1, 2, 2), 8: (2, 2, 2), 16: (2, 2, 4), 32: (2, 4, 4),
+                 64: (4, 4, 4), 512: (8, 8, 8), 4096: (16, 16, 16)}
+
+
+def _full_run(dims, blocks, n, like):
+    with jb.Jacobi3D(dims, blocks) as s:
+        s.set_init_hash(1)
+        s.step(n)
+        return s.field(like)
+
+
+def test_c2_full_memcmp_every_odf():
+    """BASELINE configs[1] in full: 512^3, device hash init, 100 iterations, every ODF of
+    the bench sweep (R9 block shapes) plus 64^3 and 32^3 blocks (C5's block shape) --
+    the whole padded array equals the OpenMP oracle's bit for bit."""
+    dims = (512, 512, 512)
+    u0 = JI.hash_field(*dims, seed=1)
+    want, _ = oracle.jacobi3d_omp(u0, N_IT)
+    wv = want.view(np.uint64)
+    for odf, blocks in C2_ODF_BLOCKS.items():
+        got = _full_run(dims, blocks, N_IT, u0)
+        nbad = int(np.count_nonzero(got.view(np.uint64) != wv))
+        assert nbad == 0, f"ODF {odf} blocks {blocks}: {nbad} mismatches"
+        del got
+
+
+def test_c3x1_full_memcmp():
+    """BASELINE configs[2] at one GPU in full: 768^3, ODF 8 (384^3 blocks), 100 iterations."""
+    dims = (768, 768, 768)
+    u0 = JI.hash_field(*dims, seed=1)
+    want, _ = oracle.jacobi3d_omp(u0, N_IT)
+    got = _full_run(dims, (2, 2, 2), N_IT, u0)
+    assert np.array_equal(got.view(np.uint64), want.view(np.uint64))

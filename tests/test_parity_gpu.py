@@ -244,3 +244,33 @@ def test_autotune_picks_a_wide_variant_and_stays_exact():
         s.set_init(u0)
         s.step(6)
         assert_bits(s.field(u0), ref(u0, 6))
+
+
+@pytest.mark.parametrize("dense", [True, False])
+@pytest.mark.parametrize("dims,blocks", [((64, 64, 64), (2, 2, 2)), ((70, 37, 23), (5, 1, 1)),
+                                         ((96, 66, 40), (3, 3, 5)), ((33, 5, 9), (1, 1, 3))])
+def test_get_block_every_block(monkeypatch, dense, dims, blocks):
+    """jac_get_block (north-star call 4): every block's interior equals the oracle's
+    slice [iz*ez:(iz+1)*ez, iy*ey:.., ix*ex:..] -- C1 and ragged decompositions, dense
+    rows (ex % 8 == 0) and the padded layout."""
+    if not dense:
+        monkeypatch.setenv("JAC_EXPERIMENT", "1")
+        monkeypatch.setenv("JAC_NO_DENSE", "1")
+    u0 = JI.hash_field(*dims, seed=3)
+    n = 6
+    want = ref(u0, n)
+    with jb.Jacobi3D(dims, blocks) as s:
+        s.set_init(u0)
+        s.step(n)
+        ex, ey, ez = s.block_extent
+        for iz in range(blocks[2]):
+            for iy in range(blocks[1]):
+                for ix in range(blocks[0]):
+                    b = s.block(ix, iy, iz)
+                    assert b.shape == (ez, ey, ex)
+                    assert_bits(b, want[1 + iz * ez:1 + (iz + 1) * ez, 1 + iy * ey:1 + (iy + 1) * ey,
+                                         1 + ix * ex:1 + (ix + 1) * ex])
+        with pytest.raises(ValueError):  # the binding refuses a wrong-shaped buffer
+            J.jac_get_block(s.ctx, 0, 0, 0, np.empty((ez, ey, ex + 1)))
+        with pytest.raises(ValueError):
+            J.jac_get_block(s.ctx, 0, 0, 0, np.empty((ez, ey, ex), dtype=np.float32))
