@@ -42,16 +42,23 @@ int jac_mb_launch_rate(int32_t device, int32_t chares, int32_t threads, double s
  * moved from device `src` to device `dst` over NVLink split into `odf` sender /
  * receiver pairs (one stream pair and one cudaMemcpyPeerAsync each); with
  * `with_compute` != 0 every receive is followed by an O(n) kernel on the received
- * message on the destination.  *us = time until the last transfer (and kernel) done. */
+ * message on the destination.  *us = time until the last transfer (and kernel) done.
+ * The source holds a counter-based byte pattern; after timing, one more transfer
+ * (without the consumer kernel) lands in a zeroed destination and every delivered
+ * byte is compared with the source on the destination device (byte conservation,
+ * SPEC.md:398): any difference returns JAC_ECUDA naming the count. */
 int jac_mb_pipeline(int32_t src, int32_t dst, int64_t total_bytes, int32_t odf, int32_t with_compute, double *us);
 
 /* E4/E5 with the design's transport: the same `odf` messages (separate buffers,
  * 4 KiB apart) moved by ONE kernel on `src` that stores them into `dst`'s memory over
  * NVLink (message table on the device, as the sweep's face table); with
  * `with_compute` one batched O(n) kernel on `dst` consumes all messages.  Host wall
- * time from launch until both devices are done, best of 5. */
+ * time from launch until both devices are done, best of 5.  Delivery verified as for
+ * jac_mb_pipeline. */
 int jac_mb_pipeline_batched(int32_t src, int32_t dst, int64_t total_bytes, int32_t odf, int32_t with_compute,
                             double *us);
+/* Bytes the calling thread's last jac_mb_pipeline[_batched] call verified (0 before). */
+int64_t jac_mb_last_verified_bytes(void);
 
 #if defined(__GNUC__)
 #pragma GCC visibility pop

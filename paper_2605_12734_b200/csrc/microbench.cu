@@ -74,6 +74,61 @@ __global__ void consume_kernel(double *p, int64_t n)
         p[i] = p[i] * 1.0000001 + 1e-12;
 }
 
+// Byte conservation of the pipelined transfers ("destination buffer region
+// equals source region contents"): the source holds a counter-based pattern, every
+// delivered 8-byte word is compared with it on the destination device.
+__device__ __forceinline__ uint64_t pattern_word(uint64_t i)
+{
+    uint64_t z = i + 0x5EEDF00DCAFEull;
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+__global__ void fill_pattern_kernel(uint64_t *p, int64_t n)
+{
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        p[i] = pattern_word((uint64_t)i);
+}
+
+// words [base, base + n) of the source pattern, delivered at p
+__global__ void verify_pattern_kernel(const uint64_t *p, int64_t n, int64_t base, unsigned long long *bad)
+{
+    unsigned long long mine = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        mine += p[i] != pattern_word((uint64_t)(base + i)) ? 8 : 0;
+    if (mine) atomicAdd(bad, mine);
+}
+
+// Zeroes the destination words [dst_off, dst_off + n) per message, runs `copy_once`
+// (one untimed transfer without the consumer kernel), verifies every delivered word.
+template <class F>
+int verify_delivery(int dst, char *b, const std::vector<std::pair<int64_t, int64_t>> &msgs, F copy_once,
+                    int64_t *bad_bytes)
+{
+    MCK(cudaSetDevice(dst));
+    for (const auto &m : msgs) MCK(cudaMemset(b + m.first, 0, m.second));
+    MCK(cudaDeviceSynchronize());
+    int rc = copy_once();
+    if (rc) return rc;
+    MCK(cudaSetDevice(dst));
+    unsigned long long *bad = nullptr;
+    MCK(cudaMalloc(&bad, sizeof *bad));
+    MCK(cudaMemset(bad, 0, sizeof *bad));
+    for (const auto &m : msgs) {
+        const int64_t n = m.second / 8;
+        verify_pattern_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(1184, (n + 255) / 256)), 256>>>(
+            reinterpret_cast<const uint64_t *>(b + m.first), n, m.first / 8, bad);
+        MCK(cudaGetLastError());
+    }
+    unsigned long long h = 0;
+    MCK(cudaMemcpy(&h, bad, sizeof h, cudaMemcpyDeviceToHost));
+    cudaFree(bad);
+    *bad_bytes = (int64_t)h;
+    return JAC_OK;
+}
+
 typedef CUresult (*PFN_waitValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
 
 struct Msg {
@@ -106,7 +161,11 @@ __global__ void batched_consume_kernel(const Msg *msgs, int nmsg)
 
 }  // namespace
 
+thread_local int64_t g_mb_verified = 0;  // bytes the last pipeline call checked
+
 extern "C" {
+
+int64_t jac_mb_last_verified_bytes(void) { return g_mb_verified; }
 
 int jac_mb_launch_latency(int32_t device, int32_t iters, double *us)
 {
@@ -238,7 +297,9 @@ int jac_mb_pipeline(int32_t src, int32_t dst, int64_t total_bytes, int32_t odf, 
     double *a = nullptr, *b = nullptr;
     MCK(cudaSetDevice(src));
     MCK(cudaMalloc(&a, total_bytes));
-    MCK(cudaMemset(a, 0, total_bytes));
+    fill_pattern_kernel<<<1184, 256>>>(reinterpret_cast<uint64_t *>(a), total_bytes / 8);
+    MCK(cudaGetLastError());
+    MCK(cudaDeviceSynchronize());
     MCK(cudaSetDevice(dst));
     MCK(cudaMalloc(&b, total_bytes));
     if (src != dst) {
@@ -293,6 +354,18 @@ int jac_mb_pipeline(int32_t src, int32_t dst, int64_t total_bytes, int32_t odf, 
         best = std::min(best, (double)mx * 1e3);
     }
     *us = best;
+    {  // every delivered byte of one more (untimed, consumer-free) transfer
+        std::vector<std::pair<int64_t, int64_t>> msgs;
+        for (int k = 0; k < odf; ++k) msgs.push_back({k * chunk, chunk});
+        const int wc = with_compute;
+        with_compute = 0;
+        int64_t bad = 0;
+        if ((rc = verify_delivery(dst, reinterpret_cast<char *>(b), msgs, run, &bad))) return rc;
+        with_compute = wc;
+        if (bad) return mb_fail(JAC_ECUDA, "pipeline: %lld of %lld delivered bytes differ from the source",
+                                (long long)bad, (long long)(chunk * odf));
+        g_mb_verified = chunk * odf;
+    }
     for (int k = 0; k < odf; ++k) {
         cudaStreamDestroy(st[k]);
         cudaEventDestroy(ev[k]);
@@ -320,7 +393,9 @@ int jac_mb_pipeline_batched(int32_t src, int32_t dst, int64_t total_bytes, int32
     MCK(cudaMalloc(&b, pitch * odf));
     MCK(cudaSetDevice(src));
     MCK(cudaMalloc(&a, pitch * odf));
-    MCK(cudaMemset(a, 0, pitch * odf));
+    fill_pattern_kernel<<<1184, 256>>>(reinterpret_cast<uint64_t *>(a), pitch * odf / 8);
+    MCK(cudaGetLastError());
+    MCK(cudaDeviceSynchronize());
     if (src != dst) {
         int can = 0;
         MCK(cudaDeviceCanAccessPeer(&can, src, dst));
@@ -372,6 +447,18 @@ int jac_mb_pipeline_batched(int32_t src, int32_t dst, int64_t total_bytes, int32
         best = std::min(best, now_us() - t0);
     }
     *us = best;
+    {  // every delivered byte of one more (untimed, consumer-free) transfer
+        std::vector<std::pair<int64_t, int64_t>> msgs;
+        for (int k = 0; k < odf; ++k) msgs.push_back({k * pitch, chunk});
+        const int wc = with_compute;
+        with_compute = 0;
+        int64_t bad = 0;
+        if ((rc = verify_delivery(dst, b, msgs, run, &bad))) return rc;
+        with_compute = wc;
+        if (bad) return mb_fail(JAC_ECUDA, "pipeline_batched: %lld of %lld delivered bytes differ from the source",
+                                (long long)bad, (long long)(chunk * odf));
+        g_mb_verified = chunk * odf;
+    }
     cudaEventDestroy(done);
     cudaStreamDestroy(ss);
     cudaFree(dmsg_src);

@@ -43,7 +43,7 @@ EXPORTED = ["jac_plan", "jac_plan_face", "jac_create", "jac_create_rank", "jac_i
             "jac_destroy", "jac_last_error", "jac_version", "jac_set_option", "jac_nccl_id_bytes",
             "jac_nccl_get_unique_id", "jac_nccl_init", "jac_get_region", "jac_get_grid"]
 MICROBENCH_EXPORTED = ["jac_mb_launch_latency", "jac_mb_overlap", "jac_mb_launch_rate", "jac_mb_pipeline",
-                       "jac_mb_pipeline_batched"]
+                       "jac_mb_pipeline_batched", "jac_mb_last_verified_bytes"]
 
 _ERRNAMES = {-1: "JAC_EINVAL", -2: "JAC_EDECOMP", -3: "JAC_EDEVICE", -4: "JAC_ENOMEM",
              -5: "JAC_ECUDA", -6: "JAC_ENCCL", -7: "JAC_ESTATE"}
@@ -121,6 +121,8 @@ def load() -> ctypes.CDLL:
     L.jac_last_error.restype = ctypes.c_char_p
     L.jac_version.argtypes = []
     L.jac_version.restype = ctypes.c_int
+    L.jac_mb_last_verified_bytes.argtypes = []
+    L.jac_mb_last_verified_bytes.restype = ctypes.c_int64
     _lib = L
     return L
 
@@ -374,6 +376,10 @@ def jac_mb_pipeline_batched(src, dst, total_bytes, odf, with_compute=False) -> f
     _check(load().jac_mb_pipeline_batched(src, dst, total_bytes, odf, int(bool(with_compute)), ctypes.byref(v)),
            "jac_mb_pipeline_batched")
     return v.value
+
+
+def jac_mb_last_verified_bytes() -> int:
+    return int(load().jac_mb_last_verified_bytes())
 
 
 def jac_destroy(ctx) -> None:
