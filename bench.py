@@ -89,6 +89,35 @@ def blocks_for_odf(box, odf):
     return tuple(b)
 
 
+def blocks_for_odf_2d(box, odf):
+    """Reading R9 in 2-D: halve the largest block extent, ties go to y."""
+    b = [1, 1]
+    e = list(box)
+    left = odf
+    while left > 1:
+        if left % 2:
+            raise ValueError(f"ODF {odf} is not a power of two")
+        k = 1 if e[1] >= e[0] else 0
+        e[k] //= 2
+        b[k] *= 2
+        left //= 2
+    return tuple(b)
+
+
+def gpu_grid_2d_r10(n, nx, ny):
+    """Reading R10 in 2-D: the GPU grid (gx, gy) with the least inter-GPU face length,
+    ties prefer splitting y."""
+    best = None
+    for gx in range(1, n + 1):
+        if n % gx:
+            continue
+        gy = n // gx
+        cut = (gx - 1) * ny + (gy - 1) * nx
+        if best is None or cut < best[0] or (cut == best[0] and gy > best[2]):
+            best = (cut, gx, gy)
+    return (best[1], best[2])
+
+
 def weak_gpu_grid(n):
     """Weak scaling: the global grid doubles z, then y, then x (PAPER.md:285
     'grid dimensions are alternately increased'; matches reading R10)."""
@@ -121,16 +150,15 @@ def workload(cfg, n, odf):
             g2[d] *= 2
             d ^= 1
             m //= 2
-        b = [1, 1]
-        e = list(box)
-        left = odf
-        while left > 1:
-            k = 1 if e[1] >= e[0] else 0
-            e[k] //= 2
-            b[k] *= 2
-            left //= 2
+        b = blocks_for_odf_2d(box, odf)
         dims = (box[0] * g2[0], box[1] * g2[1], 1)
         return dims, (b[0] * g2[0], b[1] * g2[1], 1), (g2[0], g2[1], 1), f"jacobi2d_32768^2_per_gpu_odf{odf}", "weak"
+    if cfg == "j2d_strong":  # NEXT-1 strong scaling: the paper's fixed 131072 x 98304 grid
+        nx, ny = 131072, 98304
+        g2 = gpu_grid_2d_r10(n, nx, ny)
+        b = blocks_for_odf_2d((nx // g2[0], ny // g2[1]), odf)
+        return ((nx, ny, 1), (b[0] * g2[0], b[1] * g2[1], 1), (g2[0], g2[1], 1),
+                f"jacobi2d_131072x98304_global_odf{odf}", "strong")
     if cfg == "c4":
         dims = (1536, 1536, 1536)
         g = weak_gpu_grid(n)
@@ -372,14 +400,16 @@ def run_reference(args, D):
         return
     dims, blocks, g, label, scaling = workload(args.config, args.gpus, args.odf)
     box = tuple(dims[d] // g[d] for d in range(3))
-    if args.config in ("c4", "c5", "j2d"):
-        box = (512, 512, 512)  # bounded sample (j2d: the 3-D oracle's box)
-    if args.config == "j2d":
-        box = (8192, 8192)
+    if args.config in ("c4", "c5"):
+        box = (512, 512, 512)  # bounded sample of the strong-scaling grids
+    two_d = args.config in ("j2d", "j2d_strong")
+    if two_d:
+        box = (8192, 8192)  # bounded 2-D sample
         cb = cpu_oracle_2d(box=box, steps=args.steps, warmup=args.warmup)
     else:
-        cb = cpu_oracle(box=box, steps=args.steps, warmup=args.warmup)
-    line = {"impl": "reference", "metric": "Jacobi3D GLUP/s (whole job)", "value": cb["value"],
+        cb = cpu_oracle(box=box, steps=args.steps, warmup=args.warmup, serial=False)
+    line = {"impl": "reference", "metric": ("Jacobi2D" if two_d else "Jacobi3D") + " GLUP/s (whole job)",
+            "value": cb["value"],
             "unit": "GLUP/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": cb["ms_per_iter"], "higher_is_better": True, "scaling": scaling,
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (R11 splitmix64 hash, seed 1)",
@@ -454,7 +484,11 @@ def run_ours(args, D):
     from paper_2605_12734_b200 import jacobi3d as JB
 
     K, W = args.steps, max(3, args.warmup)
-    MODE_2D[0] = args.config == "j2d"
+    MODE_2D[0] = args.config in ("j2d", "j2d_strong")
+    if args.config == "j2d_strong":
+        if args.gpus < 2:
+            raise SystemExit("bench.py: j2d_strong (131072 x 98304, two 103 GB fp64 arrays) needs >= 2 B200")
+        args.no_e2e = True  # a 206 GB host copy of the grid is not a sensible e2e job
     dims, blocks, g, label, scaling = workload(args.config, args.gpus, args.odf)
     pts = dims[0] * dims[1] * dims[2]
     pts_gpu = pts // args.gpus
@@ -683,7 +717,7 @@ def main():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=["c2", "c3", "c4", "c5", "j2d"])
+    ap.add_argument("--config", default="c2", choices=["c2", "c3", "c4", "c5", "j2d", "j2d_strong"])
     ap.add_argument("--odf", type=int, default=8)
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")

@@ -123,3 +123,27 @@ def test_c3x1_full_memcmp():
     want, _ = oracle.jacobi3d_omp(u0, N_IT)
     got = _full_run(dims, (2, 2, 2), N_IT, u0)
     assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
+
+
+def test_j2d_strong_paper_grid_multi_gpu():
+    """NEXT-1 strong scaling at the paper's fixed grid, 131072 x 98304:
+    two 103 GB fp64 arrays, so >= 2 B200 through jac_create(n_gpus=2) (one process);
+    light-cone probes at the GPU seam, block seams and the corners after 100 iterations."""
+    import torch
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs (206 GB of state)")
+    nx, ny = 131072, 98304
+    n, s = N_IT, 16
+    with jb.Jacobi2D((nx, ny), (4, 4), n_gpus=2) as J2:
+        assert J2.gpu_grid[:2] == (2, 1)
+        J2.set_init_hash(1)
+        J2.step(n)
+        for (x0, y0) in [(0, 0), (65528, 49144), (65536, 0), (32760, 24568), (131056, 98288), (98300, 73720)]:
+            got = J2.region((x0, y0, 0), (s, s, 1))[0]
+            a = [max(0, x0 - n), max(0, y0 - n)]
+            b = [min(nx, x0 + s + n), min(ny, y0 + s + n)]
+            ys = np.arange(a[1], b[1] + 2, dtype=np.uint64)[:, None]
+            xs = np.arange(a[0], b[0] + 2, dtype=np.uint64)[None, :]
+            sub = JI.hash_values(1, ys * np.uint64(nx + 2) + xs)
+            res, _ = oracle.jacobi2d_omp(np.ascontiguousarray(sub), n)
+            bits(got, res[y0 - a[1] + 1:y0 - a[1] + 1 + s, x0 - a[0] + 1:x0 - a[0] + 1 + s])

@@ -46,20 +46,23 @@ def test_multi_process_parity(case):
     if _ngpu() < n:
         pytest.skip(f"needs {n} GPUs")
     import socket
-    with socket.socket() as sk:
-        sk.bind(("127.0.0.1", 0))
-        port = sk.getsockname()[1]
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--master-addr", "127.0.0.1",
-           "--master-port", str(port), "--nproc-per-node", str(n),
-           os.path.join(ROOT, "tools", "mp_parity.py"), "--dims", *map(str, dims), "--blocks", *map(str, blocks),
-           "--iters", str(iters), "--flags", str(flags)]
-    if grid:
-        cmd += ["--grid", *map(str, grid)]
-    if hashed:
-        cmd += ["--hash-init"]
-    if flags & (1 << 9):
-        cmd += ["--two-d"]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT)
+    for attempt in range(4):  # a probed-free port can be taken before torchrun binds it
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--master-addr", "127.0.0.1",
+               "--master-port", str(port), "--nproc-per-node", str(n),
+               os.path.join(ROOT, "tools", "mp_parity.py"), "--dims", *map(str, dims), "--blocks", *map(str, blocks),
+               "--iters", str(iters), "--flags", str(flags)]
+        if grid:
+            cmd += ["--grid", *map(str, grid)]
+        if hashed:
+            cmd += ["--hash-init"]
+        if flags & (1 << 9):
+            cmd += ["--two-d"]
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT)
+        if r.returncode == 0 or "EADDRINUSE" not in r.stderr:
+            break
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "OK" in r.stdout
 
