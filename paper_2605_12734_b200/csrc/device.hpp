@@ -122,6 +122,9 @@ struct SweepArgs {
     int32_t fused_sync;
     int32_t nremote;         // remote-touching items of all hosted partitions (the first
                              // nremote entries of item_map)
+    int32_t slot_base;       // slot of blocks[0] (JAC_F_PER_BLOCK launches one block's table
+                             // entry; 0 otherwise: the work list enumerates slots in order)
+    int32_t pad3_;
     // jac_profile_sweep: when set, every CTA atomicMin's %globaltimer into span[0] after
     // the dependency wait and atomicMax's it into span[1] when done (ns)
     unsigned long long *span;

@@ -907,6 +907,7 @@ int enqueue_per_block(jac_ctx *c, int64_t t, int first, int stride)
         }
         jac::SweepArgs a = base;  // the stencil of this block alone
         a.blocks = c->dblocks + b;
+        a.slot_base = b;
         a.ncols = c->ntx * c->nty;
         a.nitems = a.ncols * c->nzc;
         a.gcols = a.ncols;

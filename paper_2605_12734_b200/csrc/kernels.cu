@@ -345,6 +345,16 @@ __device__ __forceinline__ void signal_done(const PartSync &ps)
     }
 }
 
+// Copies a block descriptor into shared memory, 16 bytes per thread (threads 0..10).
+// The caller's first __syncthreads publishes it.
+static_assert(sizeof(DevBlock) % 16 == 0, "DevBlock is copied in 16-byte pieces");
+__device__ __forceinline__ void load_descriptor(DevBlock *dst, const DevBlock *src)
+{
+    constexpr int kPieces = (int)(sizeof(DevBlock) / 16);
+    if ((int)threadIdx.x < kPieces)
+        reinterpret_cast<int4 *>(dst)[threadIdx.x] = __ldg(reinterpret_cast<const int4 *>(src) + threadIdx.x);
+}
+
 // Staged column of the tile's first point i = x0.  Interior tiles stage x0-2 ..
 // x0+BX+1 (soff = 2).  The box never reads the inline x-ghost sectors (x ghosts come
 // from the x-ghost arrays): the first tile starts at the interior (soff = 0) and the
@@ -384,8 +394,14 @@ __global__ void __launch_bounds__(NT, min_ctas_per_sm(NT, NS))
     const Geom &g = a.g;
     const TileItem t = decode_item<BX, BY>(a, a.item_map ? a.item_map[blockIdx.x] : (int)blockIdx.x);
     const bool remote = a.fused_sync && (int)blockIdx.x < a.nremote;  // item_map puts them first
-    __shared__ DevBlock blk;  // this item's descriptor, read once from the table
-    if (threadIdx.x == 0) blk = a.blocks[t.b];
+    // The work list enumerates the table's slots in order, so the staging copies need
+    // no descriptor: thread 0 issues them without waiting for the table read.  The
+    // descriptor (store targets, for the epilogue) is copied to shared memory 16 bytes
+    // per thread in parallel (a measured 12% of the small-block sweep's stall samples
+    // sat at the prologue barrier while thread 0 serially read it first).
+    const int slot = a.slot_base + t.b;
+    __shared__ __align__(16) DevBlock blk;
+    load_descriptor(&blk, a.blocks + t.b);
     pdl_launch_dependents_then_wait();
     span_begin(a.span);
     const int soff = tile_soff<BX, W>(g, t.x0);  // staged column of point i = x0 (0, 2 or 4)
@@ -413,9 +429,7 @@ __global__ void __launch_bounds__(NT, min_ctas_per_sm(NT, NS))
     };
 
     if (threadIdx.x == 0) {
-        const DevBlock &gb = a.blocks[t.b];
-        const int slot = gb.slot;
-        if (remote) wait_peers(a, a.sync[gb.part]);
+        if (remote) wait_peers(a, a.sync[a.blocks[t.b].part]);
         c3 = a.src * g.nslots + slot;
         xg0 = xg_array(a.xg, g, a.src, slot, 0) + t.y0;
         xg1 = xg_array(a.xg, g, a.src, slot, 1) + t.y0;
@@ -436,7 +450,7 @@ __global__ void __launch_bounds__(NT, min_ctas_per_sm(NT, NS))
     const int jl0 = rg * RY;                       // tile row of this thread's row 0
     const int sb = (jl0 + 1) * W + col;            // stage index of (row 0, element 0)
     const int xg = L::XG_OFF + jl0;                // stage index of row 0's x- ghost (+BY: x+)
-    double *const own = a.arena + (int64_t)(dst * g.nslots + blk.slot) * g.bstride;
+    double *const own = a.arena + (int64_t)(dst * g.nslots + slot) * g.bstride;
     auto plane = [&](int q) { return stage + (q % NS) * L::STRIDE; };
     auto wait = [&](int q) { mbar_wait(&bars[q % NS], (q / NS) & 1); };
     // every thread is done with plane q -> the producer refills its stage with q + NS.
@@ -523,7 +537,7 @@ __global__ void __launch_bounds__(NT, min_ctas_per_sm(NT, NS))
                 xf = blk.nb[f][dst];
                 xs = g.eyp;
             } else if (blk.nb[f][0]) {
-                xf = a.outbox + (int64_t)blk.slot * g.ostride + g.ooff[f];
+                xf = a.outbox + (int64_t)slot * g.ostride + g.ooff[f];
                 xs = g.ey;
             }
             if (xf) xf += t.y0 + jl0 + (int64_t)(t.zs - 1 + q) * xs;
@@ -548,7 +562,7 @@ __global__ void __launch_bounds__(NT, min_ctas_per_sm(NT, NS))
                         }
                     }
                 } else if (blk.nb[f][0]) {
-                    yf = a.outbox + (int64_t)blk.slot * g.ostride + g.ooff[f] + i;
+                    yf = a.outbox + (int64_t)slot * g.ostride + g.ooff[f] + i;
                     ys = g.ex;
                 }
                 if (yf) yf += (int64_t)(t.zs - 1 + q) * ys;
@@ -651,11 +665,12 @@ __global__ void __launch_bounds__(NT, 4) sweep2d_tma_kernel(const __grid_constan
     const TileItem t = decode_item2d(a, a.item_map ? a.item_map[blockIdx.x] : (int)blockIdx.x, BX, BY);
     const bool remote = a.fused_sync && (int)blockIdx.x < a.nremote;
     const int b = t.b;
+    const int slot = a.slot_base + b;  // see the 3-D sweep
     const int ty0 = t.zs;
     const int nq = max(0, t.ze - t.zs);
     const int x0 = t.x0;
-    __shared__ DevBlock blk;
-    if (threadIdx.x == 0) blk = a.blocks[b];
+    __shared__ __align__(16) DevBlock blk;
+    load_descriptor(&blk, a.blocks + b);
     pdl_launch_dependents_then_wait();
     span_begin(a.span);
     const int soff = tile_soff<BX, W>(g, x0);
@@ -673,9 +688,7 @@ __global__ void __launch_bounds__(NT, 4) sweep2d_tma_kernel(const __grid_constan
         if (xhi) bulk_copy(st + L::XG_OFF + BY, xg1 + y0, L::XG_BYTES, bar);
     };
     if (threadIdx.x == 0) {
-        const DevBlock &gb = a.blocks[b];
-        const int slot = gb.slot;
-        if (remote) wait_peers(a, a.sync[gb.part]);
+        if (remote) wait_peers(a, a.sync[a.blocks[b].part]);
         c3 = a.src * g.nslots + slot;
         xg0 = xg_array(a.xg, g, a.src, slot, 0);
         xg1 = xg_array(a.xg, g, a.src, slot, 1);
@@ -691,7 +704,7 @@ __global__ void __launch_bounds__(NT, 4) sweep2d_tma_kernel(const __grid_constan
     const int i = x0 + 2 * lane;
     const int dst = 1 - a.src;
     const bool ilo = (i == 0), ihi0 = (i == g.ex - 1), ihi1 = (i + 1 == g.ex - 1);
-    double *own = a.arena + (int64_t)(dst * g.nslots + blk.slot) * g.bstride;  // plane k = 0 (zg = 0)
+    double *own = a.arena + (int64_t)(dst * g.nslots + slot) * g.bstride;  // plane k = 0 (zg = 0)
     // Lean y tiles (as in the 3-D sweep): full in x and y, no y-face row -> one 16-byte
     // store per pair (+ the x-face value on x-edge lanes), rows shared between a
     // thread's RY rows instead of reloaded.  Other tiles take emit_pair.
@@ -707,7 +720,7 @@ __global__ void __launch_bounds__(NT, 4) sweep2d_tma_kernel(const __grid_constan
     if (xfull && exch && (ilo || ihi1)) {
         const int f = ilo ? XM : XP;
         if (a.mode == MODE_FUSED) xf = blk.nb[f][dst];
-        else if (blk.nb[f][0]) xf = a.outbox + (int64_t)blk.slot * g.ostride + g.ooff[f];
+        else if (blk.nb[f][0]) xf = a.outbox + (int64_t)slot * g.ostride + g.ooff[f];
     }
     // general y tile: every store through emit_pair
     auto tile_general = [&](int q) {
