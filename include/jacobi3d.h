@@ -273,7 +273,10 @@ enum jac_stat {
     JAC_STAT_EPOCH_MAX = 13,      /* synchronised phases (sweeps + barriers) completed */
     JAC_STAT_EXPERIMENT = 14,     /* bit mask of active experiment knobs (JAC_EXPERIMENT=1);
                                      0 in production: no environment variable changes the library */
-    JAC_STAT_N = 15
+    JAC_STAT_PEER_WAIT_NS = 15,   /* last jac_profile_sweep: median over its sweeps of the time the
+                                     remote CTAs spent waiting for neighbour signals, summed (ns) */
+    JAC_STAT_PEER_WAIT_MAX_NS = 16, /* ... and the longest single wait (ns); group: max over devices */
+    JAC_STAT_N = 17
 };
 int jac_get_stats(const jac_ctx *c, int64_t *stats /* [JAC_STAT_N] */);
 

@@ -116,7 +116,7 @@ struct SweepArgs {
     // launch first (item_map), wait for the neighbours' signal of the previous sweep,
     // and the last of them per partition (PartSync::nremote) signals this sweep's.
     // Other items never wait.
-    const int32_t *item_map; // launch order -> item, or nullptr
+    const int32_t *item_map; // launch order -> item (~item for a remote-touching item), or nullptr
     const PartSync *sync;    // [partitions hosted], indexed by DevBlock::part
     Watchdog wd;
     int32_t fused_sync;
@@ -126,7 +126,8 @@ struct SweepArgs {
                              // entry; 0 otherwise: the work list enumerates slots in order)
     int32_t pad3_;
     // jac_profile_sweep: when set, every CTA atomicMin's %globaltimer into span[0] after
-    // the dependency wait and atomicMax's it into span[1] when done (ns)
+    // the dependency wait and atomicMax's it into span[1] when done (ns); remote CTAs add
+    // their peer-wait time to span[2] and max it into span[3]
     unsigned long long *span;
 };
 

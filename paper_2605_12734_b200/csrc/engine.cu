@@ -160,6 +160,7 @@ struct jac_ctx {
     int nzc = 1, ncols = 1, nitems = 1, gcols = 1;
     float tuned_ms[2] = {0.f, 0.f};  // autotune: sweep ms for the 6- and 4-stage wide tiles
     double last_gap_ms = -1.0;       // jac_profile_sweep: median gap between consecutive sweeps
+    int64_t last_wait_sum_ns = 0, last_wait_max_ns = 0;  // jac_profile_sweep: remote CTAs' peer waits
     unsigned long long *prof_span = nullptr;  // jac_profile_sweep capture: per-iteration [start, end]
     int prof_it = 0;
     bool pdl = true;                 // sweeps use programmatic dependent launch (JAC_PDL=0: off)
@@ -242,7 +243,7 @@ uint64_t fingerprint(const jac_ctx *c)
 const char *const kKnobs[] = {"JAC_L2PROMO", "JAC_ZC",     "JAC_ZCHUNK", "JAC_GCOLS",   "JAC_VARIANT",
                               "JAC_AUTOTUNE", "JAC_A",      "JAC_PALIGN", "JAC_NO_DENSE", "JAC_UNROLL",
                               "JAC_PDL",     "JAC_NO_FUSED_SYNC", "JAC_ORDER_EXP", "JAC_DROP_REMOTE",
-                              "JAC_HOLD_SIGNAL"};
+                              "JAC_HOLD_SIGNAL", "JAC_REMOTE_SPREAD"};
 
 const char *knob(jac_ctx *c, const char *name)
 {
@@ -270,7 +271,7 @@ jac::SweepArgs sweep_args(const jac_ctx *c, int src, int mode)
     a.ntx = c->ntx; a.nty = c->nty; a.ntz = c->ntz; a.zc = c->zc;
     a.nzc = c->nzc; a.ncols = c->ncols; a.nitems = c->nitems; a.gcols = c->gcols;
     if (c->ditem_map && !c->fused) a.item_map = c->ditem_map;  // JAC_ORDER_EXP
-    if (c->prof_span) a.span = c->prof_span + 2 * (int64_t)c->prof_it;
+    if (c->prof_span) a.span = c->prof_span + 4 * (int64_t)c->prof_it;
     a.wd = c->wd();
     if (c->fused && mode == jac::MODE_FUSED) {
         a.fused_sync = 1;
@@ -837,9 +838,28 @@ int create_common(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, in
         // remote-touching items first: their signal leaves early in the sweep, so the
         // next sweep's remote items (which wait for it) find it already set
         int32_t nfirst = 0;
-        const std::vector<int32_t> order =
-            remote_first_order(c, mask, order_exp == 2, &nfirst, &nremote_part);
-        if (c->fused) c->nremote = nfirst;
+        std::vector<int32_t> order = remote_first_order(c, mask, order_exp == 2, &nfirst, &nremote_part);
+        if (c->fused) {
+            c->nremote = nfirst;
+            // remote-touching items are marked in the map (~item): they wait before their
+            // first staging copy and signal after their last store
+            for (int32_t i = 0; i < nfirst; ++i) order[i] = ~order[i];
+            // experiment: spread the remote items evenly over the first fraction f of the
+            // launch order instead of putting them first (f = JAC_REMOTE_SPREAD / 100)
+            if (const char *sp = knob(c, "JAC_REMOTE_SPREAD"); sp && nfirst > 0 && nfirst < c->nitems) {
+                const double f = std::min(1.0, std::max(0.0, atof(sp) / 100.0));
+                const int64_t span = std::max<int64_t>(nfirst, (int64_t)(f * c->nitems));
+                std::vector<int32_t> spread;
+                spread.reserve(order.size());
+                int32_t r = 0, o = nfirst;
+                for (int64_t pos = 0; pos < (int64_t)order.size(); ++pos) {
+                    const bool take_remote = r < nfirst && (pos >= span - (nfirst - r) ||
+                                                            pos * nfirst >= (int64_t)r * span);
+                    spread.push_back(take_remote ? order[r++] : order[o++]);
+                }
+                order.swap(spread);
+            }
+        }
         if (cudaMalloc(&c->ditem_map, sizeof(int32_t) * order.size()) != cudaSuccess ||
             cudaMemcpy(c->ditem_map, order.data(), sizeof(int32_t) * order.size(), cudaMemcpyHostToDevice) != cudaSuccess)
             return bail(fail(JAC_ENOMEM, "item map"));
@@ -1584,7 +1604,12 @@ int jac_profile_sweep(jac_ctx *c, int32_t n, double *avg_ms)
         if (rc) return rc;
         *avg_ms = *std::max_element(ms.begin(), ms.end());
         c->last_gap_ms = -1.0;
-        for (const jac_ctx *sc : c->subs) c->last_gap_ms = std::max(c->last_gap_ms, sc->last_gap_ms);
+        c->last_wait_sum_ns = c->last_wait_max_ns = 0;
+        for (const jac_ctx *sc : c->subs) {
+            c->last_gap_ms = std::max(c->last_gap_ms, sc->last_gap_ms);
+            c->last_wait_sum_ns = std::max(c->last_wait_sum_ns, sc->last_wait_sum_ns);
+            c->last_wait_max_ns = std::max(c->last_wait_max_ns, sc->last_wait_max_ns);
+        }
         c->iters = c->subs[0]->iters;
         return JAC_OK;
     }
@@ -1603,8 +1628,8 @@ int jac_profile_sweep(jac_ctx *c, int32_t n, double *avg_ms)
         jac_ctx *c;
         ~Span() { if (d) cudaFree(d); c->prof_span = nullptr; }
     } span{nullptr, c};
-    std::vector<unsigned long long> hspan(2 * (size_t)n);
-    for (int it = 0; it < n; ++it) { hspan[2 * it] = ~0ull; hspan[2 * it + 1] = 0ull; }
+    std::vector<unsigned long long> hspan(4 * (size_t)n, 0ull);  // [start, end, wait sum, wait max]
+    for (int it = 0; it < n; ++it) hspan[4 * it] = ~0ull;
     if (use_span) {
         CK(cudaMalloc(&span.d, sizeof(unsigned long long) * hspan.size()));
         CK(cudaMemcpy(span.d, hspan.data(), sizeof(unsigned long long) * hspan.size(), cudaMemcpyHostToDevice));
@@ -1639,9 +1664,18 @@ int jac_profile_sweep(jac_ctx *c, int32_t n, double *avg_ms)
     std::vector<float> dur(n), gap(n > 1 ? n - 1 : 0);
     if (use_span) {
         CK(cudaMemcpy(hspan.data(), span.d, sizeof(unsigned long long) * hspan.size(), cudaMemcpyDeviceToHost));
-        for (int it = 0; it < n; ++it) dur[it] = (float)((double)(hspan[2 * it + 1] - hspan[2 * it]) * 1e-6);
+        for (int it = 0; it < n; ++it) dur[it] = (float)((double)(hspan[4 * it + 1] - hspan[4 * it]) * 1e-6);
         for (int it = 0; it + 1 < n; ++it)
-            gap[it] = (float)(((double)hspan[2 * it + 2] - (double)hspan[2 * it + 1]) * 1e-6);
+            gap[it] = (float)(((double)hspan[4 * it + 4] - (double)hspan[4 * it + 1]) * 1e-6);
+        // peer waits of the remote CTAs: median over sweeps of the summed wait, max of any
+        std::vector<unsigned long long> ws(n);
+        c->last_wait_max_ns = 0;
+        for (int it = 0; it < n; ++it) {
+            ws[it] = hspan[4 * it + 2];
+            c->last_wait_max_ns = std::max<int64_t>(c->last_wait_max_ns, (int64_t)hspan[4 * it + 3]);
+        }
+        std::sort(ws.begin(), ws.end());
+        c->last_wait_sum_ns = (int64_t)ws[n / 2];
     } else {
         for (int it = 0; it < n; ++it) CK(cudaEventElapsedTime(&dur[it], ev[2 * it], ev[2 * it + 1]));
         for (int it = 0; it + 1 < n; ++it) CK(cudaEventElapsedTime(&gap[it], ev[2 * it + 1], ev[2 * it + 2]));
@@ -1859,6 +1893,8 @@ int jac_get_stats(const jac_ctx *c, int64_t *st)
         st[JAC_STAT_KERNELS_PER_ITER] = sub[JAC_STAT_KERNELS_PER_ITER];
         st[JAC_STAT_SWEEP_VARIANT] = sub[JAC_STAT_SWEEP_VARIANT];
         st[JAC_STAT_FUSED_SYNC] = sub[JAC_STAT_FUSED_SYNC];
+        st[JAC_STAT_PEER_WAIT_NS] = c->last_wait_sum_ns;
+        st[JAC_STAT_PEER_WAIT_MAX_NS] = c->last_wait_max_ns;
         return JAC_OK;
     }
     st[JAC_STAT_KERNEL_LAUNCHES] = c->kernel_launches;
@@ -1890,6 +1926,8 @@ int jac_get_stats(const jac_ctx *c, int64_t *st)
         st[JAC_STAT_EPOCH_MAX] = hi;
     }
     st[JAC_STAT_EXPERIMENT] = experiment_mask(c);
+    st[JAC_STAT_PEER_WAIT_NS] = c->last_wait_sum_ns;
+    st[JAC_STAT_PEER_WAIT_MAX_NS] = c->last_wait_max_ns;
     return JAC_OK;
 }
 

@@ -327,6 +327,20 @@ __device__ __forceinline__ void wait_peers(const SweepArgs &a, const PartSync &p
     wait_flags(ps, e, a.wd);
 }
 
+// wait_peers, timed under jac_profile_sweep: span[2] += wait ns, span[3] = max(wait ns)
+__device__ __forceinline__ void timed_wait_peers(const SweepArgs &a, const PartSync &ps)
+{
+    if (!a.span) {
+        wait_peers(a, ps);
+        return;
+    }
+    const uint64_t w0 = globaltimer_ns();
+    wait_peers(a, ps);
+    const unsigned long long w = globaltimer_ns() - w0;
+    atomicAdd(&a.span[2], w);
+    atomicMax(&a.span[3], w);
+}
+
 // All threads of a remote-touching item: after the CTA's last store.  The last such
 // CTA of its partition in this launch bumps the partition's epoch and releases it to
 // every neighbour partition.
@@ -392,8 +406,9 @@ __global__ void __launch_bounds__(NT, min_ctas_per_sm(NT, NS))
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + NS * L::STRIDE * sizeof(double));
 
     const Geom &g = a.g;
-    const TileItem t = decode_item<BX, BY>(a, a.item_map ? a.item_map[blockIdx.x] : (int)blockIdx.x);
-    const bool remote = a.fused_sync && (int)blockIdx.x < a.nremote;  // item_map puts them first
+    const int code = a.item_map ? a.item_map[blockIdx.x] : (int)blockIdx.x;  // ~item: remote-touching
+    const TileItem t = decode_item<BX, BY>(a, code < 0 ? ~code : code);
+    const bool remote = a.fused_sync && code < 0;
     // The work list enumerates the table's slots in order, so the staging copies need
     // no descriptor: thread 0 issues them without waiting for the table read.  The
     // descriptor (store targets, for the epilogue) is copied to shared memory 16 bytes
@@ -429,7 +444,7 @@ __global__ void __launch_bounds__(NT, min_ctas_per_sm(NT, NS))
     };
 
     if (threadIdx.x == 0) {
-        if (remote) wait_peers(a, a.sync[a.blocks[t.b].part]);
+        if (remote) timed_wait_peers(a, a.sync[a.blocks[t.b].part]);
         c3 = a.src * g.nslots + slot;
         xg0 = xg_array(a.xg, g, a.src, slot, 0) + t.y0;
         xg1 = xg_array(a.xg, g, a.src, slot, 1) + t.y0;
@@ -450,7 +465,7 @@ __global__ void __launch_bounds__(NT, min_ctas_per_sm(NT, NS))
     const int jl0 = rg * RY;                       // tile row of this thread's row 0
     const int sb = (jl0 + 1) * W + col;            // stage index of (row 0, element 0)
     const int xg = L::XG_OFF + jl0;                // stage index of row 0's x- ghost (+BY: x+)
-    double *const own = a.arena + (int64_t)(dst * g.nslots + slot) * g.bstride;
+    double *const own = a.arena + (int64_t)(dst * g.nslots + blk.slot) * g.bstride;  // (slot here spills at 64 regs)
     auto plane = [&](int q) { return stage + (q % NS) * L::STRIDE; };
     auto wait = [&](int q) { mbar_wait(&bars[q % NS], (q / NS) & 1); };
     // every thread is done with plane q -> the producer refills its stage with q + NS.
@@ -593,7 +608,7 @@ __global__ void __launch_bounds__(NT, min_ctas_per_sm(NT, NS))
                 v.y = stencil7(B[r].y, B[r].x, xp1, ym.y, yp.y, A[r].y, C[r].y);
                 *reinterpret_cast<double2 *>(op + r * P) = v;
                 if (XE && xf) xf[r] = ilo ? v.x : v.y;
-                if (XE && yf && ((r == 0 && yf_lo) || (r == RY - 1 && !yf_lo))) { yf[0] = v.x; yf[1] = v.y; }
+                if (XE && yf && ((r == 0 && yf_lo) || (r == RY - 1 && !yf_lo))) *reinterpret_cast<double2 *>(yf) = v;  // 16-byte aligned: i even
             }
             op += Qs;
             if (XE && xf) xf += xs;
@@ -662,8 +677,9 @@ __global__ void __launch_bounds__(NT, 4) sweep2d_tma_kernel(const __grid_constan
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + NS * L::STRIDE * sizeof(double));
 
     const Geom &g = a.g;
-    const TileItem t = decode_item2d(a, a.item_map ? a.item_map[blockIdx.x] : (int)blockIdx.x, BX, BY);
-    const bool remote = a.fused_sync && (int)blockIdx.x < a.nremote;
+    const int code = a.item_map ? a.item_map[blockIdx.x] : (int)blockIdx.x;  // ~item: remote-touching
+    const TileItem t = decode_item2d(a, code < 0 ? ~code : code, BX, BY);
+    const bool remote = a.fused_sync && code < 0;
     const int b = t.b;
     const int slot = a.slot_base + b;  // see the 3-D sweep
     const int ty0 = t.zs;
@@ -688,7 +704,7 @@ __global__ void __launch_bounds__(NT, 4) sweep2d_tma_kernel(const __grid_constan
         if (xhi) bulk_copy(st + L::XG_OFF + BY, xg1 + y0, L::XG_BYTES, bar);
     };
     if (threadIdx.x == 0) {
-        if (remote) wait_peers(a, a.sync[a.blocks[b].part]);
+        if (remote) timed_wait_peers(a, a.sync[a.blocks[b].part]);
         c3 = a.src * g.nslots + slot;
         xg0 = xg_array(a.xg, g, a.src, slot, 0);
         xg1 = xg_array(a.xg, g, a.src, slot, 1);

@@ -34,7 +34,8 @@ JAC_OPT_WATCHDOG_MS = 2
 JAC_FACE_BOUNDARY, JAC_FACE_LOCAL, JAC_FACE_REMOTE = 0, 1, 2
 STAT_NAMES = ["kernel_launches", "graph_launches", "kernels_per_iter", "local_blocks",
               "local_faces", "remote_faces", "remote_bytes", "arena_bytes", "sweep_variant",
-              "partitions", "remote_items", "fused_sync", "epoch_min", "epoch_max", "experiment"]
+              "partitions", "remote_items", "fused_sync", "epoch_min", "epoch_max", "experiment",
+              "peer_wait_ns", "peer_wait_max_ns"]
 EXPORTED = ["jac_plan", "jac_plan_face", "jac_create", "jac_create_rank", "jac_ipc_handle_bytes",
             "jac_export_ipc", "jac_import_ipc", "jac_set_init", "jac_set_init_hash", "jac_step",
             "jac_get_block", "jac_get_block_padded", "jac_get_field", "jac_get_layout",
