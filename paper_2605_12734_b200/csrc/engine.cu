@@ -844,10 +844,16 @@ int create_common(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, in
             // remote-touching items are marked in the map (~item): they wait before their
             // first staging copy and signal after their last store
             for (int32_t i = 0; i < nfirst; ++i) order[i] = ~order[i];
-            // experiment: spread the remote items evenly over the first fraction f of the
-            // launch order instead of putting them first (f = JAC_REMOTE_SPREAD / 100)
-            if (const char *sp = knob(c, "JAC_REMOTE_SPREAD"); sp && nfirst > 0 && nfirst < c->nitems) {
-                const double f = std::min(1.0, std::max(0.0, atof(sp) / 100.0));
+            // The remote items are spread evenly over the first quarter of the launch order
+            // rather than all launched first: their signal still leaves early (the next
+            // sweep's waits stay short), but the first waves no longer consist only of
+            // scattered face items that lose their halo partners' L2 reuse and all store
+            // over NVLink at once.  Same-box A/B at N = 4 (profiles/r02_remote_spread.txt):
+            // C2 ODF 8 0.3461 -> 0.3374-0.3382 ms/iter, ODF 64 -2.0%, C3 -1.3%, C4 ODF 16
+            // -0.8%, C5 -0.8%; N = 2 neutral.  JAC_REMOTE_SPREAD=<percent> (0 = all first).
+            double f = 0.25;
+            if (const char *sp = knob(c, "JAC_REMOTE_SPREAD")) f = std::min(1.0, std::max(0.0, atof(sp) / 100.0));
+            if (f > 0 && nfirst > 0 && nfirst < c->nitems) {
                 const int64_t span = std::max<int64_t>(nfirst, (int64_t)(f * c->nitems));
                 std::vector<int32_t> spread;
                 spread.reserve(order.size());
