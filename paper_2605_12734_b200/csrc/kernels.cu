@@ -583,6 +583,7 @@ __global__ void __launch_bounds__(NT, min_ctas_per_sm(NT, NS))
                 if (yf) yf += (int64_t)(t.zs - 1 + q) * ys;
             }
         }
+        const bool yv = (ys & 1) == 0;  // y-face rows 16-byte aligned (ghost rows; packed, even ex)
         double *op = own + (int64_t)(t.zs + q) * g.Q + (int64_t)(t.y0 + jl0 + 1) * g.P + g.A + i;
         const int64_t P = g.P, Qs = g.Q;
         int sn = (q + 1) % NS;               // ring slot of plane q+1
@@ -608,7 +609,12 @@ __global__ void __launch_bounds__(NT, min_ctas_per_sm(NT, NS))
                 v.y = stencil7(B[r].y, B[r].x, xp1, ym.y, yp.y, A[r].y, C[r].y);
                 *reinterpret_cast<double2 *>(op + r * P) = v;
                 if (XE && xf) xf[r] = ilo ? v.x : v.y;
-                if (XE && yf && ((r == 0 && yf_lo) || (r == RY - 1 && !yf_lo))) *reinterpret_cast<double2 *>(yf) = v;  // 16-byte aligned: i even
+                if (XE && yf && ((r == 0 && yf_lo) || (r == RY - 1 && !yf_lo))) {
+                    // one 16-byte store (NVLink sends a half-written 32-byte sector as its own
+                    // transfer); packed rows of odd width ex are only 8-byte aligned
+                    if (yv) *reinterpret_cast<double2 *>(yf) = v;
+                    else { yf[0] = v.x; yf[1] = v.y; }
+                }
             }
             op += Qs;
             if (XE && xf) xf += xs;
