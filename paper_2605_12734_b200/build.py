@@ -3,6 +3,10 @@ travels to the GPU box with the repo snapshot).
 
 Flags: -gencode arch=compute_100a,code=sm_100a, -fmad=false (north star: fixed
 summation order, no contraction), -lineinfo (ncu source page), -O3.
+
+``build(checked=True)`` builds libjacobi3d_checked.so with -DJAC_CHECKED: every kernel
+store range- and alignment-checked, TMA coordinates asserted (device.hpp CheckArgs) --
+the test-only substitute for compute-sanitizer, which is closed on this GPU pool.
 """
 from __future__ import annotations
 
@@ -14,6 +18,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libjacobi3d.so")
+LIB_CHECKED = os.path.join(PKG, "libjacobi3d_checked.so")
 SOURCES = ["engine.cu", "kernels.cu", "microbench.cu", "plan.cpp"]
 HEADERS = ["device.hpp", "kernels.hpp", "plan.hpp"]
 
@@ -33,47 +38,56 @@ def _inputs():
     return files
 
 
-STAMP = LIB + ".stamp"  # sha256 of the inputs + flags the .so was built from
+def _lib(checked: bool) -> str:
+    return LIB_CHECKED if checked else LIB
 
 
-def _digest() -> str:
+def _flags(checked: bool):
+    return NVCC_FLAGS + (["-DJAC_CHECKED"] if checked else [])
+
+
+def _digest(checked: bool = False) -> str:
     import hashlib
-    h = hashlib.sha256(" ".join(NVCC_FLAGS).encode())
+    h = hashlib.sha256(" ".join(_flags(checked)).encode())
     for f in _inputs():
         with open(f, "rb") as fh:
             h.update(os.path.basename(f).encode() + b"\0" + fh.read())
     return h.hexdigest()
 
 
-def needs_build() -> bool:
+def needs_build(checked: bool = False) -> bool:
     """Content-based: a copied tree (new mtimes, e.g. the gpurun snapshot) reuses a
     .so built from the same sources; without a stamp, fall back to mtimes."""
-    if not os.path.exists(LIB):
+    lib = _lib(checked)
+    stamp = lib + ".stamp"  # sha256 of the inputs + flags the .so was built from
+    if not os.path.exists(lib):
         return True
-    if os.path.exists(STAMP):
-        with open(STAMP) as fh:
-            return fh.read().strip() != _digest()
-    t = os.path.getmtime(LIB)
+    if os.path.exists(stamp):
+        with open(stamp) as fh:
+            return fh.read().strip() != _digest(checked)
+    t = os.path.getmtime(lib)
     return any(os.path.getmtime(f) > t for f in _inputs())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
-        return LIB
+def build(force: bool = False, verbose: bool = False, checked: bool = False) -> str:
+    lib = _lib(checked)
+    if not force and not needs_build(checked):
+        return lib
     nvcc = os.environ.get("NVCC", "nvcc")
-    tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [nvcc, *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-o", tmp,
+    tmp = lib + f".tmp{os.getpid()}"
+    cmd = [nvcc, *_flags(checked), "-I", os.path.join(ROOT, "include"), "-o", tmp,
            *[os.path.join(CSRC, s) for s in SOURCES]]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
-    digest = _digest()
+    digest = _digest(checked)
     subprocess.check_call(cmd)
-    os.replace(tmp, LIB)
-    with open(STAMP + f".tmp{os.getpid()}", "w") as fh:
+    os.replace(tmp, lib)
+    stamp = lib + ".stamp"
+    with open(stamp + f".tmp{os.getpid()}", "w") as fh:
         fh.write(digest + "\n")
-    os.replace(STAMP + f".tmp{os.getpid()}", STAMP)
-    return LIB
+    os.replace(stamp + f".tmp{os.getpid()}", stamp)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    print(build(force="--force" in sys.argv, verbose=True, checked="--checked" in sys.argv))

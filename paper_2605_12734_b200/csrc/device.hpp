@@ -77,6 +77,25 @@ enum SweepMode { MODE_FUSED = 0, MODE_PACK = 1, MODE_NOEXCHANGE = 2 };
 // live in the hosting context's ctrl area: [0] = epoch (phases completed here),
 // [1 + q] = the flag word partition q stores its epoch into (st.release.sys, over
 // NVLink for a peer GPU), [1 + n_gpus] = count of this sweep's finished remote CTAs.
+// Checked build (-DJAC_CHECKED, libjacobi3d_checked.so): every global store of the
+// kernels is tested against these ranges (the context's allocation and its peers') and
+// its alignment, every TMA coordinate against the tensor extent; a violation is
+// recorded in the mapped status words and the store is skipped -- the substitute for
+// compute-sanitizer, which is closed on this pool.  Unused in the production build.
+struct MemRange {
+    unsigned long long lo, hi;  // [lo, hi) byte addresses
+};
+constexpr uint32_t kStatusMisaligned = 2u;  // status[0] bits (with kStatusPeerTimeout)
+constexpr uint32_t kStatusOutOfRange = 4u;
+constexpr uint32_t kStatusAssert = 8u;
+struct CheckArgs {
+    const MemRange *ranges;  // device table
+    int32_t nranges;
+    int32_t pad_;
+    uint32_t *status;        // mapped host words: [0] flags, [1] first failing source line,
+                             // [2..3] its address (low, high)
+};
+
 struct PartSync {
     uint64_t *ctrl;
     unsigned long long *count;
@@ -125,6 +144,7 @@ struct SweepArgs {
     int32_t slot_base;       // slot of blocks[0] (JAC_F_PER_BLOCK launches one block's table
                              // entry; 0 otherwise: the work list enumerates slots in order)
     int32_t pad3_;
+    CheckArgs chk;           // checked build only
     // jac_profile_sweep: when set, every CTA atomicMin's %globaltimer into span[0] after
     // the dependency wait and atomicMax's it into span[1] when done (ns); remote CTAs add
     // their peer-wait time to span[2] and max it into span[3]

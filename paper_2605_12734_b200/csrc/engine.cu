@@ -65,8 +65,9 @@ struct IpcRecord {
     int32_t rank;
     uint64_t fingerprint;
     uint64_t arena_off, outbox_off, ctrl_off, xg_off;
+    uint64_t alloc_bytes;  // size of the mapped allocation (checked build: store ranges)
     cudaIpcMemHandle_t handle;
-    unsigned char pad_[256 - 48 - sizeof(cudaIpcMemHandle_t)];
+    unsigned char pad_[256 - 56 - sizeof(cudaIpcMemHandle_t)];
 };
 static_assert(sizeof(IpcRecord) == 256, "IPC record size");
 
@@ -169,7 +170,9 @@ struct jac_ctx {
     std::vector<std::vector<int32_t>> part_peers;  // [hosted partition] -> neighbour partitions
     std::vector<jac::PartSync> hsync;              // [hosted partition]
     jac::PartSync *dsync = nullptr;
-    uint32_t *status_h = nullptr, *status_d = nullptr;  // watchdog word (mapped pinned host)
+    uint32_t *status_h = nullptr, *status_d = nullptr;  // watchdog / check words (mapped pinned host)
+    std::vector<jac::MemRange> ranges;                  // own allocation + connected peers'
+    jac::MemRange *dranges = nullptr;
     uint64_t watchdog_ns = 60ull * 1000 * 1000 * 1000;
     std::vector<void *> ipc_opened;
     bool ipc_done = false;
@@ -220,6 +223,7 @@ struct jac_ctx {
         return arena + (int64_t)(buf * nslots + slot) * geom.bstride;
     }
     jac::Watchdog wd() const { return {status_d, watchdog_ns}; }
+    jac::CheckArgs chk() const { return {dranges, (int32_t)ranges.size(), 0, status_d}; }
 };
 
 namespace {
@@ -243,7 +247,7 @@ uint64_t fingerprint(const jac_ctx *c)
 const char *const kKnobs[] = {"JAC_L2PROMO", "JAC_ZC",     "JAC_ZCHUNK", "JAC_GCOLS",   "JAC_VARIANT",
                               "JAC_AUTOTUNE", "JAC_A",      "JAC_PALIGN", "JAC_NO_DENSE", "JAC_UNROLL",
                               "JAC_PDL",     "JAC_NO_FUSED_SYNC", "JAC_ORDER_EXP", "JAC_DROP_REMOTE",
-                              "JAC_HOLD_SIGNAL", "JAC_REMOTE_SPREAD"};
+                              "JAC_HOLD_SIGNAL", "JAC_REMOTE_SPREAD", "JAC_CHECK_SELFTEST"};
 
 const char *knob(jac_ctx *c, const char *name)
 {
@@ -273,6 +277,7 @@ jac::SweepArgs sweep_args(const jac_ctx *c, int src, int mode)
     if (c->ditem_map && !c->fused) a.item_map = c->ditem_map;  // JAC_ORDER_EXP
     if (c->prof_span) a.span = c->prof_span + 4 * (int64_t)c->prof_it;
     a.wd = c->wd();
+    a.chk = c->chk();
     if (c->fused && mode == jac::MODE_FUSED) {
         a.fused_sync = 1;
         a.nremote = c->nremote;
@@ -314,12 +319,29 @@ int enqueue_barrier(jac_ctx *c)
 // The watchdog word the cross-partition waits set when a neighbour never signalled.
 int check_status(jac_ctx *c)
 {
-    if (c->status_h && *reinterpret_cast<volatile uint32_t *>(c->status_h)) {
-        *reinterpret_cast<volatile uint32_t *>(c->status_h) = 0;
-        return fail(JAC_ECUDA, "peer watchdog: a neighbour partition did not signal within %.1f s (rank skew, "
-                               "dead peer or unequal call sequences); this call's results are invalid",
-                    (double)c->watchdog_ns * 1e-9);
-    }
+    if (!c->status_h) return JAC_OK;
+    volatile uint32_t *w = c->status_h;
+    const uint32_t f = w[0];
+    if (!f) return JAC_OK;
+    const uint32_t line = w[1];
+    const unsigned long long addr = (unsigned long long)w[2] | ((unsigned long long)w[3] << 32);
+    w[0] = w[1] = w[2] = w[3] = 0;
+    if (f & (jac::kStatusMisaligned | jac::kStatusOutOfRange | jac::kStatusAssert))
+        return fail(JAC_ECUDA, "checked build: %s%s%s at kernels.cu:%u (address %#llx); the store was skipped",
+                    (f & jac::kStatusOutOfRange) ? "out-of-range store " : "",
+                    (f & jac::kStatusMisaligned) ? "misaligned store " : "",
+                    (f & jac::kStatusAssert) ? "failed assertion " : "", line, addr);
+    return fail(JAC_ECUDA, "peer watchdog: a neighbour partition did not signal within %.1f s (rank skew, "
+                           "dead peer or unequal call sequences); this call's results are invalid",
+                (double)c->watchdog_ns * 1e-9);
+}
+
+// Device copy of the store ranges (checked build): own allocation + connected peers'.
+int upload_ranges(jac_ctx *c)
+{
+    if (!c->dranges) CK(cudaMalloc(&c->dranges, sizeof(jac::MemRange) * 8));
+    if (c->ranges.size() > 8) return fail(JAC_EINVAL, "too many store ranges");
+    CK(cudaMemcpy(c->dranges, c->ranges.data(), sizeof(jac::MemRange) * c->ranges.size(), cudaMemcpyHostToDevice));
     return JAC_OK;
 }
 
@@ -780,6 +802,19 @@ int create_common(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, in
     }
     for (const auto &pp : c->part_peers)
         if (pp.size() > 6) return bail(fail(JAC_EINVAL, "more than 6 neighbour partitions"));
+#ifdef JAC_CHECKED
+    // checker self-test (tests): the first local face of the table stores 1 MiB past the
+    // end of the allocation; the checked kernels must report and skip those stores
+    if (knob(c, "JAC_CHECK_SELFTEST")) {
+        bool done = false;
+        for (jac::DevBlock &d : c->hblocks)
+            for (int f = 0; f < 6 && !done; ++f)
+                if (d.nb[f][0] && !((d.remote_mask >> f) & 1u)) {
+                    d.nb[f][0] = d.nb[f][1] = reinterpret_cast<double *>(c->alloc + c->alloc_bytes + (1 << 20));
+                    done = true;
+                }
+    }
+#endif
     // negative-control experiment (tests): faces between virtual partitions get no store
     // target, so a neighbour partition's ghosts go stale -- the result must differ
     if (c->virtual_parts && knob(c, "JAC_DROP_REMOTE"))
@@ -873,10 +908,12 @@ int create_common(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, in
     }
     // watchdog word of the cross-partition waits: mapped pinned host memory, read after
     // every synchronising call
-    if (cudaHostAlloc(&c->status_h, sizeof(uint32_t), cudaHostAllocMapped) != cudaSuccess ||
+    if (cudaHostAlloc(&c->status_h, 4 * sizeof(uint32_t), cudaHostAllocMapped) != cudaSuccess ||
         cudaHostGetDevicePointer(&c->status_d, c->status_h, 0) != cudaSuccess)
         return bail(fail(JAC_ENOMEM, "watchdog status word"));
-    *c->status_h = 0;
+    for (int k = 0; k < 4; ++k) c->status_h[k] = 0;
+    c->ranges.push_back({(unsigned long long)(uintptr_t)c->alloc, (unsigned long long)(uintptr_t)c->alloc + c->alloc_bytes});
+    if ((rc = upload_ranges(c))) return bail(rc);
     // per-partition sync table: own control words; neighbours' flag slots are local
     // for virtual partitions, filled when the peers are connected for a rank context
     c->hsync.assign(c->parts.size(), jac::PartSync{});
@@ -1133,6 +1170,13 @@ int connect_peers(jac_ctx *c, const std::vector<char *> &base, const IpcRecord *
         uint64_t *pc = reinterpret_cast<uint64_t *>(base[q] + recs[q].ctrl_off);  // rank q hosts one partition
         ps.peer_slot[n] = pc + 1 + c->rank;
     }
+    for (int n = 0; n < ps.npeers; ++n) {
+        const int32_t q = ps.peer_id[n];
+        c->ranges.push_back({(unsigned long long)(uintptr_t)base[q],
+                             (unsigned long long)(uintptr_t)base[q] + recs[q].alloc_bytes});
+    }
+    int rc;
+    if ((rc = upload_ranges(c))) return rc;
     CK(cudaMemcpy(c->dblocks, c->hblocks.data(), sizeof(jac::DevBlock) * c->nslots, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(c->dsync, c->hsync.data(), sizeof(jac::PartSync) * c->hsync.size(), cudaMemcpyHostToDevice));
     c->ipc_done = true;
@@ -1236,6 +1280,7 @@ int create_group(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, int
         recs[q].outbox_off = c->outbox_off;
         recs[q].ctrl_off = c->ctrl_off;
         recs[q].xg_off = c->xg_off;
+        recs[q].alloc_bytes = c->alloc_bytes;
     }
     for (jac_ctx *c : G->subs) {
         CK(cudaSetDevice(c->device));
@@ -1359,6 +1404,7 @@ int jac_export_ipc(jac_ctx *c, void *out)
     r.outbox_off = c->outbox_off;
     r.ctrl_off = c->ctrl_off;
     r.xg_off = c->xg_off;
+    r.alloc_bytes = c->alloc_bytes;
     CK(cudaIpcGetMemHandle(&r.handle, c->alloc));
     memcpy(out, &r, sizeof r);
     return JAC_OK;
@@ -1993,6 +2039,7 @@ int jac_destroy(jac_ctx *c)
     if (c->dblocks) cudaFree(c->dblocks);
     if (c->ditem_map) cudaFree(c->ditem_map);
     if (c->dsync) cudaFree(c->dsync);
+    if (c->dranges) cudaFree(c->dranges);
     if (c->dvcopies) cudaFree(c->dvcopies);
     if (c->status_h) cudaFreeHost(c->status_h);
     if (c->alloc) cudaFree(c->alloc);

@@ -51,10 +51,43 @@ __device__ __forceinline__ double stencil7(double c, double xm, double xp, doubl
     return __dmul_rn(s, K);
 }
 
-__device__ __forceinline__ void st_pair(double *p, double2 v, bool both)
+// ------------------------------------------------------------------ checked stores
+// Production build: plain stores.  -DJAC_CHECKED (libjacobi3d_checked.so): every store
+// is range- and alignment-checked against CheckArgs (device.hpp) and skipped on a
+// violation, which is recorded with its source line and address.
+#ifdef JAC_CHECKED
+__device__ __noinline__ void check_fail(const CheckArgs &c, uint32_t code, int line, const void *p)
 {
-    if (both) *reinterpret_cast<double2 *>(p) = v;
-    else p[0] = v.x;
+    if (!c.status) return;
+    atomicOr(c.status, code);
+    if (atomicCAS(c.status + 1, 0u, (unsigned)line) == 0u) {
+        c.status[2] = (uint32_t)(uintptr_t)p;
+        c.status[3] = (uint32_t)((unsigned long long)(uintptr_t)p >> 32);
+    }
+    __threadfence_system();
+}
+__device__ __noinline__ bool check_ptr(const CheckArgs &c, const void *p, int bytes, int line)
+{
+    const unsigned long long u = (unsigned long long)(uintptr_t)p;
+    if (u % (unsigned)bytes) { check_fail(c, kStatusMisaligned, line, p); return false; }
+    for (int r = 0; r < c.nranges; ++r)
+        if (u >= c.ranges[r].lo && u + bytes <= c.ranges[r].hi) return true;
+    check_fail(c, kStatusOutOfRange, line, p);
+    return false;
+}
+#define JAC_OK_PTR(a, p, bytes) check_ptr((a).chk, (p), (bytes), __LINE__)
+#define JAC_ASSERT(a, cond) do { if (!(cond)) check_fail((a).chk, kStatusAssert, __LINE__, nullptr); } while (0)
+#else
+#define JAC_OK_PTR(a, p, bytes) true
+#define JAC_ASSERT(a, cond) ((void)0)
+#endif
+#define ST8(a, p, v) do { double *p_ = (p); if (JAC_OK_PTR(a, p_, 8)) *p_ = (v); } while (0)
+#define ST16(a, p, v) do { double *p_ = (p); if (JAC_OK_PTR(a, p_, 16)) *reinterpret_cast<double2 *>(p_) = (v); } while (0)
+
+__device__ __forceinline__ void st_pair(const SweepArgs &a, double *p, double2 v, bool both)
+{
+    if (both) ST16(a, p, v);
+    else ST8(a, p, v.x);
 }
 
 // Does face f of `blk` have a store target in this sweep's mode (neighbour ghosts of
@@ -77,7 +110,7 @@ __device__ __forceinline__ void emit_pair(const SweepArgs &a, const DevBlock &bl
     const Geom &g = a.g;
     if (i >= g.ex) return;
     const bool both = (i + 1) < g.ex;
-    st_pair(own_plane + rowoff, v, both);
+    st_pair(a, own_plane + rowoff, v, both);
     if (a.mode == MODE_NOEXCHANGE) return;
     const bool zface = HAS_Z && ((k == 0) || (k == g.ez - 1));
     const bool yface = (j == 0) || (j == g.ey - 1);
@@ -90,20 +123,20 @@ __device__ __forceinline__ void emit_pair(const SweepArgs &a, const DevBlock &bl
         // direct-to-ghost: the neighbour's ghost layer of the OUTPUT buffer is not
         // read by anyone during this sweep, so writing it here is race-free.
         // (pack_mask faces -- JAC_F_NCCL -- go to a contiguous send buffer instead.)
-        auto packed = [&](double *p, int64_t idx) { p[idx] = v.x; if (both) p[idx + 1] = v.y; };
+        auto packed = [&](double *p, int64_t idx) { ST8(a, p + idx, v.x); if (both) ST8(a, p + idx + 1, v.y); };
         if (zface) {
             if (k == 0) {
                 double *p = blk.nb[ZM][dst];
                 if (p) {
                     if (blk.pack_mask & (1u << ZM)) packed(p, (int64_t)j * g.ex + i);
-                    else st_pair(p + (int64_t)(g.ez + 1) * g.Q + rowoff, v, both);
+                    else st_pair(a, p + (int64_t)(g.ez + 1) * g.Q + rowoff, v, both);
                 }
             }
             if (k == g.ez - 1) {
                 double *p = blk.nb[ZP][dst];
                 if (p) {
                     if (blk.pack_mask & (1u << ZP)) packed(p, (int64_t)j * g.ex + i);
-                    else st_pair(p + rowoff, v, both);
+                    else st_pair(a, p + rowoff, v, both);
                 }
             }
         }
@@ -112,14 +145,14 @@ __device__ __forceinline__ void emit_pair(const SweepArgs &a, const DevBlock &bl
                 double *p = blk.nb[YM][dst];
                 if (p) {
                     if (blk.pack_mask & (1u << YM)) packed(p, (int64_t)k * g.ex + i);
-                    else st_pair(p + (int64_t)(k + g.zg) * g.Q + (int64_t)(g.ey + 1) * g.P + g.A + i, v, both);
+                    else st_pair(a, p + (int64_t)(k + g.zg) * g.Q + (int64_t)(g.ey + 1) * g.P + g.A + i, v, both);
                 }
             }
             if (j == g.ey - 1) {
                 double *p = blk.nb[YP][dst];
                 if (p) {
                     if (blk.pack_mask & (1u << YP)) packed(p, (int64_t)k * g.ex + i);
-                    else st_pair(p + (int64_t)(k + g.zg) * g.Q + g.A + i, v, both);
+                    else st_pair(a, p + (int64_t)(k + g.zg) * g.Q + g.A + i, v, both);
                 }
             }
         }
@@ -127,32 +160,32 @@ __device__ __forceinline__ void emit_pair(const SweepArgs &a, const DevBlock &bl
         // tile write one 128-byte run per plane (merged in L2 into full sectors).
         if (i == 0) {
             double *p = blk.nb[XM][dst];
-            if (p) p[xgi] = v.x;
+            if (p) ST8(a, p + xgi, v.x);
         }
         if (last_x) {
             double *p = blk.nb[XP][dst];
-            if (p) p[xgi] = last_v;
+            if (p) ST8(a, p + xgi, last_v);
         }
     } else {  // MODE_PACK: contiguous outbox faces, layouts x:[k][j] y:[k][i] z:[j][i]
         double *ob = a.outbox + (int64_t)blk.slot * g.ostride;
         if (k == 0 && blk.nb[ZM][0]) {
             double *p = ob + g.ooff[ZM] + (int64_t)j * g.ex + i;
-            p[0] = v.x; if (both) p[1] = v.y;
+            ST8(a, p, v.x); if (both) ST8(a, p + 1, v.y);
         }
         if (k == g.ez - 1 && blk.nb[ZP][0]) {
             double *p = ob + g.ooff[ZP] + (int64_t)j * g.ex + i;
-            p[0] = v.x; if (both) p[1] = v.y;
+            ST8(a, p, v.x); if (both) ST8(a, p + 1, v.y);
         }
         if (j == 0 && blk.nb[YM][0]) {
             double *p = ob + g.ooff[YM] + (int64_t)k * g.ex + i;
-            p[0] = v.x; if (both) p[1] = v.y;
+            ST8(a, p, v.x); if (both) ST8(a, p + 1, v.y);
         }
         if (j == g.ey - 1 && blk.nb[YP][0]) {
             double *p = ob + g.ooff[YP] + (int64_t)k * g.ex + i;
-            p[0] = v.x; if (both) p[1] = v.y;
+            ST8(a, p, v.x); if (both) ST8(a, p + 1, v.y);
         }
-        if (i == 0 && blk.nb[XM][0]) ob[g.ooff[XM] + (int64_t)k * g.ey + j] = v.x;
-        if (last_x && blk.nb[XP][0]) ob[g.ooff[XP] + (int64_t)k * g.ey + j] = last_v;
+        if (i == 0 && blk.nb[XM][0]) ST8(a, ob + g.ooff[XM] + (int64_t)k * g.ey + j, v.x);
+        if (last_x && blk.nb[XP][0]) ST8(a, ob + g.ooff[XP] + (int64_t)k * g.ey + j, last_v);
     }
 }
 
@@ -434,10 +467,13 @@ __global__ void __launch_bounds__(NT, min_ctas_per_sm(NT, NS))
         uint64_t *bar = &bars[q % NS];
         const bool mid = (q >= 1) && (q <= nq - 2);
         const uint32_t bytes = L::BOX_BYTES + (mid ? ((xlo ? L::XG_BYTES : 0) + (xhi ? L::XG_BYTES : 0)) : 0);
+        JAC_ASSERT(a, c0 >= 0 && c0 < g.P && t.y0 >= 0 && t.y0 < g.ey && t.zs + q >= 0 &&
+                          t.zs + q < g.ez + 2 * g.zg && c3 >= 0 && c3 < 2 * g.nslots && q < nq);
         mbar_expect(bar, bytes);
         tma_box(&tmap, st, bar, c0, t.y0, t.zs + q, c3);
         if (mid) {
             const int64_t ko = (int64_t)(t.zs - 1 + q) * g.eyp;
+            JAC_ASSERT(a, ko + t.y0 + BY <= g.xgstride);
             if (xlo) bulk_copy(st + L::XG_OFF, xg0 + ko, L::XG_BYTES, bar);
             if (xhi) bulk_copy(st + L::XG_OFF + BY, xg1 + ko, L::XG_BYTES, bar);
         }
@@ -607,13 +643,13 @@ __global__ void __launch_bounds__(NT, min_ctas_per_sm(NT, NS))
                 double2 v;
                 v.x = stencil7(B[r].x, xm, B[r].y, ym.x, yp.x, A[r].x, C[r].x);
                 v.y = stencil7(B[r].y, B[r].x, xp1, ym.y, yp.y, A[r].y, C[r].y);
-                *reinterpret_cast<double2 *>(op + r * P) = v;
-                if (XE && xf) xf[r] = ilo ? v.x : v.y;
+                ST16(a, op + r * P, v);
+                if (XE && xf) ST8(a, xf + r, ilo ? v.x : v.y);
                 if (XE && yf && ((r == 0 && yf_lo) || (r == RY - 1 && !yf_lo))) {
                     // one 16-byte store (NVLink sends a half-written 32-byte sector as its own
                     // transfer); packed rows of odd width ex are only 8-byte aligned
-                    if (yv) *reinterpret_cast<double2 *>(yf) = v;
-                    else { yf[0] = v.x; yf[1] = v.y; }
+                    if (yv) ST16(a, yf, v);
+                    else { ST8(a, yf, v.x); ST8(a, yf + 1, v.y); }
                 }
             }
             op += Qs;
@@ -704,6 +740,8 @@ __global__ void __launch_bounds__(NT, 4) sweep2d_tma_kernel(const __grid_constan
         double *st = stage + (q % NS) * L::STRIDE;
         uint64_t *bar = &bars[q % NS];
         const int y0 = (ty0 + q) * BY;
+        JAC_ASSERT(a, c0 >= 0 && c0 < g.P && y0 >= 0 && y0 < g.ey && c3 >= 0 && c3 < 2 * g.nslots &&
+                          y0 + BY <= g.xgstride);
         mbar_expect(bar, L::BOX_BYTES + (xlo ? L::XG_BYTES : 0) + (xhi ? L::XG_BYTES : 0));
         tma_box(&tmap, st, bar, c0, y0, 0, c3);
         if (xlo) bulk_copy(st + L::XG_OFF, xg0 + y0, L::XG_BYTES, bar);
@@ -802,8 +840,8 @@ __global__ void __launch_bounds__(NT, 4) sweep2d_tma_kernel(const __grid_constan
                     double2 v;
                     v.x = stencil5(c.x, xm, c.y, rw[r].x, rw[r + 2].x);
                     v.y = stencil5(c.y, c.x, xp1, rw[r].y, rw[r + 2].y);
-                    *reinterpret_cast<double2 *>(op + r * P) = v;
-                    if (XE && xfp) xfp[r] = ilo ? v.x : v.y;
+                    ST16(a, op + r * P, v);
+                    if (XE && xfp) ST8(a, xfp + r, ilo ? v.x : v.y);
                 }
                 op += TP;
                 if (XE && xfp) xfp += BY;
@@ -881,7 +919,7 @@ __global__ void __launch_bounds__(256) ghost_fill_kernel(const SweepArgs a, int 
         if (d == 0) {
             const int64_t k = e / g.ey, j = e % g.ey;
             // JAC_F_NCCL inboxes keep the x-ghost layout (pitch eyp); outboxes [k][ey]
-            xg[k * g.eyp + j] = (blk.pack_mask & (1u << f)) ? src[k * g.eyp + j] : src[e];
+            ST8(a, xg + k * g.eyp + j, (blk.pack_mask & (1u << f)) ? src[k * g.eyp + j] : src[e]);
             continue;
         }
         int64_t off;
@@ -892,7 +930,7 @@ __global__ void __launch_bounds__(256) ghost_fill_kernel(const SweepArgs a, int 
             const int64_t j = e / g.ex, i = e % g.ex;
             off = ((f == ZM) ? 0 : (int64_t)(g.ez + 1) * g.Q) + (j + 1) * g.P + g.A + i;
         }
-        base[off] = src[e];
+        ST8(a, base + off, src[e]);
     }
 }
 
@@ -921,7 +959,7 @@ __global__ void __launch_bounds__(256) pack_face_kernel(const SweepArgs a, int s
             const int64_t j = e / g.ex, i = e % g.ex;
             off = ((f == ZM) ? 1 : (int64_t)g.ez) * g.Q + (j + 1) * g.P + g.A + i;
         }
-        ob[e] = base[off];
+        ST8(a, ob + e, base[off]);
     }
 }
 
@@ -938,7 +976,7 @@ __global__ void __launch_bounds__(256) unpack_face_kernel(const SweepArgs a, int
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
         if (d == 0) {
             const int64_t k = e / g.ey, j = e % g.ey;
-            xg[k * g.eyp + j] = src[e];
+            ST8(a, xg + k * g.eyp + j, src[e]);
             continue;
         }
         int64_t off;
@@ -949,7 +987,7 @@ __global__ void __launch_bounds__(256) unpack_face_kernel(const SweepArgs a, int
             const int64_t j = e / g.ex, i = e % g.ex;
             off = ((f == ZM) ? 0 : (int64_t)(g.ez + 1) * g.Q) + (j + 1) * g.P + g.A + i;
         }
-        base[off] = src[e];
+        ST8(a, base + off, src[e]);
     }
 }
 
@@ -1017,8 +1055,8 @@ __global__ void xghost_extract_kernel(const SweepArgs a)
         const int64_t row = (k + g.zg) * g.Q + (j + 1) * g.P + g.A;
         const double lo = b0[row - 1], hi = b0[row + g.ex];
         for (int buf = 0; buf < 2; ++buf) {
-            xg_array(a.xg, g, buf, blk.slot, 0)[k * g.eyp + j] = lo;
-            xg_array(a.xg, g, buf, blk.slot, 1)[k * g.eyp + j] = hi;
+            ST8(a, xg_array(a.xg, g, buf, blk.slot, 0) + k * g.eyp + j, lo);
+            ST8(a, xg_array(a.xg, g, buf, blk.slot, 1) + k * g.eyp + j, hi);
         }
     }
 }
@@ -1050,14 +1088,14 @@ __global__ void hash_init_kernel(const SweepArgs a, int64_t nx, int64_t ny, uint
         if (g.A == 0 && (ii == 0 || ii == sx - 1)) {  // dense rows: x ghosts -> x-ghost arrays
             if (jj >= 1 && jj <= g.ey && kk >= g.zg && kk < g.ez + g.zg) {
                 const int64_t xi = (kk - g.zg) * g.eyp + (jj - 1);
-                xg_array(a.xg, g, 0, blk.slot, ii ? 1 : 0)[xi] = v;
-                xg_array(a.xg, g, 1, blk.slot, ii ? 1 : 0)[xi] = v;
+                ST8(a, xg_array(a.xg, g, 0, blk.slot, ii ? 1 : 0) + xi, v);
+                ST8(a, xg_array(a.xg, g, 1, blk.slot, ii ? 1 : 0) + xi, v);
             }
             continue;
         }
         const int64_t off = kk * g.Q + jj * g.P + (g.A - 1) + ii;
-        b0[off] = v;
-        b1[off] = v;
+        ST8(a, b0 + off, v);
+        ST8(a, b1 + off, v);
     }
 }
 
