@@ -1,6 +1,7 @@
 #!/bin/bash
 # 1-GPU measurement campaign: bench lines per config, tile-variant check for 32-wide blocks,
-# ncu launch list of the default bench command and a full capture of the C2 ODF 8 sweep.
+# ncu launch list of the default bench command and a full capture of the C2 ODF 8 sweep
+# (-s 20: skips the 18 create-time autotune sweeps and the first two profiled ones).
 set -x
 python bench.py --steps 20 --warmup 5 > gpurun_out/r02_bench_n1.json 2> gpurun_out/r02_bench_n1.err
 for cfg in c3 c5 j2d; do
@@ -19,6 +20,6 @@ python bench.py --steps 2 --warmup 3 --no-sweep --no-cpu --no-e2e --no-sustained
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/r02_launches_bench_n1.csv \
   python bench.py --steps 2 --warmup 3 --no-sweep --no-cpu --no-e2e --no-sustained > gpurun_out/launch_ncu.log 2>&1
 python tools/profile_sweep.py --dims 512 512 512 --blocks 2 2 2 --iters 4 > gpurun_out/prof_odf8_plain.log 2>&1 &&
-ncu --set full --clock-control none --import-source on -k regex:sweep_tma -s 2 -c 1 -o gpurun_out/r02_prof_odf8 \
+ncu --set full --clock-control none --import-source on -k regex:sweep_tma -s 20 -c 1 -o gpurun_out/r02_prof_odf8 \
   python tools/profile_sweep.py --dims 512 512 512 --blocks 2 2 2 --iters 4 > gpurun_out/prof_odf8_ncu.log 2>&1
 cat gpurun_out/var_*.txt
