@@ -1,6 +1,7 @@
 """Graph-replayed us/iter of a 512^3 decomposition for values of one environment knob
 read at jac_create.  KNOB=JAC_ORDER_EXP VALUES=0,1,2 BLOCKS=2x2x2 [DIMS=512x512x512]."""
 import os, sys
+os.environ.setdefault("JAC_EXPERIMENT", "1")  # the library reads experiment knobs only with this set
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2605_12734_b200 import Jacobi3D
 

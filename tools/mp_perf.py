@@ -1,5 +1,6 @@
 """Multi-rank timing of one decomposition (torchrun).  FLAGS env = jac flags."""
 import os, sys
+os.environ.setdefault("JAC_EXPERIMENT", "1")  # the library reads experiment knobs only with this set
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch, torch.distributed as dist
 from paper_2605_12734_b200.dist import create_rank_context, destroy_rank_context

@@ -1,6 +1,7 @@
 """Graph-replayed iteration time with and without programmatic dependent launch,
 for small (launch-bound) and large grids.  JAC_PDL is read at jac_create."""
 import os, sys
+os.environ.setdefault("JAC_EXPERIMENT", "1")  # the library reads experiment knobs only with this set
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2605_12734_b200 import Jacobi3D
 

@@ -1,6 +1,7 @@
 """Graph-replayed us/iter per forced tile variant (JAC_VARIANT) for given block grids
 of a 512^3 domain.  VARS='3,13' BLOCKS='16x16x16,8x8x8'."""
 import os, sys
+os.environ.setdefault("JAC_EXPERIMENT", "1")  # the library reads experiment knobs only with this set
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2605_12734_b200 import Jacobi3D
 
