@@ -696,7 +696,15 @@ int create_common(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, in
     // took the general epilogue -- lean y faces: 445 vs 462 us for 512^3 in 32^3 blocks)
     // (64-wide blocks: 6-stage ring, 377-379 vs 399-409 us for 512^3 in 64^3 blocks;
     // 32-wide blocks: 6 stages within noise of 4, which stay)
-    else c->variant = (g.ex <= 32) ? jac::TMA_EXACT32 : (g.ex <= 64) ? jac::TMA_EXACT64_6 : jac::TMA_WIDE;
+    // 32-wide blocks of a large grid take a whole 32 x 32 face per item (half the items
+    // of 32 x 16 tiles, so half the per-item prologues and ring fills): 1024^3 in 32^3
+    // blocks 3.28-3.33 -> 3.09 ms, 512^3 in 32^3 blocks 396-398 -> 392 us.  Small grids
+    // (launch / latency bound: C1 3.9 vs 4.1 us) and rows not a multiple of 32 (ragged
+    // 22-row blocks 4.3 vs 5.1 us) keep the 32 x 16 tile (profiles/r02_tile_variants.txt).
+    else if (g.ex <= 32) {
+        const bool tall = g.ey % 32 == 0 && (int64_t)c->nslots * g.ex * g.ey * g.ez >= (int64_t)1 << 24;
+        c->variant = tall ? jac::TMA_EXACT32_TALL : jac::TMA_EXACT32;
+    } else c->variant = (g.ex <= 64) ? jac::TMA_EXACT64_6 : jac::TMA_WIDE;
     if (const char *s = knob(c, "JAC_VARIANT"); s && c->variant != kPlain) {
         const int v = atoi(s);  // tuning knob; EXACT* only where one tile spans the block row
         if (v == jac::TMA_WIDE || v == jac::TMA_WIDE4 || v == jac::TMA_NARROW ||
