@@ -28,8 +28,9 @@ for mb in (0.5, 2, 8, 64):
         for comp in (0, 1):
             us = J.jac_mb_pipeline(0, dst, nbytes, odf, comp)
             ub = J.jac_mb_pipeline_batched(0, dst, nbytes, odf, comp)
+            vb = J.jac_mb_last_verified_bytes()  # every delivered byte checked
             e4[f"{mb}MiB_odf{odf}_c{comp}"] = {"MiB": mb, "odf": odf, "compute": comp, "us": us,
                                                 "GBps": nbytes / us / 1e3, "batched_kernel_us": ub,
-                                                "batched_GBps": nbytes / ub / 1e3}
+                                                "batched_GBps": nbytes / ub / 1e3, "verified_bytes": vb}
 out["E4E5_pipeline"] = {"src": 0, "dst": dst, "rows": e4}
 print(json.dumps(out))
