@@ -37,3 +37,35 @@ def test_product_arm_refuses_without_gpu():
     p = _run("--steps", "1", "--warmup", "3", "--no-sweep", "--no-cpu", timeout=300)
     assert p.returncode != 0
     assert "no CUDA device" in (p.stderr + p.stdout)
+
+
+def test_multi_gpu_without_torchrun_is_a_single_process_run():
+    """`bench.py --gpus N` without torchrun drives the N GPUs from one process
+    (jac_create(n_gpus)); on a CPU box it stops at the missing device, not at a
+    launcher complaint, and the reference arm prints its line."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    p = _run("--gpus", "2", "--steps", "1", "--warmup", "3", "--no-sweep", "--no-cpu", timeout=300)
+    assert p.returncode != 0 and "no CUDA device" in (p.stderr + p.stdout)
+    assert "torchrun" not in (p.stderr + p.stdout)
+    p = _run("--impl", "reference", "--gpus", "4", "--steps", "1", "--warmup", "3")
+    assert p.returncode == 0, p.stderr[-2000:]
+    d = json.loads(p.stdout.strip().splitlines()[-1])
+    assert d["n_gpus"] == 4 and d["impl"] == "reference"
+
+
+def test_workload_geometry():
+    """Bench workloads follow readings R9 / R10 and the paper's grids."""
+    sys.path.insert(0, ROOT)
+    import bench
+    assert bench.workload("c2", 1, 8)[:3] == ((512, 512, 512), (2, 2, 2), (1, 1, 1))
+    assert bench.workload("c2", 4, 8)[:3] == ((512, 1024, 1024), (2, 4, 4), (1, 2, 2))
+    assert bench.workload("c2", 8, 8)[:3] == ((1024, 1024, 1024), (4, 4, 4), (2, 2, 2))
+    assert bench.workload("c4", 8, 16)[:3] == ((1536, 1536, 1536), (4, 4, 8), (2, 2, 2))
+    # the paper's Jacobi2D strong grid: minimum cut splits x first (98304 < 131072)
+    assert bench.workload("j2d_strong", 2, 1)[:3] == ((131072, 98304, 1), (2, 1, 1), (2, 1, 1))
+    assert bench.workload("j2d_strong", 4, 8)[:3] == ((131072, 98304, 1), (8, 4, 1), (2, 2, 1))
+    assert bench.workload("j2d_strong", 8, 16)[2] == (4, 2, 1)
+    assert bench.gpu_grid_2d_r10(4, 131072, 98304) == (2, 2)
+    assert bench.blocks_for_odf_2d((32768, 32768), 8) == (2, 4)
