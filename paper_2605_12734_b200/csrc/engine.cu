@@ -182,8 +182,10 @@ struct jac_ctx {
     std::vector<jac::FaceCopy> vcopies; // JAC_F_VIRTUAL_GPUS | JAC_F_NCCL: the virtual transport
     jac::FaceCopy *dvcopies = nullptr;
     int64_t vcopy_max = 0;
-    int32_t *ditem_map = nullptr;       // launch order -> item (remote-touching items first)
+    int32_t *ditem_map = nullptr;       // launch order -> item (~item: remote-touching)
     int32_t nremote = 0;
+    std::vector<int32_t> nremote_part;  // remote-touching items per hosted partition
+    bool tuned = false;                 // the create-time default variant was re-timed on data
 
     cudaStream_t stream = nullptr;
     // JAC_F_PER_BLOCK (paper-style): one stream per block, events per block and parity
@@ -501,17 +503,19 @@ void configure_tiles(jac_ctx *c)
     }
 }
 
-// Create-time autotune of the wide tile's TMA ring depth (6 stages at 3 CTAs / SM vs
-// 4 stages at 4 CTAs / SM) on the context's own decomposition and GPU: 1 + 8 sweeps
-// each, exchange off, the faster wins (ties within 0.5%: 6 stages).  Measured with
-// the lean z-march: 3-D 512^3 ODF 1 and 8 within 0.6% either way (a few boxes: 4
-// stages 2% faster), ODF 16 / 64 6 stages 1.5% / 3% faster.  2-D takes 4 stages
-// without timing: 5% faster on every box and in both power regimes (2614 vs 2742 us
-// per 32768^2 sweep), while the create-time timing on the fresh arena sometimes
-// picked 6.  Results are bit-identical either way.  JAC_AUTOTUNE=0 (6 stages) or
-// JAC_VARIANT skip it.
-int autotune(jac_ctx *c)
+int build_item_map(jac_ctx *c);
+
+// Autotune of the wide tile's TMA ring depth (6 stages at 3 CTAs / SM vs 4 stages at
+// 4 CTAs / SM) on the context's own decomposition, GPU and data: 1 + 8 sweeps each,
+// exchange off, the faster wins (ties within 0.5%: 6 stages).  Measured with the lean
+// z-march: 3-D 512^3 ODF 1 and 8 within 0.6% either way (a few boxes: 4 stages 2%
+// faster), ODF 16 / 64 6 stages 1.5% / 3% faster.  2-D takes 4 stages without timing:
+// 5% faster on every box and in both power regimes (2614 vs 2742 us per 32768^2 sweep).
+// Results are bit-identical either way.  JAC_AUTOTUNE=0 (6 stages) or JAC_VARIANT skip it.
+// At create: the fixed choices (2-D: 4 stages); whether the 3-D wide tile is timed.
+int autotune_at_create(jac_ctx *c)
 {
+    c->tuned = true;
     if (c->variant != jac::TMA_WIDE || knob(c, "JAC_VARIANT")) return JAC_OK;
     if (c->flags & JAC_F_2D) {  // 2-D: 4 stages measured 5% faster on every box, both regimes
         c->variant = jac::TMA_WIDE4;
@@ -519,6 +523,21 @@ int autotune(jac_ctx *c)
         return JAC_OK;
     }
     if (const char *s = knob(c, "JAC_AUTOTUNE"); s && atoi(s) == 0) return JAC_OK;
+    c->tuned = false;  // timed at the first jac_step / jac_profile_sweep, on the initial field
+    return JAC_OK;
+}
+
+// The timing itself, run once before the first graph is built: both ring depths sweep
+// the context's own initialised field (MODE_NOEXCHANGE reads the current buffer and
+// writes only the other buffer's interiors, which the next real sweep overwrites
+// whole; no ghost, shell or neighbour memory is touched), so the choice is made on real
+// data and in the state the run will be in, not on the zeroed arena of jac_create.
+int autotune(jac_ctx *c)
+{
+    if (c->tuned) return JAC_OK;
+    c->tuned = true;
+    const int src = (int)(c->iters & 1);
+    const int before = c->variant;
     const int cands[2] = {jac::TMA_WIDE, jac::TMA_WIDE4};
     float ms_of[2] = {0.f, 0.f};
     for (int n = 0; n < 2; ++n) {
@@ -527,7 +546,7 @@ int autotune(jac_ctx *c)
         configure_tiles(c);
         if (jac::prepare_sweep_tma(v) != cudaSuccess || jac::prepare_sweep2d_tma(v) != cudaSuccess)
             return fail(JAC_ECUDA, "autotune: kernel attribute");
-        const jac::SweepArgs a = sweep_args(c, 0, jac::MODE_NOEXCHANGE);
+        const jac::SweepArgs a = sweep_args(c, src, jac::MODE_NOEXCHANGE);
         auto launch = [&]() {
             return (c->flags & JAC_F_2D) ? jac::launch_sweep2d_tma(c->tmap, a, v, c->stream)
                                          : jac::launch_sweep_tma(c->tmap, a, v, c->stream);
@@ -543,6 +562,12 @@ int autotune(jac_ctx *c)
     // ties (< 0.5%) go to the usual winner, 6 stages
     c->variant = (ms_of[1] < 0.995f * ms_of[0]) ? jac::TMA_WIDE4 : jac::TMA_WIDE;
     configure_tiles(c);
+    if (c->variant != before) {  // the launch order depends on the tile list
+        int rc;
+        if ((rc = build_item_map(c))) return rc;
+        for (size_t h = 0; h < c->hsync.size(); ++h) c->hsync[h].nremote = c->nremote_part[h];
+        CK(cudaMemcpy(c->dsync, c->hsync.data(), sizeof(jac::PartSync) * c->hsync.size(), cudaMemcpyHostToDevice));
+    }
     return JAC_OK;
 }
 
@@ -599,6 +624,66 @@ std::vector<int32_t> remote_first_order(jac_ctx *c, const std::vector<uint32_t> 
             if (cls[it] == 0) (*first_per_part)[c->hblocks[items[it].b].part]++;
     }
     return order;
+}
+
+// Launch order of the sweep's work items (depends on the tile variant): with fused
+// cross-partition ordering, the remote-touching items (marked ~item) spread over the
+// first quarter; sets c->fused, c->nremote and the per-partition remote item counts.
+int build_item_map(jac_ctx *c)
+{
+    c->fused = (c->rank_mode || c->virtual_parts) && c->has_remote() && sweep_mode(c) == jac::MODE_FUSED &&
+               c->variant != kPlain && !(c->flags & (JAC_F_NCCL | JAC_F_PER_BLOCK)) && !knob(c, "JAC_NO_FUSED_SYNC");
+    // experiment knob (single-GPU contexts): the remote-first launch order of a rank
+    // whose z- and y- faces were remote, without any sync -- isolates the cost of the
+    // order itself.  1 = remote-first, 2 = remote-first + halo partners.
+    const int order_exp = (!c->rank_mode && !c->virtual_parts && knob(c, "JAC_ORDER_EXP")) ? atoi(knob(c, "JAC_ORDER_EXP")) : 0;
+    std::vector<int32_t> &nremote_part = c->nremote_part;
+    nremote_part.assign(c->parts.size(), 0);
+    c->nremote = 0;
+    if (c->ditem_map) { cudaFree(c->ditem_map); c->ditem_map = nullptr; }
+    if (c->fused || (order_exp && c->variant != kPlain)) {
+        std::vector<uint32_t> mask(c->nslots);
+        for (int32_t sl = 0; sl < c->nslots; ++sl)
+            mask[sl] = c->fused ? c->hblocks[sl].remote_mask
+                                : (((c->hblocks[sl].org[2] == 0) ? 1u << jac::ZM : 0u) |
+                                   ((c->hblocks[sl].org[1] == 0) ? 1u << jac::YM : 0u));
+        // remote-touching items first: their signal leaves early in the sweep, so the
+        // next sweep's remote items (which wait for it) find it already set
+        int32_t nfirst = 0;
+        std::vector<int32_t> order = remote_first_order(c, mask, order_exp == 2, &nfirst, &nremote_part);
+        if (c->fused) {
+            c->nremote = nfirst;
+            // remote-touching items are marked in the map (~item): they wait before their
+            // first staging copy and signal after their last store
+            for (int32_t i = 0; i < nfirst; ++i) order[i] = ~order[i];
+            // The remote items are spread evenly over the first quarter of the launch order
+            // rather than all launched first: their signal still leaves early (the next
+            // sweep's waits stay short), but the first waves no longer consist only of
+            // scattered face items that lose their halo partners' L2 reuse and all store
+            // over NVLink at once.  Same-box A/B at N = 4 (profiles/r02_remote_spread.txt):
+            // C2 ODF 8 0.3461 -> 0.3374-0.3382 ms/iter, ODF 64 -2.0%, C3 -1.3%, C4 ODF 16
+            // -0.8%, C5 -0.8%; N = 2 neutral.  JAC_REMOTE_SPREAD=<percent> (0 = all first).
+            double f = 0.25;
+            if (const char *sp = knob(c, "JAC_REMOTE_SPREAD")) f = std::min(1.0, std::max(0.0, atof(sp) / 100.0));
+            if (f > 0 && nfirst > 0 && nfirst < c->nitems) {
+                const int64_t span = std::max<int64_t>(nfirst, (int64_t)(f * c->nitems));
+                std::vector<int32_t> spread;
+                spread.reserve(order.size());
+                int32_t r = 0, o = nfirst;
+                for (int64_t pos = 0; pos < (int64_t)order.size(); ++pos) {
+                    const bool take_remote = r < nfirst && (pos >= span - (nfirst - r) ||
+                                                            pos * nfirst >= (int64_t)r * span);
+                    spread.push_back(take_remote ? order[r++] : order[o++]);
+                }
+                order.swap(spread);
+            }
+        }
+        if (cudaMalloc(&c->ditem_map, sizeof(int32_t) * order.size()) != cudaSuccess ||
+            cudaMemcpy(c->ditem_map, order.data(), sizeof(int32_t) * order.size(), cudaMemcpyHostToDevice) != cudaSuccess)
+            return fail(JAC_ENOMEM, "item map");
+        if (c->fused && c->nremote == 0) c->fused = false;
+    }
+    return JAC_OK;
 }
 
 int create_common(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, int32_t bz,
@@ -864,56 +949,8 @@ int create_common(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, in
             if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess)
                 return bail(fail(JAC_ECUDA, "per-block event creation"));
     }
-    if ((rc = autotune(c))) return bail(rc);  // fixes the variant: the item map depends on it
-    c->fused = (rank_mode || c->virtual_parts) && c->has_remote() && sweep_mode(c) == jac::MODE_FUSED &&
-               c->variant != kPlain && !(flags & (JAC_F_NCCL | JAC_F_PER_BLOCK)) && !knob(c, "JAC_NO_FUSED_SYNC");
-    // experiment knob (single-GPU contexts): the remote-first launch order of a rank
-    // whose z- and y- faces were remote, without any sync -- isolates the cost of the
-    // order itself.  1 = remote-first, 2 = remote-first + halo partners.
-    const int order_exp = (!rank_mode && !c->virtual_parts && knob(c, "JAC_ORDER_EXP")) ? atoi(knob(c, "JAC_ORDER_EXP")) : 0;
-    std::vector<int32_t> nremote_part(c->parts.size(), 0);
-    if (c->fused || (order_exp && c->variant != kPlain)) {
-        std::vector<uint32_t> mask(c->nslots);
-        for (int32_t sl = 0; sl < c->nslots; ++sl)
-            mask[sl] = c->fused ? c->hblocks[sl].remote_mask
-                                : (((c->hblocks[sl].org[2] == 0) ? 1u << jac::ZM : 0u) |
-                                   ((c->hblocks[sl].org[1] == 0) ? 1u << jac::YM : 0u));
-        // remote-touching items first: their signal leaves early in the sweep, so the
-        // next sweep's remote items (which wait for it) find it already set
-        int32_t nfirst = 0;
-        std::vector<int32_t> order = remote_first_order(c, mask, order_exp == 2, &nfirst, &nremote_part);
-        if (c->fused) {
-            c->nremote = nfirst;
-            // remote-touching items are marked in the map (~item): they wait before their
-            // first staging copy and signal after their last store
-            for (int32_t i = 0; i < nfirst; ++i) order[i] = ~order[i];
-            // The remote items are spread evenly over the first quarter of the launch order
-            // rather than all launched first: their signal still leaves early (the next
-            // sweep's waits stay short), but the first waves no longer consist only of
-            // scattered face items that lose their halo partners' L2 reuse and all store
-            // over NVLink at once.  Same-box A/B at N = 4 (profiles/r02_remote_spread.txt):
-            // C2 ODF 8 0.3461 -> 0.3374-0.3382 ms/iter, ODF 64 -2.0%, C3 -1.3%, C4 ODF 16
-            // -0.8%, C5 -0.8%; N = 2 neutral.  JAC_REMOTE_SPREAD=<percent> (0 = all first).
-            double f = 0.25;
-            if (const char *sp = knob(c, "JAC_REMOTE_SPREAD")) f = std::min(1.0, std::max(0.0, atof(sp) / 100.0));
-            if (f > 0 && nfirst > 0 && nfirst < c->nitems) {
-                const int64_t span = std::max<int64_t>(nfirst, (int64_t)(f * c->nitems));
-                std::vector<int32_t> spread;
-                spread.reserve(order.size());
-                int32_t r = 0, o = nfirst;
-                for (int64_t pos = 0; pos < (int64_t)order.size(); ++pos) {
-                    const bool take_remote = r < nfirst && (pos >= span - (nfirst - r) ||
-                                                            pos * nfirst >= (int64_t)r * span);
-                    spread.push_back(take_remote ? order[r++] : order[o++]);
-                }
-                order.swap(spread);
-            }
-        }
-        if (cudaMalloc(&c->ditem_map, sizeof(int32_t) * order.size()) != cudaSuccess ||
-            cudaMemcpy(c->ditem_map, order.data(), sizeof(int32_t) * order.size(), cudaMemcpyHostToDevice) != cudaSuccess)
-            return bail(fail(JAC_ENOMEM, "item map"));
-        if (c->fused && c->nremote == 0) c->fused = false;
-    }
+    if ((rc = autotune_at_create(c))) return bail(rc);
+    if ((rc = build_item_map(c))) return bail(rc);
     // watchdog word of the cross-partition waits: mapped pinned host memory, read after
     // every synchronising call
     if (cudaHostAlloc(&c->status_h, 4 * sizeof(uint32_t), cudaHostAllocMapped) != cudaSuccess ||
@@ -930,7 +967,7 @@ int create_common(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, in
         ps.ctrl = c->ctrl + (int64_t)h * c->ctrl_stride;
         ps.count = reinterpret_cast<unsigned long long *>(ps.ctrl + 1 + n_gpus);
         ps.npeers = (int32_t)c->part_peers[h].size();
-        ps.nremote = nremote_part[h];
+        ps.nremote = c->nremote_part[h];
         // watchdog experiment (tests): partition 0 never signals its sweeps
         if (h == 0 && knob(c, "JAC_HOLD_SIGNAL")) ps.nremote = 0x7fffffff;
         for (int n = 0; n < ps.npeers; ++n) {
@@ -1099,6 +1136,7 @@ bool use_graphs(const jac_ctx *c) { return !(c->flags & (JAC_F_NO_GRAPH | JAC_F_
 int step_begin(jac_ctx *c)
 {
     int rc;
+    if ((rc = autotune(c))) return rc;
     if (use_graphs(c) && !c->g1[0]) {
         for (int s = 0; s < 2; ++s) {
             if ((rc = build_graph(c, s, 1, &c->g1[s]))) return rc;
@@ -1675,6 +1713,7 @@ int jac_profile_sweep(jac_ctx *c, int32_t n, double *avg_ms)
     }
     if (c->flags & JAC_F_PER_BLOCK) return fail(JAC_EINVAL, "jac_profile_sweep: not available with JAC_F_PER_BLOCK");
     CK(cudaSetDevice(c->device));
+    if ((rc = autotune(c))) return rc;
     struct Events {  // destroyed on every return path
         std::vector<cudaEvent_t> v;
         ~Events() { for (cudaEvent_t e : v) if (e) cudaEventDestroy(e); }
