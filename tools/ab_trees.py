@@ -2,7 +2,8 @@
 its own built libjacobi3d.so, e.g. _r1/), graph-replayed us/iter per case, one child
 process per (tree, case) so each loads its own binding and library; interleaved
 repetitions, median reported.
-    ROOT_B=_r1 CASES=512x512x512:16x16x16 REPS=3 python tools/ab_trees.py"""
+    ROOT_B=_r1 CASES=512x512x512:16x16x16 REPS=3 python tools/ab_trees.py
+2-D cases: "2d131072x98304:2x1" (dims:blocks); AB_GPUS=N runs jac_create(n_gpus=N)."""
 import json
 import os
 import statistics
@@ -10,16 +11,21 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-ROOTS = [os.environ.get("ROOT_A", ROOT), os.environ.get("ROOT_B", os.path.join(ROOT, "_r1"))]
+ROOTS = [os.environ.get("ROOT_A", ROOT), os.environ.get("ROOT_B", os.path.join(ROOT, "_prev"))]
 CASES = os.environ.get("CASES", "512x512x512:1x1x1,512x512x512:2x2x2,512x512x512:4x4x4,512x512x512:8x8x8,"
                        "512x512x512:16x16x16,1024x1024x1024:32x32x32").split(",")
 CHILD = r'''
 import os, sys, json, time
 sys.path.insert(0, sys.argv[1])
 from paper_2605_12734_b200 import Jacobi3D
-dims = tuple(int(x) for x in sys.argv[2].split("x")); blocks = tuple(int(x) for x in sys.argv[3].split("x"))
-n = max(10, int(4e9 / (dims[0] * dims[1] * dims[2])))
-with Jacobi3D(dims, blocks) as J:
+from paper_2605_12734_b200 import Jacobi2D
+ngpu = int(os.environ.get("AB_GPUS", "1"))
+two_d = sys.argv[2].startswith("2d")
+dims = tuple(int(x) for x in sys.argv[2].replace("2d", "").split("x")); blocks = tuple(int(x) for x in sys.argv[3].split("x"))
+pts = 1
+for d in dims: pts *= d
+n = max(10, int(4e9 * ngpu / pts))
+with (Jacobi2D(dims, blocks, n_gpus=ngpu) if two_d else Jacobi3D(dims, blocks, n_gpus=ngpu)) as J:
     J.set_init_hash(1); J.step(10); time.sleep(0.25); J.step(n)
     ms = J.last_step_ms() / n
     time.sleep(0.25)
