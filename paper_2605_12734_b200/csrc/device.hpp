@@ -184,22 +184,16 @@ JAC_HD inline TileItem decode_item3d(const SweepArgs &a, int item, int BX, int B
     return t;
 }
 
-// item -> (block, x tile, chunk of y tiles) for the 2-D sweep; nzc = y chunks per
-// block.  2-D columns (block, x tile) are grouped like the 3-D ones (ncols = 2-D
-// columns, gcols per group) and the y chunks of a group run chunk-major inside it, so
-// the y-halo rows two vertically adjacent chunks share are read while still in L2
-// even when a block is thousands of tiles wide.
+// item -> (block, x tile, chunk of y tiles) for the 2-D sweep; nzc = y chunks per block.
+// (x tile fastest.  Grouping the x tiles into column groups like the 3-D list, with the
+// y chunks of a group chunk-major, was measured 1-4% slower on 32768^2 and 131072-wide
+// blocks: profiles/r02_j2d_column_groups.txt.)
 JAC_HD inline TileItem decode_item2d(const SweepArgs &a, int item, int BX, int BY)
 {
     TileItem t;
-    const int grp = item / (a.gcols * a.nzc);
-    const int r = item - grp * a.gcols * a.nzc;
-    const int rest = a.ncols - grp * a.gcols;
-    const int gsize = a.gcols < rest ? a.gcols : rest;
-    const int yc = r / gsize;
-    const int col = grp * a.gcols + (r - yc * gsize);
-    const int tx = col % a.ntx;
-    t.b = col / a.ntx;
+    const int tx = item % a.ntx; item /= a.ntx;
+    const int yc = item % a.nzc;
+    t.b = item / a.nzc;
     const int tpc = (a.nty + a.nzc - 1) / a.nzc;
     t.x0 = tx * BX;
     t.zs = yc * tpc;

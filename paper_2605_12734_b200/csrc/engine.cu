@@ -498,9 +498,7 @@ void configure_tiles(jac_ctx *c)
         c->gcols = std::max(1, std::min(c->ncols, gcols > 0 ? gcols : c->ncols));
         if (flags & JAC_F_2D) {  // 2-D: items = (block, x tile, chunk of 8 y tiles), nzc = y chunks
             c->nzc = std::max(1, (c->nty + 7) / 8);
-            c->ncols = c->nslots * c->ntx;  // 2-D columns: (block, x tile)
-            c->gcols = std::max(1, std::min(c->ncols, gcols > 0 ? gcols : c->ncols));
-            c->nitems = c->ncols * c->nzc;
+            c->nitems = c->nslots * c->ntx * c->nzc;
         }
     }
 }
@@ -1025,8 +1023,7 @@ int enqueue_per_block(jac_ctx *c, int64_t t, int first, int stride)
         if (c->variant == kPlain) {
             CK(jac::launch_sweep_plain_one(a, s));
         } else if (c->flags & JAC_F_2D) {
-            a.ncols = a.gcols = c->ntx;  // (x tile, y chunk) items of this block
-            a.nitems = c->ntx * c->nzc;
+            a.nitems = c->ntx * c->nzc;  // (x tile, y chunk) items of this block
             CK(jac::launch_sweep2d_tma(c->tmap, a, c->variant, s));
         } else {
             CK(jac::launch_sweep_tma(c->tmap, a, c->variant, s));
