@@ -249,7 +249,7 @@ uint64_t fingerprint(const jac_ctx *c)
 const char *const kKnobs[] = {"JAC_L2PROMO", "JAC_ZC",     "JAC_ZCHUNK", "JAC_GCOLS",   "JAC_VARIANT",
                               "JAC_AUTOTUNE", "JAC_A",      "JAC_PALIGN", "JAC_NO_DENSE", "JAC_UNROLL",
                               "JAC_PDL",     "JAC_NO_FUSED_SYNC", "JAC_ORDER_EXP", "JAC_DROP_REMOTE",
-                              "JAC_HOLD_SIGNAL", "JAC_REMOTE_SPREAD", "JAC_CHECK_SELFTEST"};
+                              "JAC_HOLD_SIGNAL", "JAC_REMOTE_SPREAD", "JAC_CHECK_SELFTEST", "JAC_YCHUNK"};
 
 const char *knob(jac_ctx *c, const char *name)
 {
@@ -497,7 +497,9 @@ void configure_tiles(jac_ctx *c)
         if (const char *s = knob(c, "JAC_GCOLS")) gcols = atoi(s);
         c->gcols = std::max(1, std::min(c->ncols, gcols > 0 ? gcols : c->ncols));
         if (flags & JAC_F_2D) {  // 2-D: items = (block, x tile, chunk of 8 y tiles), nzc = y chunks
-            c->nzc = std::max(1, (c->nty + 7) / 8);
+            int ytiles = 8;
+            if (const char *s = knob(c, "JAC_YCHUNK")) ytiles = std::max(1, atoi(s));
+            c->nzc = std::max(1, (c->nty + ytiles - 1) / ytiles);
             c->nitems = c->nslots * c->ntx * c->nzc;
         }
     }
