@@ -131,3 +131,49 @@ def test_single_process_multi_gpu_2d():
         s.step(13)
         got = s.field(u0)
     assert np.array_equal(got.view(np.uint64), oracle.jacobi2d_omp(u0, 13)[0].view(np.uint64))
+
+
+def test_single_process_multi_gpu_api_surface():
+    """The group context answers the whole C ABI like a 1-GPU one: layout, owner,
+    regions spanning devices, padded blocks, stats totals, options, errors naming the
+    argument, and the watchdog option on every device."""
+    import numpy as np
+
+    sys.path.insert(0, ROOT)
+    import jac_inputs as JI
+    import oracle
+    import paper_2605_12734_b200 as jb
+    from paper_2605_12734_b200 import jacobi3d as J
+
+    if _ngpu() < 2:
+        pytest.skip("needs 2 GPUs")
+    dims, blocks = (64, 48, 80), (2, 2, 4)
+    u0 = JI.hash_field(*dims, seed=5)
+    want = oracle.jacobi3d_omp(u0, 7)[0]
+    with jb.Jacobi3D(dims, blocks, n_gpus=2) as s:
+        assert s.gpu_grid == (1, 1, 2)
+        assert s.owner(0, 0, 0) == 0 and s.owner(1, 1, 3) == 1
+        o, e = s.local_box()
+        assert o == (0, 0, 0) and e == (66, 50, 82)
+        s.set_option(J.JAC_OPT_WATCHDOG_MS, 30000)
+        s.set_init(u0)
+        s.step(7)
+        # a region across the device seam (z = 40)
+        reg = s.region((5, 3, 30), (20, 30, 20))
+        assert np.array_equal(reg, want[31:51, 4:34, 6:26])
+        pb = s.block_padded(1, 1, 2)   # device 1, ghosts written by device 0 over NVLink
+        ex, ey, ez = s.block_extent
+        assert np.array_equal(pb[1:-1, 1:-1, 1:-1], want[1 + 2 * ez:1 + 3 * ez, 1 + ey:1 + 2 * ey, 1 + ex:1 + 2 * ex])
+        assert np.array_equal(pb[0, 1:-1, 1:-1], want[2 * ez, 1 + ey:1 + 2 * ey, 1 + ex:1 + 2 * ex])  # z- ghost
+        st = s.stats()
+        assert st["local_blocks"] == 16 and st["partitions"] == 2 and st["kernels_per_iter"] == 1
+        assert s.iterations == 7 and s.last_step_ms() > 0
+        with pytest.raises(J.JacError) as ei:
+            s.block(2, 0, 0)
+        assert ei.value.code == J.JAC_EINVAL
+        with pytest.raises(J.JacError) as ei:
+            J.jac_export_ipc(s.ctx)
+        assert ei.value.code == J.JAC_ESTATE
+    with pytest.raises(J.JacError) as ei:
+        jb.Jacobi3D(dims, blocks, n_gpus=2, flags=J.JAC_F_NCCL)
+    assert ei.value.code == J.JAC_EINVAL

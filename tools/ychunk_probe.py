@@ -5,19 +5,22 @@ os.environ.setdefault("JAC_EXPERIMENT", "1")
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2605_12734_b200 import Jacobi2D
 
-cases = [tuple(map(int, c.split("x"))) for c in os.environ.get("DIMS", "131072x16384,32768x32768").split(",")]
+cases = []
+for c in os.environ.get("DIMS", "131072x16384,32768x32768").split(","):
+    d, _, b = c.partition(":")
+    cases.append((tuple(map(int, d.split("x"))), tuple(map(int, b.split("x"))) if b else (1, 1)))
 chunks = os.environ.get("CHUNKS", "2,4,8,16,32").split(",")
 R = int(os.environ.get("R", "3"))
-for dims in cases:
+for dims, blocks in cases:
     res = {c: [] for c in chunks}
     for _ in range(R):
         for ch in chunks:
             os.environ["JAC_YCHUNK"] = ch
-            with Jacobi2D(dims, (1, 1)) as J:
+            with Jacobi2D(dims, blocks) as J:
                 J.set_init_hash(1)
                 J.step(10)
                 time.sleep(0.2)
                 n = max(10, int(4e9 / (dims[0] * dims[1])))
                 J.step(n)
                 res[ch].append(J.last_step_ms() / n * 1e3)
-    print(f"{dims[0]}x{dims[1]}: " + "  ".join(f"ychunk {c}: {statistics.median(v):.1f} us" for c, v in res.items()), flush=True)
+    print(f"{dims[0]}x{dims[1]} blocks {blocks}: " + "  ".join(f"ychunk {c}: {statistics.median(v):.1f} us" for c, v in res.items()), flush=True)
