@@ -796,7 +796,7 @@ int create_common(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, in
     } else c->variant = (g.ex <= 64) ? jac::TMA_EXACT64_6 : jac::TMA_WIDE;
     if (const char *s = knob(c, "JAC_VARIANT"); s && c->variant != kPlain) {
         const int v = atoi(s);  // tuning knob; EXACT* only where one tile spans the block row
-        if (v == jac::TMA_WIDE || v == jac::TMA_WIDE4 || v == jac::TMA_NARROW ||
+        if (v == jac::TMA_WIDE || v == jac::TMA_WIDE4 || v == jac::TMA_NARROW || v == jac::TMA_WIDE_TALL ||
             ((v == jac::TMA_EXACT32 || v == jac::TMA_EXACT32_TALL || v == jac::TMA_EXACT32_6) && g.ex <= 32) ||
             ((v == jac::TMA_EXACT64 || v == jac::TMA_EXACT64_6) && g.ex <= 64))
             c->variant = v;

@@ -417,13 +417,14 @@ __device__ __forceinline__ int tile_soff(const Geom &g, int x0)
 // Persistent-free TMA z-march: one CTA per work item.  BX x BY column tile, NT
 // threads, NS-deep plane ring, staged width W (BX + 4 with in-block x halo, or BX
 // for single-tile blocks).  Each thread owns a pair of x-points (double2) in RY rows.
-constexpr int min_ctas_per_sm(int NT, int NS)
+constexpr int min_ctas_per_sm(int NT, int NS, int BX = 64, int BY = 16)
 {
-    return NT >= 512 ? 2 : NT <= 128 ? 8 : (NS >= 8 ? 2 : (NS >= 6 ? 3 : 4));
+    // 64 x 32 tiles (4 rows per thread) need > 80 registers: 2 CTAs per SM
+    return (BX >= 64 && BY >= 32) ? 2 : NT >= 512 ? 2 : NT <= 128 ? 8 : (NS >= 8 ? 2 : (NS >= 6 ? 3 : 4));
 }
 
 template <int BX, int BY, int W, int NT, int NS>
-__global__ void __launch_bounds__(NT, min_ctas_per_sm(NT, NS))
+__global__ void __launch_bounds__(NT, min_ctas_per_sm(NT, NS, BX, BY))
     sweep_tma_kernel(const __grid_constant__ CUtensorMap tmap, const SweepArgs a)
 {
     using L = StageLayout<BX, BY, W>;
@@ -1175,7 +1176,8 @@ static cudaError_t launch_tma_t(const CUtensorMap &tm, const SweepArgs &a, cudaS
     X(TMA_EXACT64, 64, 16, 64, 256, 4)    \
     X(TMA_EXACT32_TALL, 32, 32, 32, 256, 4) \
     X(TMA_EXACT32_6, 32, 16, 32, 256, 6)    \
-    X(TMA_EXACT64_6, 64, 16, 64, 256, 6)
+    X(TMA_EXACT64_6, 64, 16, 64, 256, 6)    \
+    X(TMA_WIDE_TALL, 64, 32, 68, 256, 4)
 
 int sweep_resident_ctas(int variant)
 {

@@ -15,7 +15,9 @@ enum TmaVariant {
     TMA_EXACT64 = 4, /* 64 x 16 tiles, staged 64 wide: one tile per block row (ex <= 64) */
     TMA_EXACT32_TALL = 12, /* 32 x 32 tiles: a whole 32^2 block face per item (ex <= 32) */
     TMA_EXACT32_6 = 13,    /* 32 x 16 tiles, 6-stage ring (ex <= 32) */
-    TMA_EXACT64_6 = 14     /* 64 x 16 tiles, 6-stage ring (ex <= 64) */
+    TMA_EXACT64_6 = 14,    /* 64 x 16 tiles, 6-stage ring (ex <= 64) */
+    TMA_WIDE_TALL = 15     /* 64 x 32 tiles staged 68 x 34, 4-stage ring, 2 CTAs / SM (experiment:
+                              fewer shared-memory loads and less staging over-fetch per point) */
 };
 struct TileShape { int bx, by, w; };
 
