@@ -201,7 +201,7 @@ def test_c2_full_size_bench_config():
     _lightcone_check(got, u0, n, [(0, 0, 0), (252, 252, 252), (504, 100, 255), (127, 383, 504)])
 
 
-@pytest.mark.parametrize("variant", ["0", "1", "3", "4", "5", "12", "13", "14"])
+@pytest.mark.parametrize("variant", ["0", "1", "3", "4", "5", "12", "13", "14", "15"])
 @pytest.mark.parametrize("dims,blocks", [((64, 40, 36), (2, 2, 2)), ((128, 34, 20), (2, 1, 1)),
                                          ((58, 30, 17), (2, 1, 1)), ((130, 51, 33), (1, 3, 1))])
 def test_tma_tile_variants(monkeypatch, variant, dims, blocks):
