@@ -202,7 +202,12 @@ int jac_local_box(const jac_ctx *c, int64_t *origin, int64_t *extent);
 int jac_set_init_hash(jac_ctx *c, uint64_t seed);
 
 /* Runs exactly n_iters >= 0 Jacobi sweeps (R12; 0 = identity; accumulates across
- * calls).  Blocking: returns after this context's GPUs finish. */
+ * calls).  Blocking: returns after this context's GPUs finish.  The first call after
+ * jac_create (or the first jac_profile_sweep) also times the two ring depths of the
+ * wide tile on the initialised field (18 extra sweeps that write only the other
+ * buffer's interiors; results unaffected) unless JAC_AUTOTUNE=0 / JAC_VARIANT are set
+ * as experiment knobs.  JAC_ECUDA with "peer watchdog" if a neighbour partition did
+ * not signal within JAC_OPT_WATCHDOG_MS (the results of this call are then invalid). */
 int jac_step(jac_ctx *c, int32_t n_iters);
 
 /* Interior of block (ix,iy,iz) after the sweeps so far, ex*ey*ez doubles, x fastest,
