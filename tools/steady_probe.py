@@ -31,7 +31,7 @@ def main():
         # SETTINGS: ';'-separated list of env settings, each 'K=V,K=V' ('plain' = JAC_F_NO_TMA)
         for var in os.environ.get("SETTINGS", "JAC_VARIANT=0;JAC_VARIANT=5;JAC_VARIANT=12;plain").split(";"):
             flags = 0
-            for key in ("JAC_VARIANT", "JAC_ZCHUNK", "JAC_GCOLS", "JAC_ZC", "JAC_L2PROMO", "JAC_PDL"):
+            for key in ("JAC_VARIANT", "JAC_ZCHUNK", "JAC_GCOLS", "JAC_ZC", "JAC_L2PROMO", "JAC_PDL", "JAC_YCHUNK"):
                 os.environ.pop(key, None)
             if var == "plain":
                 flags = 1 << 5
