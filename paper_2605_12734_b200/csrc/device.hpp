@@ -71,6 +71,9 @@ struct Geom {
 };
 
 enum SweepMode { MODE_FUSED = 0, MODE_PACK = 1, MODE_NOEXCHANGE = 2 };
+// JAC_NO_CTA_SYSFENCE experiment: remote CTAs skip their system fence before the count
+// (UNSAFE: peer data may trail the flag) -- measures that fence's cost, nothing else
+constexpr int32_t kExpNoCtaSysFence = 1;
 
 // Cross-partition ordering state of one partition hosted by a context (one per rank
 // context; one per virtual partition under JAC_F_VIRTUAL_GPUS).  Its control words
@@ -143,7 +146,7 @@ struct SweepArgs {
                              // nremote entries of item_map)
     int32_t slot_base;       // slot of blocks[0] (JAC_F_PER_BLOCK launches one block's table
                              // entry; 0 otherwise: the work list enumerates slots in order)
-    int32_t pad3_;
+    int32_t exp_bits;        // timing experiments only (kExpNoCtaSysFence); 0 in production
     CheckArgs chk;           // checked build only
     // jac_profile_sweep: when set, every CTA atomicMin's %globaltimer into span[0] after
     // the dependency wait and atomicMax's it into span[1] when done (ns); remote CTAs add

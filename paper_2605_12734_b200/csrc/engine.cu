@@ -196,6 +196,7 @@ struct jac_ctx {
     cudaGraphExec_t g1[2] = {nullptr, nullptr}, gU[2] = {nullptr, nullptr};
     int unroll = 10;
     uint64_t exp_mask = 0;  // experiment knobs this context read (JAC_STAT_EXPERIMENT)
+    int32_t exp_bits = 0;   // kernel-side timing experiments (SweepArgs::exp_bits)
 
     bool inited = false;
     int64_t iters = 0;
@@ -249,7 +250,8 @@ uint64_t fingerprint(const jac_ctx *c)
 const char *const kKnobs[] = {"JAC_L2PROMO", "JAC_ZC",     "JAC_ZCHUNK", "JAC_GCOLS",   "JAC_VARIANT",
                               "JAC_AUTOTUNE", "JAC_A",      "JAC_PALIGN", "JAC_NO_DENSE", "JAC_UNROLL",
                               "JAC_PDL",     "JAC_NO_FUSED_SYNC", "JAC_ORDER_EXP", "JAC_DROP_REMOTE",
-                              "JAC_HOLD_SIGNAL", "JAC_REMOTE_SPREAD", "JAC_CHECK_SELFTEST", "JAC_YCHUNK"};
+                              "JAC_HOLD_SIGNAL", "JAC_REMOTE_SPREAD", "JAC_CHECK_SELFTEST", "JAC_YCHUNK",
+                              "JAC_NO_CTA_SYSFENCE"};
 
 const char *knob(jac_ctx *c, const char *name)
 {
@@ -280,6 +282,7 @@ jac::SweepArgs sweep_args(const jac_ctx *c, int src, int mode)
     if (c->prof_span) a.span = c->prof_span + 4 * (int64_t)c->prof_it;
     a.wd = c->wd();
     a.chk = c->chk();
+    a.exp_bits = c->exp_bits;
     if (c->fused && mode == jac::MODE_FUSED) {
         a.fused_sync = 1;
         a.nremote = c->nremote;
@@ -802,6 +805,7 @@ int create_common(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, in
             c->variant = v;
     }
     configure_tiles(c);
+    if (knob(c, "JAC_NO_CTA_SYSFENCE")) c->exp_bits |= jac::kExpNoCtaSysFence;  // UNSAFE timing experiment
     if (const char *s = knob(c, "JAC_UNROLL")) c->unroll = std::max(2, atoi(s) & ~1);
     if (const char *s = knob(c, "JAC_PDL")) c->pdl = atoi(s) != 0;
     if ((int64_t)c->nslots * c->ntx * c->nty * c->ntz > 0x7fffffffLL) {

@@ -377,11 +377,12 @@ __device__ __forceinline__ void timed_wait_peers(const SweepArgs &a, const PartS
 // All threads of a remote-touching item: after the CTA's last store.  The last such
 // CTA of its partition in this launch bumps the partition's epoch and releases it to
 // every neighbour partition.
-__device__ __forceinline__ void signal_done(const PartSync &ps)
+__device__ __forceinline__ void signal_done(const PartSync &ps, int32_t exp_bits = 0)
 {
     __syncthreads();
     if (threadIdx.x != 0) return;
-    __threadfence_system();  // this CTA's stores (peer stores included) before the count
+    if (!(exp_bits & kExpNoCtaSysFence))
+        __threadfence_system();  // this CTA's stores (peer stores included) before the count
     if (atomicAdd(ps.count, 1ull) == (unsigned long long)ps.nremote - 1) {
         *reinterpret_cast<volatile unsigned long long *>(ps.count) = 0;
         __threadfence_system();
@@ -685,7 +686,7 @@ __global__ void __launch_bounds__(NT, min_ctas_per_sm(NT, NS, BX, BY))
         for (; q <= qlean_end; ++q) plane_general(q);
     }
     if (q <= qlast) plane_general(q);  // z+ face plane
-    if (remote) signal_done(a.sync[blk.part]);
+    if (remote) signal_done(a.sync[blk.part], a.exp_bits);
     span_end(a.span);
 }
 
@@ -857,7 +858,7 @@ __global__ void __launch_bounds__(NT, 4) sweep2d_tma_kernel(const __grid_constan
         for (; q < qend; ++q) tile_general(q);
     }
     if (q < nq) tile_general(q);
-    if (remote) signal_done(a.sync[blk.part]);
+    if (remote) signal_done(a.sync[blk.part], a.exp_bits);
     span_end(a.span);
 }
 

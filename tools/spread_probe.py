@@ -19,10 +19,18 @@ import bench  # geometry helpers only
 
 dims, blocks, g, _, _ = bench.workload(os.environ.get("CFG", "c2"), N, ODF)
 settings = os.environ.get("SPREADS", "first,25,50,80").split(",")
+# SETTINGS overrides: ';'-separated env settings 'K=V,K=V' or 'default'
+if os.environ.get("SETTINGS"):
+    settings = os.environ["SETTINGS"].split(";")
 res = {s: [] for s in settings}
 for rep in range(R):
     for sp in settings:
-        env = {"JAC_EXPERIMENT": "1", "JAC_REMOTE_SPREAD": sp} if sp != "first" else {}
+        if "=" in sp:
+            env = {"JAC_EXPERIMENT": "1", **dict(kv.split("=") for kv in sp.split(","))}
+        elif sp in ("first", "default"):
+            env = {"JAC_EXPERIMENT": "1", "JAC_REMOTE_SPREAD": "0"} if sp == "first" else {}
+        else:
+            env = {"JAC_EXPERIMENT": "1", "JAC_REMOTE_SPREAD": sp}
         os.environ.update(env)
         with jb.Jacobi3D(dims, blocks, n_gpus=N, gpu_grid=g) as G:
             for k in env:
@@ -38,7 +46,7 @@ for rep in range(R):
             res[sp].append((ms, sw, st["peer_wait_ns"], st["peer_wait_max_ns"], st["remote_items"]))
 for sp in settings:
     v = res[sp]
-    print(f"N={N} ODF={ODF} remote={sp:6s} ms/iter {statistics.median(x[0] for x in v):.4f} "
+    print(f"N={N} ODF={ODF} {sp:28s} ms/iter {statistics.median(x[0] for x in v):.4f} "
           f"sweep {1e3 * statistics.median(x[1] for x in v):.1f} us  peer-wait sum/sweep "
           f"{statistics.median(x[2] for x in v) / 1e3:.1f} us max {max(x[3] for x in v) / 1e3:.1f} us "
           f"remote_items {v[0][4]}", flush=True)
