@@ -499,10 +499,12 @@ void configure_tiles(jac_ctx *c)
         int gcols = 2 * sms;
         if (const char *s = knob(c, "JAC_GCOLS")) gcols = atoi(s);
         c->gcols = std::max(1, std::min(c->ncols, gcols > 0 ? gcols : c->ncols));
-        if (flags & JAC_F_2D) {  // 2-D: items = (block, x tile, chunk of 4 y tiles), nzc = y chunks
-            // 4 y tiles (64 rows) per item: 1.6-2.3% faster than 8 on every width measured,
-            // 3 / 5 / 6 between, 2 much slower (profiles/r02_j2d_ychunk.txt)
-            int ytiles = 4;
+        if (flags & JAC_F_2D) {  // 2-D: items = (block, x tile, chunk of 8 y tiles), nzc = y chunks
+            // 8 y tiles (128 rows) per item.  4 is 1.6-2.3% faster in the cold regime on
+            // every width measured but 1-2% slower at the power-cap equilibrium (it holds
+            // a 50-150 MHz lower clock), as 8-plane z-chunks are in 3-D
+            // (profiles/r02_j2d_ychunk.txt, r02_zchunk.txt); JAC_YCHUNK overrides.
+            int ytiles = 8;
             if (const char *s = knob(c, "JAC_YCHUNK")) ytiles = std::max(1, atoi(s));
             c->nzc = std::max(1, (c->nty + ytiles - 1) / ytiles);
             c->nitems = c->nslots * c->ntx * c->nzc;
