@@ -111,8 +111,9 @@ def test_c2_full_memcmp_every_odf():
     wv = want.view(np.uint64)
     for odf, blocks in C2_ODF_BLOCKS.items():
         got = _full_run(dims, blocks, N_IT, u0)
-        nbad = int(np.count_nonzero(got.view(np.uint64) != wv))
-        assert nbad == 0, f"ODF {odf} blocks {blocks}: {nbad} mismatches"
+        bad = np.argwhere(got.view(np.uint64) != wv)
+        assert len(bad) == 0, (f"ODF {odf} blocks {blocks}: {len(bad)} mismatches; bounding box (z, y, x) "
+                               f"{bad.min(axis=0).tolist()} .. {bad.max(axis=0).tolist()}")
         del got
 
 
@@ -122,7 +123,9 @@ def test_c3x1_full_memcmp():
     u0 = JI.hash_field(*dims, seed=1)
     want, _ = oracle.jacobi3d_omp(u0, N_IT)
     got = _full_run(dims, (2, 2, 2), N_IT, u0)
-    assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
+    bad = np.argwhere(got.view(np.uint64) != want.view(np.uint64))
+    assert len(bad) == 0, (f"{len(bad)} mismatches; bounding box (z, y, x) {bad.min(axis=0).tolist()} .. "
+                           f"{bad.max(axis=0).tolist()}; first {bad[:3].tolist()}")
 
 
 def test_j2d_strong_paper_grid_multi_gpu():
