@@ -435,10 +435,15 @@ __global__ void __launch_bounds__(NT, min_ctas_per_sm(NT, NS, BX, BY))
     static_assert(RY >= 1 && RY * NRG == BY, "tile shape");
     static_assert(W == BX || W == BX + 4, "staged width");
     static_assert(NS >= 3, "ring must hold planes k, k+1 and prefetch");
+    // A ring of NSL = NS stages with NS - 1 planes in flight: the refill after plane q
+    // overwrites the stage of plane q-1, whose values were all consumed (in registers)
+    // one plane earlier -- see refill below.
+    constexpr int NSL = NS;
+    constexpr int NIF = NS - 1;  // planes in flight
 
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double *stage = reinterpret_cast<double *>(smem_raw);
-    uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + NS * L::STRIDE * sizeof(double));
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + NSL * L::STRIDE * sizeof(double));
 
     const Geom &g = a.g;
     const int code = a.item_map ? a.item_map[blockIdx.x] : (int)blockIdx.x;  // ~item: remote-touching
@@ -465,8 +470,8 @@ __global__ void __launch_bounds__(NT, min_ctas_per_sm(NT, NS, BX, BY))
 
     // plane q of the item = interior plane k = zs - 1 + q; x-ghosts only for k in [zs, ze)
     auto issue = [&](int q) {
-        double *st = stage + (q % NS) * L::STRIDE;
-        uint64_t *bar = &bars[q % NS];
+        double *st = stage + (q % NSL) * L::STRIDE;
+        uint64_t *bar = &bars[q % NSL];
         const bool mid = (q >= 1) && (q <= nq - 2);
         const uint32_t bytes = L::BOX_BYTES + (mid ? ((xlo ? L::XG_BYTES : 0) + (xhi ? L::XG_BYTES : 0)) : 0);
         JAC_ASSERT(a, c0 >= 0 && c0 < g.P && t.y0 >= 0 && t.y0 < g.ey && t.zs + q >= 0 &&
@@ -486,9 +491,9 @@ __global__ void __launch_bounds__(NT, min_ctas_per_sm(NT, NS, BX, BY))
         c3 = a.src * g.nslots + slot;
         xg0 = xg_array(a.xg, g, a.src, slot, 0) + t.y0;
         xg1 = xg_array(a.xg, g, a.src, slot, 1) + t.y0;
-        for (int s = 0; s < NS; ++s) mbar_init(&bars[s], 1);  // producer arrive + TMA bytes
+        for (int s = 0; s < NSL; ++s) mbar_init(&bars[s], 1);  // producer arrive + TMA bytes
         mbar_fence_init();
-        for (int q = 0; q < NS && q < nq; ++q) issue(q);
+        for (int q = 0; q < NIF && q < nq; ++q) issue(q);
     }
     __syncthreads();
 
@@ -504,21 +509,30 @@ __global__ void __launch_bounds__(NT, min_ctas_per_sm(NT, NS, BX, BY))
     const int sb = (jl0 + 1) * W + col;            // stage index of (row 0, element 0)
     const int xg = L::XG_OFF + jl0;                // stage index of row 0's x- ghost (+BY: x+)
     double *const own = a.arena + (int64_t)(dst * g.nslots + blk.slot) * g.bstride;  // (slot here spills at 64 regs)
-    auto plane = [&](int q) { return stage + (q % NS) * L::STRIDE; };
-    auto wait = [&](int q) { mbar_wait(&bars[q % NS], (q / NS) & 1); };
-    // every thread is done with plane q -> the producer refills its stage with q + NS.
-    // (Per-warp "empty" mbarriers instead of this CTA barrier were measured: no robust
-    // gain, and slower for the small-block tiles.)
+    auto plane = [&](int q) { return stage + (q % NSL) * L::STRIDE; };
+    auto wait = [&](int q) { mbar_wait(&bars[q % NSL], (q / NSL) & 1); };
+    // Plane q is done -> the producer issues plane q + NIF into the stage of plane q-1.
+    // A stage may be overwritten only once every value read from it has reached
+    // registers: the barrier orders the threads' shared-memory loads before the refill,
+    // but a load whose result is not yet used can still be in flight when the TMA (async
+    // proxy) overwrites the stage.  Plane q-1's loads were all consumed by the stencil of
+    // plane q-1 or q -- including plane 0's, which only feed zm for plane 1 -- whereas
+    // plane q's own stage may still hold values in flight.  (The first version refilled
+    // plane q's stage, and plane 0's straight after loading zm: a rare write-after-read
+    // race -- a few stale 32-point row segments in one run out of dozens, and in every run
+    // of a build whose scheduling delayed those loads.)  (Per-warp "empty" mbarriers
+    // instead of this CTA barrier were measured: no robust gain, and slower for the
+    // small-block tiles.)
     auto refill = [&](int q) {
         __syncthreads();
-        if (threadIdx.x == 0 && q + NS < nq) issue(q + NS);
+        if (threadIdx.x == 0 && q + NIF < nq) issue(q + NIF);
     };
 
     double2 zm[RY], c[RY], zp[RY];
     wait(0);
 #pragma unroll
     for (int r = 0; r < RY; ++r) zm[r] = *reinterpret_cast<const double2 *>(plane(0) + sb + r * W);
-    refill(0);  // plane zs-1 only feeds zm
+    refill(0);  // plane NIF into the spare stage (plane -1's): plane 0's stage stays intact
     wait(1);
 #pragma unroll
     for (int r = 0; r < RY; ++r) c[r] = *reinterpret_cast<const double2 *>(plane(1) + sb + r * W);
@@ -624,8 +638,8 @@ __global__ void __launch_bounds__(NT, min_ctas_per_sm(NT, NS, BX, BY))
         const bool yv = (ys & 1) == 0;  // y-face rows 16-byte aligned (ghost rows; packed, even ex)
         double *op = own + (int64_t)(t.zs + q) * g.Q + (int64_t)(t.y0 + jl0 + 1) * g.P + g.A + i;
         const int64_t P = g.P, Qs = g.Q;
-        int sn = (q + 1) % NS;               // ring slot of plane q+1
-        uint32_t pn = ((q + 1) / NS) & 1u;   // its mbarrier parity
+        int sn = (q + 1) % NSL;               // ring slot of plane q+1
+        uint32_t pn = ((q + 1) / NSL) & 1u;   // its mbarrier parity
         const double *Sc = plane(q);
         auto step = [&](const bool XE, const double2 (&A)[RY], const double2 (&B)[RY], double2 (&C)[RY]) {
             mbar_wait(&bars[sn], pn);
@@ -660,7 +674,7 @@ __global__ void __launch_bounds__(NT, min_ctas_per_sm(NT, NS, BX, BY))
             refill(q);  // centre plane done
             ++q;
             Sc = Sn;
-            if (++sn == NS) { sn = 0; pn ^= 1u; }
+            if (++sn == NSL) { sn = 0; pn ^= 1u; }
         };
         auto run = [&](const bool xe) {
             while (q + 2 <= qlean_end) {
@@ -1107,7 +1121,7 @@ static int resident_tma_t()
 {
     static int resident = 0;  // SMs x CTAs per SM (per process; one device per process)
     if (!resident) {
-        constexpr size_t smem = tma_smem_bytes(BX, BY, W, NS);
+        constexpr size_t smem = tma_smem_bytes(BX, BY, W, NS);  // NS stages, NS - 1 planes in flight
         // the occupancy query needs the kernel's dynamic shared-memory limit raised
         // first (above 48 KB it would report 0 CTAs per SM)
         cudaFuncSetAttribute(sweep_tma_kernel<BX, BY, W, NT, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -43,14 +43,15 @@ def test_library_is_in_tree_and_built_for_sm100a():
     assert "sm_100a" in out
 
 
-def test_tma_kernels_have_no_stack_frame():
-    """Every TMA sweep instantiation of the production build runs without a stack
-    frame (STACK:0).  Measured on B200: a non-inlined peer-wait call inside the 3-D sweep
-    (STACK:240: the kernel-parameter struct copied to local memory for the by-reference
-    argument) gave sporadic stale 32-point row segments at 512^3, while the same code
-    inlined was bit-exact.  The bounds-checked build, whose frames come from spills and
-    its check calls, is bit-exact at 512^3 too, so the trigger is narrower than "any
-    frame"; the guard stays as the conservative rule for the production kernels."""
+def test_tma_kernels_have_no_large_stack_frame():
+    """No TMA sweep instantiation of the production build carries more than a spilled
+    register or two of stack (performance hygiene: the z-march keeps its state in
+    registers).  History: a build whose peer-wait call copied the 240-byte kernel
+    parameters to a stack frame showed stale 32-point row segments at 512^3.  The cause
+    was not the frame but a write-after-read race it exposed -- plane 0's stage was
+    refilled while the loads feeding the first plane's z- neighbour could still be in
+    flight; the same frame-carrying build is bit-exact once refills overwrite the
+    previous plane's stage (profiles/r02_ring_war_race.txt)."""
     import subprocess
     out = subprocess.run(["cuobjdump", "-res-usage", J.lib_path()], capture_output=True, text=True).stdout
     lines = out.splitlines()
@@ -58,7 +59,8 @@ def test_tma_kernels_have_no_stack_frame():
     for i, ln in enumerate(lines):
         if "Function" in ln and ("sweep_tma_kernel" in ln or "sweep2d_tma_kernel" in ln):
             seen += 1
-            assert "STACK:0 " in lines[i + 1], (ln, lines[i + 1])
+            stack = int(re.search(r"STACK:(\d+)", lines[i + 1]).group(1))
+            assert stack <= 16, (ln, lines[i + 1])
     assert seen >= 16
 
 

@@ -274,3 +274,22 @@ def test_get_block_every_block(monkeypatch, dense, dims, blocks):
             J.jac_get_block(s.ctx, 0, 0, 0, np.empty((ez, ey, ex + 1)))
         with pytest.raises(ValueError):
             J.jac_get_block(s.ctx, 0, 0, 0, np.empty((ez, ey, ex), dtype=np.float32))
+
+
+@pytest.mark.parametrize("blocks", [(1, 1, 1), (2, 2, 2), (16, 16, 16)])
+def test_ring_refill_race_regression(blocks):
+    """Regression guard for the staging ring's write-after-read race:
+    the first sweeps after init at 512^3, repeated, compared in full with the oracle.
+    The racy ring showed stale 32-point row segments at n = 1 in most runs of a build
+    whose scheduling delayed the first plane's loads (profiles/r02_ring_war_race.txt)."""
+    nx = 512
+    u0 = JI.hash_field(nx, nx, nx, seed=1)
+    for n in (1, 2):
+        want = ref(u0, n).view(np.uint64)
+        for _ in range(2):
+            with jb.Jacobi3D((nx, nx, nx), blocks) as s:
+                s.set_init_hash(1)
+                s.step(n)
+                got = s.field(u0)
+            bad = np.argwhere(got.view(np.uint64) != want)
+            assert len(bad) == 0, f"n={n} blocks {blocks}: {len(bad)} stale values, first {bad[:3].tolist()}"
