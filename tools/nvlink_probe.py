@@ -17,9 +17,11 @@ from paper_2605_12734_b200 import jacobi3d as J
 N = int(os.environ.get("N", "2"))
 box = int(os.environ.get("BOX", "512"))
 g = {2: (1, 1, 2), 4: (1, 2, 2), 8: (2, 2, 2)}[N]
+if os.environ.get("GRID"):  # e.g. GRID=2x1x1: an x split (remote x faces: the x-ghost arrays)
+    g = tuple(int(v) for v in os.environ["GRID"].split("x"))
 dims = tuple(box * g[d] for d in range(3))
 blocks = tuple(2 * g[d] for d in range(3))
-with jb.Jacobi3D(dims, blocks, n_gpus=N, flags=J.JAC_F_NO_GRAPH) as G:
+with jb.Jacobi3D(dims, blocks, n_gpus=N, gpu_grid=g, flags=J.JAC_F_NO_GRAPH) as G:
     G.set_init_hash(1)
     G.step(int(os.environ.get("K", "6")))
     st = G.stats()
