@@ -636,6 +636,7 @@ __global__ void __launch_bounds__(NT, min_ctas_per_sm(NT, NS, BX, BY))
             }
         }
         const bool yv = (ys & 1) == 0;  // y-face rows 16-byte aligned (ghost rows; packed, even ex)
+        const bool xv2 = (xs & 1) == 0;  // x-face row pairs 16-byte aligned (pitch eyp; outbox: even ey)
         double *op = own + (int64_t)(t.zs + q) * g.Q + (int64_t)(t.y0 + jl0 + 1) * g.P + g.A + i;
         const int64_t P = g.P, Qs = g.Q;
         int sn = (q + 1) % NSL;               // ring slot of plane q+1
@@ -647,6 +648,7 @@ __global__ void __launch_bounds__(NT, min_ctas_per_sm(NT, NS, BX, BY))
             const double *Sb = Sc + sb;
 #pragma unroll
             for (int r = 0; r < RY; ++r) C[r] = *reinterpret_cast<const double2 *>(Sn + sb + r * W);
+            double xprev = 0.0;  // x-face value of the previous row (pairs of rows: one store)
 #pragma unroll
             for (int r = 0; r < RY; ++r) {
                 double xm = Sb[r * W - 1], xp1 = Sb[r * W + 2];
@@ -660,7 +662,18 @@ __global__ void __launch_bounds__(NT, min_ctas_per_sm(NT, NS, BX, BY))
                 v.x = stencil7(B[r].x, xm, B[r].y, ym.x, yp.x, A[r].x, C[r].x);
                 v.y = stencil7(B[r].y, B[r].x, xp1, ym.y, yp.y, A[r].y, C[r].y);
                 ST16(a, op + r * P, v);
-                if (XE && xf) ST8(a, xf + r, ilo ? v.x : v.y);
+                // x face: rows r-1 and r of this lane are adjacent in the neighbour's x-ghost
+                // array, so an even row count stores them as one 16-byte pair (half the
+                // transactions; over NVLink a lone 8-byte store travels as its own transfer)
+                if (XE && xf) {
+                    const double xv = ilo ? v.x : v.y;
+                    if (RY % 2 == 0 && xv2) {
+                        if (r & 1) ST16(a, xf + r - 1, make_double2(xprev, xv));
+                        else xprev = xv;
+                    } else {
+                        ST8(a, xf + r, xv);
+                    }
+                }
                 if (XE && yf && ((r == 0 && yf_lo) || (r == RY - 1 && !yf_lo))) {
                     // one 16-byte store (NVLink sends a half-written 32-byte sector as its own
                     // transfer); packed rows of odd width ex are only 8-byte aligned
@@ -845,6 +858,7 @@ __global__ void __launch_bounds__(NT, 4) sweep2d_tma_kernel(const __grid_constan
                 double2 rw[RY + 2];  // rows jl0-1 .. jl0+RY
 #pragma unroll
                 for (int r = 0; r < RY + 2; ++r) rw[r] = *reinterpret_cast<const double2 *>(Sb + (r - 1) * W);
+                double xprev = 0.0;  // x-face value of the previous row (see the 3-D sweep)
 #pragma unroll
                 for (int r = 0; r < RY; ++r) {
                     double xm = Sb[r * W - 1], xp1 = Sb[r * W + 2];
@@ -857,7 +871,15 @@ __global__ void __launch_bounds__(NT, 4) sweep2d_tma_kernel(const __grid_constan
                     v.x = stencil5(c.x, xm, c.y, rw[r].x, rw[r + 2].x);
                     v.y = stencil5(c.y, c.x, xp1, rw[r].y, rw[r + 2].y);
                     ST16(a, op + r * P, v);
-                    if (XE && xfp) ST8(a, xfp + r, ilo ? v.x : v.y);
+                    if (XE && xfp) {  // row pairs: one 16-byte store (the x-ghost pitch eyp is even)
+                        const double xv = ilo ? v.x : v.y;
+                        if (RY % 2 == 0) {
+                            if (r & 1) ST16(a, xfp + r - 1, make_double2(xprev, xv));
+                            else xprev = xv;
+                        } else {
+                            ST8(a, xfp + r, xv);
+                        }
+                    }
                 }
                 op += TP;
                 if (XE && xfp) xfp += BY;
