@@ -8,7 +8,7 @@ Prints the library's remote bytes per GPU and iteration for comparison."""
 import os
 import sys
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.environ.get("PROBE_ROOT") or os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 os.environ.setdefault("JAC_EXPERIMENT", "1")
 os.environ.setdefault("JAC_AUTOTUNE", "0")  # no create-time timing sweeps in the launch list
 import paper_2605_12734_b200 as jb
