@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges cost nothing without a tool attached
 
 #include <algorithm>
 #include <climits>
@@ -37,6 +38,13 @@
 namespace {
 
 thread_local std::string g_err;
+
+// NVTX range over one C-ABI call (jac_step, init, profile, create), for timelines
+// taken with a tracing tool (nsys is not in this image; the ranges are inert without one)
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
 
 int fail(int code, const char *fmt, ...)
 {
@@ -1428,6 +1436,7 @@ int jac_plan_face(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, in
 int jac_create(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, int32_t bz, int32_t n_gpus,
                const int32_t *gpu_grid, uint32_t flags, jac_ctx **out)
 {
+    NvtxRange range("jac_create");
     try {
         if (n_gpus > 1 && !(flags & JAC_F_VIRTUAL_GPUS))
             return create_group(nx, ny, nz, bx, by, bz, n_gpus, gpu_grid, flags, out);
@@ -1592,6 +1601,7 @@ int region_copy(jac_ctx *c, const int64_t *lo, const int64_t *ext, double *out, 
 
 int jac_set_init_box(jac_ctx *c, const double *box, const int64_t *origin, const int64_t *extent)
 {
+    NvtxRange range("jac_set_init_box");
     int rc;
     if ((rc = require_ready(c))) return rc;
     if ((rc = check_box(c, box, origin, extent))) return rc;
@@ -1663,6 +1673,7 @@ int jac_set_init(jac_ctx *c, const double *padded)
 
 int jac_set_init_hash(jac_ctx *c, uint64_t seed)
 {
+    NvtxRange range("jac_set_init_hash");
     int rc;
     if ((rc = require_ready(c))) return rc;
     if (c->group) {
@@ -1682,6 +1693,7 @@ int jac_set_init_hash(jac_ctx *c, uint64_t seed)
 
 int jac_step(jac_ctx *c, int32_t n)
 {
+    NvtxRange range("jac_step");
     int rc;
     if (c && c->group) return group_step(c, n);
     if ((rc = step_check(c, n))) return rc;
@@ -1701,6 +1713,7 @@ int jac_step(jac_ctx *c, int32_t n)
 
 int jac_profile_sweep(jac_ctx *c, int32_t n, double *avg_ms)
 {
+    NvtxRange range("jac_profile_sweep");
     int rc;
     if ((rc = require_ready(c))) return rc;
     if (n < 1 || !avg_ms) return fail(JAC_EINVAL, "n_iters must be >= 1 and avg_sweep_ms non-NULL");
