@@ -1209,7 +1209,7 @@ static cudaError_t launch_tma_t(const CUtensorMap &tm, const SweepArgs &a, cudaS
     X(TMA_WIDE, 64, 16, 68, 256, 6)       \
     X(TMA_WIDE4, 64, 16, 68, 256, 4)      \
     X(TMA_NARROW, 32, 16, 36, 256, 4)     \
-    X(TMA_EXACT32, 32, 16, 32, 256, 4)    \
+    X(TMA_EXACT32, 32, 16, 32, 256, 5)    \
     X(TMA_EXACT64, 64, 16, 64, 256, 4)    \
     X(TMA_EXACT32_TALL, 32, 32, 32, 256, 4) \
     X(TMA_EXACT32_6, 32, 16, 32, 256, 6)    \
