@@ -113,3 +113,24 @@ def test_profile_gap(lib, ctx):
     assert lib.jac_profile_sweep(ctx, 12, ctypes.byref(d)) == J.JAC_OK
     assert lib.jac_last_profile_gap_ms(ctx, ctypes.byref(g)) == J.JAC_OK
     assert 0.0 <= g.value < 0.05, g.value
+
+
+def test_options_grid_and_stats(lib, ctx):
+    """jac_set_option validates the watchdog limit; jac_get_grid returns the creation
+    arguments; a single-GPU context reports one partition, no remote work and no
+    experiment knobs (the production state)."""
+    _expect(lib, lib.jac_set_option(ctx, J.JAC_OPT_WATCHDOG_MS, -5), J.JAC_EINVAL, "WATCHDOG")
+    assert lib.jac_set_option(ctx, J.JAC_OPT_WATCHDOG_MS, 0) == J.JAC_OK
+    _expect(lib, lib.jac_set_option(ctx, J.JAC_OPT_LAUNCH_THREADS, 0), J.JAC_EINVAL)
+    n = (i64 * 3)()
+    b = (i32 * 3)()
+    f = ctypes.c_uint32()
+    assert lib.jac_get_grid(ctx, n, b, ctypes.byref(f)) == J.JAC_OK
+    assert tuple(n) == (48, 40, 32) and tuple(b) == (2, 2, 2) and f.value == 0
+    assert lib.jac_get_grid(ctx, None, None, None) == J.JAC_OK
+    _expect(lib, lib.jac_get_grid(None, n, b, None), J.JAC_EINVAL)
+    st = J.jac_get_stats(ctx.value)
+    assert st["partitions"] == 1 and st["remote_faces"] == 0 and st["fused_sync"] == 0
+    assert st["experiment"] == 0 and st["epoch_min"] == st["epoch_max"] == 0
+    assert lib.jac_set_init_hash(ctx, 2) == J.JAC_OK
+    assert lib.jac_step(ctx, 3) == J.JAC_OK  # with the watchdog off (0 = wait forever)
