@@ -153,6 +153,7 @@ struct jac_ctx {
     // connected by plain peer pointers; every call fans out to them
     bool group = false;
     std::vector<jac_ctx *> subs;
+    bool in_group = false;  // a group's sub-context
 
     jac::Geom geom{};
     char *alloc = nullptr;    // single allocation: [ctrl][arena][x ghosts][outbox]
@@ -1161,6 +1162,14 @@ int step_begin(jac_ctx *c)
             if ((rc = build_graph(c, s, c->unroll, &c->gU[s]))) return rc;
         }
     }
+    // One process per GPU: the ranks enter jac_step at slightly different host times
+    // (tens to hundreds of microseconds after a host barrier).  A device-side neighbour
+    // barrier first aligns the GPUs, so the step's device time (CUDA events, max over
+    // ranks) measures the iterations, not the launch skew -- which the early ranks'
+    // first sweeps would otherwise absorb waiting for the late ones' signals.  (A
+    // single-process group launches every device from one thread: no skew to absorb.)
+    if (c->rank_mode && !c->in_group && c->has_remote() && !(c->flags & JAC_F_NCCL))
+        if ((rc = enqueue_barrier(c))) return rc;
     CK(cudaEventRecord(c->ev0, c->stream));
     return JAC_OK;
 }
@@ -1315,6 +1324,7 @@ int create_group(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, int
     for (int32_t g = 0; g < n_gpus; ++g) {
         jac_ctx *sub = nullptr;
         if ((rc = create_common(nx, ny, nz, bx, by, bz, n_gpus, gpu_grid, true, g, g, flags, &sub))) return bail(rc);
+        sub->in_group = true;
         G->subs.push_back(sub);
         G->parts.push_back(g);
     }
