@@ -1162,13 +1162,15 @@ int step_begin(jac_ctx *c)
             if ((rc = build_graph(c, s, c->unroll, &c->gU[s]))) return rc;
         }
     }
-    // One process per GPU: the ranks enter jac_step at slightly different host times
-    // (tens to hundreds of microseconds after a host barrier).  A device-side neighbour
-    // barrier first aligns the GPUs, so the step's device time (CUDA events, max over
-    // ranks) measures the iterations, not the launch skew -- which the early ranks'
-    // first sweeps would otherwise absorb waiting for the late ones' signals.  (A
-    // single-process group launches every device from one thread: no skew to absorb.)
-    if (c->rank_mode && !c->in_group && c->has_remote() && !(c->flags & JAC_F_NCCL))
+    // Multi-GPU: the devices start a step at different times -- one process per GPU
+    // enters jac_step tens to hundreds of microseconds apart after a host barrier, and a
+    // single-process group launches its devices one after the other.  A device-side
+    // neighbour barrier first aligns the GPUs, so the step's device time (CUDA events,
+    // max over devices / ranks) measures the iterations, not the launch skew, which the
+    // early devices' first sweeps would otherwise absorb waiting for the late ones'
+    // signals (torchrun, C2 at N = 4: rank times 0.339-0.350 ms/iter before, 0.3384-0.3392
+    // after; profiles/r02_scaling_same_lease.json).
+    if (c->rank_mode && c->has_remote() && !(c->flags & JAC_F_NCCL))
         if ((rc = enqueue_barrier(c))) return rc;
     CK(cudaEventRecord(c->ev0, c->stream));
     return JAC_OK;

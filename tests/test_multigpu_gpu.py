@@ -111,8 +111,8 @@ def test_single_process_multi_gpu_parity(case):
     ex, ey, ez = (dims[d] // blocks[d] for d in range(3))
     assert np.array_equal(blk, want[-ez - 1:-1, -ey - 1:-1, -ex - 1:-1])
     assert st["partitions"] == n and st["remote_faces"] > 0
-    if flags == 0:
-        assert st["fused_sync"] == 1 and st["epoch_min"] == st["epoch_max"] == 2 + iters
+    if flags == 0:  # init: 2 barriers; each jac_step: 1 aligning barrier + 1 signal per sweep
+        assert st["fused_sync"] == 1 and st["epoch_min"] == st["epoch_max"] == 2 + 3 + iters
 
 
 def test_single_process_multi_gpu_2d():
