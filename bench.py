@@ -674,6 +674,10 @@ def finish_ours(args, D, K, W, dims, blocks, g, label, scaling, pts, pts_gpu, pe
                                       "sustained_power_capped = the same context after ~1.5 s at the 1000 W cap"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "traffic_source": ("dram__bytes_read.sum + dram__bytes_write.sum of one ncu --set full capture "
+                                            "of this decomposition's sweep (profiles/traffic.json; captures "
+                                            "profiles/r02_ncu_sweep_*.json); null when none was taken")
+                         if traffic is not None else None,
                          "kernel": "sweep2d_tma_kernel" if MODE_2D[0] else "sweep_tma_kernel",
                          "algorithmic_bytes_per_launch": BYTES_PER_LUP * pts_gpu,
                          "avg_launch_us": 1e3 * sweep_ms,
