@@ -23,6 +23,7 @@
 #include <condition_variable>
 #include <mutex>
 #include <thread>
+#include <tuple>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -260,7 +261,7 @@ const char *const kKnobs[] = {"JAC_L2PROMO", "JAC_ZC",     "JAC_ZCHUNK", "JAC_GC
                               "JAC_AUTOTUNE", "JAC_A",      "JAC_PALIGN", "JAC_NO_DENSE", "JAC_UNROLL",
                               "JAC_PDL",     "JAC_NO_FUSED_SYNC", "JAC_ORDER_EXP", "JAC_DROP_REMOTE",
                               "JAC_HOLD_SIGNAL", "JAC_REMOTE_SPREAD", "JAC_CHECK_SELFTEST", "JAC_YCHUNK",
-                              "JAC_NO_CTA_SYSFENCE"};
+                              "JAC_NO_CTA_SYSFENCE", "JAC_REMOTE_COLMAJOR"};
 
 const char *knob(jac_ctx *c, const char *name)
 {
@@ -673,6 +674,19 @@ int build_item_map(jac_ctx *c)
             c->nremote = nfirst;
             // remote-touching items are marked in the map (~item): they wait before their
             // first staging copy and signal after their last store
+            // experiment: remote items column-major (all z-chunks of a column back to back,
+            // so consecutive chunks share their overlap planes in L2) instead of the natural
+            // chunk-major order
+            if (knob(c, "JAC_REMOTE_COLMAJOR") && !(c->flags & JAC_F_2D)) {
+                const jac::SweepArgs a0 = sweep_args(c, 0, jac::MODE_NOEXCHANGE);
+                const jac::TileShape ts = jac::tma_tile_shape(c->variant);
+                auto colkey = [&](int32_t it) {
+                    const jac::TileItem t = jac::decode_item3d(a0, it, ts.bx, ts.by);
+                    return std::make_tuple(t.b, t.y0, t.x0, t.zs);
+                };
+                std::stable_sort(order.begin(), order.begin() + nfirst,
+                                 [&](int32_t x, int32_t y) { return colkey(x) < colkey(y); });
+            }
             for (int32_t i = 0; i < nfirst; ++i) order[i] = ~order[i];
             // The remote items are spread evenly over the first quarter of the launch order
             // rather than all launched first: their signal still leaves early (the next
