@@ -1166,7 +1166,8 @@ int step_check(jac_ctx *c, int32_t n)
 
 bool use_graphs(const jac_ctx *c) { return !(c->flags & (JAC_F_NO_GRAPH | JAC_F_PER_BLOCK)); }
 
-int step_begin(jac_ctx *c)
+// The slow, once-only part of a step's start: the deferred autotune and the graphs.
+int step_prepare(jac_ctx *c)
 {
     int rc;
     if ((rc = autotune(c))) return rc;
@@ -1176,6 +1177,13 @@ int step_begin(jac_ctx *c)
             if ((rc = build_graph(c, s, c->unroll, &c->gU[s]))) return rc;
         }
     }
+    return JAC_OK;
+}
+
+int step_begin(jac_ctx *c)
+{
+    int rc;
+    if ((rc = step_prepare(c))) return rc;
     // Multi-GPU: the devices start a step at different times -- one process per GPU
     // enters jac_step tens to hundreds of microseconds apart after a host barrier, and a
     // single-process group launches its devices one after the other.  A device-side
@@ -1390,11 +1398,22 @@ int group_step(jac_ctx *G, int32_t n)
     DeviceGuard guard;
     for (jac_ctx *c : G->subs)
         if ((rc = step_check(c, n))) return rc;
+    for (jac_ctx *c : G->subs) {  // autotune / graphs first, so the starts below are quick
+        CK(cudaSetDevice(c->device));
+        if ((rc = step_prepare(c))) return rc;
+    }
+    // Per device: the aligning barrier, the start event and the first chunk back to back,
+    // so each device's first iterations are already queued when its barrier completes
+    // (the barrier releases every device once the last one has started its own).
+    int32_t left = n;
+    const int32_t k0 = n > 0 ? step_chunk(G->subs[0], n) : 0;
     for (jac_ctx *c : G->subs) {
         CK(cudaSetDevice(c->device));
         if ((rc = step_begin(c))) return rc;
+        if (k0 && (rc = step_launch(c, k0))) return rc;
     }
-    for (int32_t left = n; left > 0;) {  // interleaved: every device's chunk queued in turn
+    left -= k0;
+    while (left > 0) {  // interleaved: every device's chunk queued in turn
         const int32_t k = step_chunk(G->subs[0], left);
         for (jac_ctx *c : G->subs) {
             CK(cudaSetDevice(c->device));
