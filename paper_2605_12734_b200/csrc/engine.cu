@@ -1192,8 +1192,14 @@ int step_begin(jac_ctx *c)
     // early devices' first sweeps would otherwise absorb waiting for the late ones'
     // signals (torchrun, C2 at N = 4: rank times 0.339-0.350 ms/iter before, 0.3384-0.3392
     // after; profiles/r02_scaling_same_lease.json).
-    if (c->rank_mode && c->has_remote() && !(c->flags & JAC_F_NCCL))
-        if ((rc = enqueue_barrier(c))) return rc;
+    // The barrier is a neighbour barrier, so one round aligns only neighbours; after as
+    // many rounds as the partition grid's diameter every partition has (transitively)
+    // waited for every other (a 1x2x2 grid: 2 rounds; 2x2x2: 3).
+    if (c->rank_mode && c->has_remote() && !(c->flags & JAC_F_NCCL)) {
+        const int rounds = (c->plan.g[0] - 1) + (c->plan.g[1] - 1) + (c->plan.g[2] - 1);
+        for (int r = 0; r < rounds; ++r)
+            if ((rc = enqueue_barrier(c))) return rc;
+    }
     CK(cudaEventRecord(c->ev0, c->stream));
     return JAC_OK;
 }

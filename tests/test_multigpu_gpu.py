@@ -105,14 +105,18 @@ def test_single_process_multi_gpu_parity(case):
             s.step(k)
         got = s.field(u0)
         st = s.stats()
+        s_grid = s.gpu_grid
         blk = s.block(blocks[0] - 1, blocks[1] - 1, blocks[2] - 1)  # owned by the last device
     want = oracle.jacobi3d_omp(u0, iters)[0]
     assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
     ex, ey, ez = (dims[d] // blocks[d] for d in range(3))
     assert np.array_equal(blk, want[-ez - 1:-1, -ey - 1:-1, -ex - 1:-1])
     assert st["partitions"] == n and st["remote_faces"] > 0
-    if flags == 0:  # init: 2 barriers; each jac_step: 1 aligning barrier + 1 signal per sweep
-        assert st["fused_sync"] == 1 and st["epoch_min"] == st["epoch_max"] == 2 + 3 + iters
+    if flags == 0:  # init: 2 barriers; each of the 3 jac_step calls: `diameter` aligning
+        # barrier rounds; 1 signal per sweep
+        g = s_grid
+        diameter = (g[0] - 1) + (g[1] - 1) + (g[2] - 1)
+        assert st["fused_sync"] == 1 and st["epoch_min"] == st["epoch_max"] == 2 + 3 * diameter + iters
 
 
 def test_single_process_multi_gpu_2d():
