@@ -181,3 +181,35 @@ def test_single_process_multi_gpu_api_surface():
     with pytest.raises(J.JacError) as ei:
         jb.Jacobi3D(dims, blocks, n_gpus=2, flags=J.JAC_F_NCCL)
     assert ei.value.code == J.JAC_EINVAL
+
+
+def test_single_process_multi_gpu_watchdog(monkeypatch):
+    """Real GPUs, one process: partitions that never signal make their neighbours'
+    waits give up after the watchdog limit; jac_step reports it (JAC_ECUDA "peer
+    watchdog") instead of hanging, and the devices stay usable."""
+    import numpy as np
+
+    sys.path.insert(0, ROOT)
+    import jac_inputs as JI
+    import oracle
+    import paper_2605_12734_b200 as jb
+    from paper_2605_12734_b200 import jacobi3d as J
+
+    if _ngpu() < 2:
+        pytest.skip("needs 2 GPUs")
+    dims, blocks = (64, 48, 80), (2, 2, 4)
+    u0 = JI.hash_field(*dims, seed=1)
+    monkeypatch.setenv("JAC_EXPERIMENT", "1")
+    monkeypatch.setenv("JAC_HOLD_SIGNAL", "1")
+    with jb.Jacobi3D(dims, blocks, n_gpus=2) as s:
+        s.set_option(J.JAC_OPT_WATCHDOG_MS, 300)
+        s.set_init(u0)
+        with pytest.raises(J.JacError) as ei:
+            s.step(4)
+        assert ei.value.code == J.JAC_ECUDA and "watchdog" in str(ei.value)
+    monkeypatch.delenv("JAC_HOLD_SIGNAL")
+    monkeypatch.delenv("JAC_EXPERIMENT")
+    with jb.Jacobi3D(dims, blocks, n_gpus=2) as s:
+        s.set_init(u0)
+        s.step(4)
+        assert np.array_equal(s.field(u0).view(np.uint64), oracle.jacobi3d_omp(u0, 4)[0].view(np.uint64))
