@@ -1001,8 +1001,8 @@ int create_common(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, in
         ps.count = reinterpret_cast<unsigned long long *>(ps.ctrl + 1 + n_gpus);
         ps.npeers = (int32_t)c->part_peers[h].size();
         ps.nremote = c->nremote_part[h];
-        // watchdog experiment (tests): partition 0 never signals its sweeps
-        if (h == 0 && knob(c, "JAC_HOLD_SIGNAL")) ps.nremote = 0x7fffffff;
+        // watchdog experiment (tests): partition 0 (the global id) never signals its sweeps
+        if (c->parts[h] == 0 && knob(c, "JAC_HOLD_SIGNAL")) ps.nremote = 0x7fffffff;
         for (int n = 0; n < ps.npeers; ++n) {
             const int32_t q = c->part_peers[h][n];
             ps.peer_id[n] = q;
