@@ -257,6 +257,15 @@ __device__ __forceinline__ uint64_t globaltimer_ns()
 __device__ __forceinline__ bool mbar_try(uint32_t b, uint32_t parity)
 {
     uint32_t done;
+#ifdef JAC_MBAR_HINT  // experiment build: an explicit suspend-time hint (ns) for the wait
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(b), "r"(parity), "n"(JAC_MBAR_HINT)
+        : "memory");
+#else
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
@@ -264,6 +273,7 @@ __device__ __forceinline__ bool mbar_try(uint32_t b, uint32_t parity)
         : "=r"(done)
         : "r"(b), "r"(parity)
         : "memory");
+#endif
     return done != 0;
 }
 

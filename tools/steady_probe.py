@@ -3,7 +3,7 @@ For each (ODF, variant): hash init, `settle` iterations to reach the power/clock
 equilibrium, then reps of `n` iterations with avg power (NVML energy) and SM clock."""
 import os, sys, threading, time
 os.environ.setdefault("JAC_EXPERIMENT", "1")  # the library reads experiment knobs only with this set
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.environ.get("PROBE_ROOT") or os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import pynvml as N
 
