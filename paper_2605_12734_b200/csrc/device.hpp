@@ -131,7 +131,8 @@ struct SweepArgs {
     // TMA kernel work list.  column = (b*nty + ty)*ntx + tx; columns are cut into
     // groups of gcols (about the number of resident CTAs), and items run group by
     // group, z-chunk-major inside a group: item = g*gcols*nzc + zi*gsize + (col - g*gcols).
-    // z-chunk zi of a column covers planes [zi*ez/nzc, (zi+1)*ez/nzc).
+    // z-chunk zi of a column covers planes [zi*ez/nzc, (zi+1)*ez/nzc).  2-D: gcols =
+    // x tiles per band (decode_item2d).
     int32_t nzc, ncols, nitems, gcols;
     // Fused cross-partition ordering (contexts with remote faces, fused mode).  Only
     // the items that touch a remote face share memory with a neighbour partition: they
@@ -188,15 +189,23 @@ JAC_HD inline TileItem decode_item3d(const SweepArgs &a, int item, int BX, int B
 }
 
 // item -> (block, x tile, chunk of y tiles) for the 2-D sweep; nzc = y chunks per block.
-// (x tile fastest.  Grouping the x tiles into column groups like the 3-D list, with the
-// y chunks of a group chunk-major, was measured 1-4% slower on 32768^2 and 131072-wide
-// blocks: profiles/r02_j2d_column_groups.txt.)
+// The x tiles of a block are cut into bands of gcols tiles; items run band by band,
+// x tile fastest inside a band (y-chunk-major).  A band narrower than the block keeps the
+// rows a chunk shares with the next chunk of the same band in L2 on very wide blocks.
+// (Narrow column groups of 296 tiles, chunk-major, were measured 1-4% slower:
+// profiles/r02_j2d_column_groups.txt.)
 JAC_HD inline TileItem decode_item2d(const SweepArgs &a, int item, int BX, int BY)
 {
     TileItem t;
-    const int tx = item % a.ntx; item /= a.ntx;
-    const int yc = item % a.nzc;
-    t.b = item / a.nzc;
+    const int per_b = a.ntx * a.nzc;
+    t.b = item / per_b;
+    const int w = item - t.b * per_b;
+    const int band = w / (a.gcols * a.nzc);
+    const int r = w - band * a.gcols * a.nzc;
+    const int rest = a.ntx - band * a.gcols;
+    const int bw = a.gcols < rest ? a.gcols : rest;
+    const int yc = r / bw;
+    const int tx = band * a.gcols + (r - yc * bw);
     const int tpc = (a.nty + a.nzc - 1) / a.nzc;
     t.x0 = tx * BX;
     t.zs = yc * tpc;

@@ -261,7 +261,7 @@ const char *const kKnobs[] = {"JAC_L2PROMO", "JAC_ZC",     "JAC_ZCHUNK", "JAC_GC
                               "JAC_AUTOTUNE", "JAC_A",      "JAC_PALIGN", "JAC_NO_DENSE", "JAC_UNROLL",
                               "JAC_PDL",     "JAC_NO_FUSED_SYNC", "JAC_ORDER_EXP", "JAC_DROP_REMOTE",
                               "JAC_HOLD_SIGNAL", "JAC_REMOTE_SPREAD", "JAC_CHECK_SELFTEST", "JAC_YCHUNK",
-                              "JAC_NO_CTA_SYSFENCE", "JAC_REMOTE_COLMAJOR"};
+                              "JAC_NO_CTA_SYSFENCE", "JAC_REMOTE_COLMAJOR", "JAC_XBAND"};
 
 const char *knob(jac_ctx *c, const char *name)
 {
@@ -461,6 +461,9 @@ double *block_ptr_local(const jac_ctx *c, const int32_t nb[3], int buf, int f)
 
 // Tile / work-list geometry for the current c->variant (ntx, nty, z-chunks, item
 // count, column groups).  Called at create and for every autotune candidate.
+// 2-D x band width in x tiles (64 points each): 512 tiles = 32768 points.
+constexpr int kXBandTiles = 512;
+
 void configure_tiles(jac_ctx *c)
 {
     const jac::Geom &g = c->geom;
@@ -518,6 +521,12 @@ void configure_tiles(jac_ctx *c)
             if (const char *s = knob(c, "JAC_YCHUNK")) ytiles = std::max(1, atoi(s));
             c->nzc = std::max(1, (c->nty + ytiles - 1) / ytiles);
             c->nitems = c->nslots * c->ntx * c->nzc;
+            // x bands of <= XBAND_TILES x tiles (decode_item2d).
+            int band = kXBandTiles;
+            if (const char *s = knob(c, "JAC_XBAND")) band = atoi(s);
+            if (band <= 0 || band >= c->ntx) band = c->ntx;
+            const int nb = (c->ntx + band - 1) / band;
+            c->gcols = (c->ntx + nb - 1) / nb;  // equal bands
         }
     }
 }
@@ -1057,6 +1066,7 @@ int enqueue_per_block(jac_ctx *c, int64_t t, int first, int stride)
             CK(jac::launch_sweep_plain_one(a, s));
         } else if (c->flags & JAC_F_2D) {
             a.nitems = c->ntx * c->nzc;  // (x tile, y chunk) items of this block
+            a.gcols = c->gcols;          // x band
             CK(jac::launch_sweep2d_tma(c->tmap, a, c->variant, s));
         } else {
             CK(jac::launch_sweep_tma(c->tmap, a, c->variant, s));

@@ -76,3 +76,18 @@ def test_2d_paper_style_per_block_mode(threads, dims, blocks):
         s.step(4)
         s.step(5)
         bits(s.field(u0), ref(u0, 9))
+
+
+@pytest.mark.parametrize("band", ["1", "3", "5"])
+def test_2d_x_bands(monkeypatch, band):
+    """The 2-D work list in x bands (decode_item2d; default 512 tiles, so only blocks
+    wider than 32768 points use more than one): forced narrow bands, including a ragged
+    last band, keep every item exactly once -- plain, in blocks, and with virtual
+    partitions (remote items spread by the item map)."""
+    monkeypatch.setenv("JAC_EXPERIMENT", "1")
+    monkeypatch.setenv("JAC_XBAND", band)
+    u0 = JI.hash_field2d(1000, 300, seed=4)  # 16 x tiles of 64 (ragged last tile)
+    want = ref(u0, 7)
+    bits(run(u0, (1, 1), 7), want)
+    bits(run(u0, (2, 3), 7), want)
+    bits(run(u0, (2, 2), 7, n_gpus=4, flags=J.JAC_F_VIRTUAL_GPUS), want)
