@@ -190,10 +190,9 @@ JAC_HD inline TileItem decode_item3d(const SweepArgs &a, int item, int BX, int B
 
 // item -> (block, x tile, chunk of y tiles) for the 2-D sweep; nzc = y chunks per block.
 // The x tiles of a block are cut into bands of gcols tiles; items run band by band,
-// x tile fastest inside a band (y-chunk-major).  A band narrower than the block keeps the
-// rows a chunk shares with the next chunk of the same band in L2 on very wide blocks.
-// (Narrow column groups of 296 tiles, chunk-major, were measured 1-4% slower:
-// profiles/r02_j2d_column_groups.txt.)
+// x tile fastest inside a band (y-chunk-major).  Production uses one band (the whole
+// width): bands of 256-1024 tiles and narrow column groups of 296 tiles, chunk-major, were
+// measured equal or slower (profiles/r02_j2d_xband.txt, r02_j2d_column_groups.txt).
 JAC_HD inline TileItem decode_item2d(const SweepArgs &a, int item, int BX, int BY)
 {
     TileItem t;

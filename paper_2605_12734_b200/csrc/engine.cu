@@ -461,8 +461,10 @@ double *block_ptr_local(const jac_ctx *c, const int32_t nb[3], int buf, int f)
 
 // Tile / work-list geometry for the current c->variant (ntx, nty, z-chunks, item
 // count, column groups).  Called at create and for every autotune candidate.
-// 2-D x band width in x tiles (64 points each): 512 tiles = 32768 points.
-constexpr int kXBandTiles = 512;
+// 2-D x band width in x tiles (64 points each); 0 = the whole block width.  Bands of
+// 256 / 512 / 1024 tiles on 65536-131072-wide blocks were equal or slower (0 to +3.5%;
+// profiles/r02_j2d_xband.txt): the wide-row penalty is not L2 reuse between y chunks.
+constexpr int kXBandTiles = 0;
 
 void configure_tiles(jac_ctx *c)
 {
