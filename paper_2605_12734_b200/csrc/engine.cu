@@ -198,6 +198,15 @@ struct jac_ctx {
     bool tuned = false;                 // the create-time default variant was re-timed on data
 
     cudaStream_t stream = nullptr;
+    // staged host transfers (jac_set_init_box / jac_get_field_box): two device slabs, a
+    // copy stream, events filled[2] / drained[2] and the per-slab block lists; set up at
+    // the first transfer
+    double *stage[2] = {nullptr, nullptr};
+    size_t stage_bytes = 0;
+    cudaStream_t cstream = nullptr;
+    cudaEvent_t sev[4] = {nullptr, nullptr, nullptr, nullptr};
+    int32_t *dlist = nullptr;
+    size_t dlist_cap = 0;
     // JAC_F_PER_BLOCK (paper-style): one stream per block, events per block and parity
     std::vector<cudaStream_t> bstreams;
     std::vector<cudaEvent_t> bevents;  // [slot * 2 + parity]
@@ -261,7 +270,7 @@ const char *const kKnobs[] = {"JAC_L2PROMO", "JAC_ZC",     "JAC_ZCHUNK", "JAC_GC
                               "JAC_AUTOTUNE", "JAC_A",      "JAC_PALIGN", "JAC_NO_DENSE", "JAC_UNROLL",
                               "JAC_PDL",     "JAC_NO_FUSED_SYNC", "JAC_ORDER_EXP", "JAC_DROP_REMOTE",
                               "JAC_HOLD_SIGNAL", "JAC_REMOTE_SPREAD", "JAC_CHECK_SELFTEST", "JAC_YCHUNK",
-                              "JAC_NO_CTA_SYSFENCE", "JAC_REMOTE_COLMAJOR", "JAC_XBAND"};
+                              "JAC_NO_CTA_SYSFENCE", "JAC_REMOTE_COLMAJOR", "JAC_XBAND", "JAC_STAGE_BYTES"};
 
 const char *knob(jac_ctx *c, const char *name)
 {
@@ -1660,6 +1669,127 @@ int region_copy(jac_ctx *c, const int64_t *lo, const int64_t *ext, double *out, 
     CK(cudaStreamSynchronize(c->stream));
     return JAC_OK;
 }
+// Host <-> device transfers of the local box through two device staging slabs.  A slab
+// is a run of whole planes (3-D) or rows (2-D) of the region, moved over PCIe by one
+// pitched copy whose rows span the region's full width, then scattered into (gathered
+// from) the blocks by a kernel; the copy of one slab overlaps the kernel of the other
+// (copy stream + events).  One pitched copy per block instead ran the link at a quarter
+// of its rate for 32^3 blocks (256-byte rows), and the dense rows' x ghosts needed a
+// strided gather on the host.
+constexpr int64_t kStageSlabBytes = 64ll << 20;
+
+int ensure_staging(jac_ctx *c)
+{
+    if (c->stage[0]) return JAC_OK;
+    int64_t lo[3], ex[3];
+    jac_local_box(c, lo, ex);
+    const int64_t unit = (ex[2] > 1 ? ex[0] * ex[1] : ex[0]) * 8;  // one plane / row of the init region
+    const int64_t total = ex[0] * ex[1] * ex[2] * 8;
+    int64_t slab = kStageSlabBytes;
+    if (const char *v = knob(c, "JAC_STAGE_BYTES")) slab = std::max<int64_t>(1, atoll(v));  // tests: many slabs
+    const size_t bytes = (size_t)round_up(std::max(unit, std::min(slab, total)), 256);
+    void *p = nullptr;
+    if (cudaMalloc(&p, 2 * bytes) != cudaSuccess)
+        return fail(JAC_ENOMEM, "cudaMalloc(%zu bytes) for the host-transfer staging slabs", 2 * bytes);
+    c->stage[0] = static_cast<double *>(p);
+    c->stage[1] = c->stage[0] + bytes / 8;
+    c->stage_bytes = bytes;
+    CK(cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking));
+    for (cudaEvent_t &e : c->sev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    c->ranges.push_back({(unsigned long long)(uintptr_t)p, (unsigned long long)(uintptr_t)p + 2 * bytes});
+    return upload_ranges(c);
+}
+
+// to_device: the ghost-inclusive local box of `hbox` -> both buffers of every local
+// block (jac_set_init_box); else the interiors of the current buffer -> `hbox`
+// (jac_get_field_box).  hbox covers the region (check_box).  Returns with the transfer
+// queued on c->stream (to_device) or complete (else).
+int staged_transfer(jac_ctx *c, bool to_device, double *hbox, const int64_t *origin, const int64_t *extent)
+{
+    const jac::Geom &g = c->geom;
+    int rc;
+    if ((rc = ensure_staging(c))) return rc;
+    int64_t lo[3], ex[3];
+    jac_local_box(c, lo, ex);
+    if (!to_device)
+        for (int k = 0; k < 3; ++k) {
+            const int gh = k == 2 ? g.zg : 1;
+            lo[k] += gh;
+            ex[k] -= 2 * gh;
+        }
+    const int od = ex[2] > 1 ? 2 : 1;  // slab dimension: z (3-D), y (2-D or one interior plane)
+    const int64_t unit = (od == 2 ? ex[0] * ex[1] : ex[0]) * 8;
+    const int64_t per = std::max<int64_t>(1, (int64_t)c->stage_bytes / unit);
+    const int64_t nslab = (ex[od] + per - 1) / per;
+    // the blocks whose ghost-inclusive range meets each slab (indices into the table)
+    const int64_t bext[3] = {g.ex + 2, g.ey + 2, g.ez + 2 * g.zg};
+    std::vector<int32_t> list;
+    std::vector<int64_t> first((size_t)nslab + 1, 0);
+    for (int64_t i = 0; i < nslab; ++i) {
+        first[i] = (int64_t)list.size();
+        const int64_t s0 = lo[od] + i * per, s1 = std::min(s0 + per, lo[od] + ex[od]);
+        for (int32_t t = 0; t < c->nslots; ++t) {
+            const int64_t b0 = c->hblocks[t].org[od];
+            if (b0 < s1 && s0 < b0 + bext[od]) list.push_back(t);
+        }
+    }
+    first[nslab] = (int64_t)list.size();
+    if (list.size() > c->dlist_cap) {
+        if (c->dlist) CK(cudaFree(c->dlist));
+        c->dlist = nullptr;
+        CK(cudaMalloc(&c->dlist, list.size() * sizeof(int32_t)));
+        c->dlist_cap = list.size();
+    }
+    if (!list.empty()) CK(cudaMemcpy(c->dlist, list.data(), list.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    const jac::SweepArgs a = sweep_args(c, 0, 0);
+    cudaEvent_t *filled = c->sev, *drained = c->sev + 2;
+    // both slabs start free, after everything already queued on the main stream
+    CK(cudaEventRecord(drained[0], c->stream));
+    CK(cudaEventRecord(drained[1], c->stream));
+    const int cur = (int)(c->iters & 1);
+    const cudaPitchedPtr hp = make_cudaPitchedPtr(hbox, (size_t)extent[0] * 8, (size_t)extent[0], (size_t)extent[1]);
+    for (int64_t i = 0; i < nslab; ++i) {
+        const int b = (int)(i & 1);
+        jac::StageBox sb;
+        for (int k = 0; k < 3; ++k) { sb.o[k] = lo[k]; sb.n[k] = ex[k]; }
+        sb.o[od] = lo[od] + i * per;
+        sb.n[od] = std::min(per, lo[od] + ex[od] - sb.o[od]);
+        int64_t cells = 1;  // upper bound on one block's cells inside the slab
+        for (int k = 0; k < 3; ++k) cells *= std::min(bext[k], sb.n[k]);
+        const int32_t *L = c->dlist + first[i];
+        const int32_t nl = (int32_t)(first[i + 1] - first[i]);
+        cudaMemcpy3DParms m{};
+        const cudaPitchedPtr dp = make_cudaPitchedPtr(c->stage[b], (size_t)sb.n[0] * 8, (size_t)sb.n[0], (size_t)sb.n[1]);
+        const cudaPos hpos = make_cudaPos((size_t)(sb.o[0] - origin[0]) * 8, (size_t)(sb.o[1] - origin[1]),
+                                          (size_t)(sb.o[2] - origin[2]));
+        m.extent = make_cudaExtent((size_t)sb.n[0] * 8, (size_t)sb.n[1], (size_t)sb.n[2]);
+        if (to_device) {
+            CK(cudaStreamWaitEvent(c->cstream, drained[b], 0));
+            m.srcPtr = hp;
+            m.srcPos = hpos;
+            m.dstPtr = dp;
+            m.kind = cudaMemcpyHostToDevice;
+            CK(cudaMemcpy3DAsync(&m, c->cstream));
+            CK(cudaEventRecord(filled[b], c->cstream));
+            CK(cudaStreamWaitEvent(c->stream, filled[b], 0));
+            CK(jac::launch_stage_scatter(a, L, nl, cells, c->stage[b], sb, c->stream));
+            CK(cudaEventRecord(drained[b], c->stream));
+        } else {
+            CK(cudaStreamWaitEvent(c->stream, drained[b], 0));
+            CK(jac::launch_stage_gather(a, L, nl, cells, c->stage[b], sb, cur, c->stream));
+            CK(cudaEventRecord(filled[b], c->stream));
+            CK(cudaStreamWaitEvent(c->cstream, filled[b], 0));
+            m.srcPtr = dp;
+            m.dstPtr = hp;
+            m.dstPos = hpos;
+            m.kind = cudaMemcpyDeviceToHost;
+            CK(cudaMemcpy3DAsync(&m, c->cstream));
+            CK(cudaEventRecord(drained[b], c->cstream));
+        }
+    }
+    if (!to_device) CK(cudaStreamSynchronize(c->cstream));
+    return JAC_OK;
+}
 }  // namespace
 
 int jac_set_init_box(jac_ctx *c, const double *box, const int64_t *origin, const int64_t *extent)
@@ -1676,51 +1806,10 @@ int jac_set_init_box(jac_ctx *c, const double *box, const int64_t *origin, const
         return rc;
     }
     CK(cudaSetDevice(c->device));
-    const jac::Geom &g = c->geom;
     if ((rc = enqueue_barrier(c))) return rc;  // neighbours finished writing our ghosts
-    const bool dense = (g.A == 0);  // no inline ghost columns: the x ghosts go to the x-ghost arrays
-    for (int32_t s = 0; s < c->nslots; ++s) {
-        const jac::DevBlock &d = c->hblocks[s];
-        cudaMemcpy3DParms m{};
-        m.srcPtr = make_cudaPitchedPtr(const_cast<double *>(box), (size_t)extent[0] * 8, (size_t)extent[0],
-                                       (size_t)extent[1]);
-        m.srcPos = make_cudaPos((size_t)(d.org[0] + (dense ? 1 : 0) - origin[0]) * 8, (size_t)(d.org[1] - origin[1]),
-                                (size_t)(d.org[2] - origin[2]));
-        m.dstPtr = make_cudaPitchedPtr(c->slot_ptr(0, s), (size_t)g.P * 8, (size_t)g.P, (size_t)(g.ey + 2));
-        m.dstPos = make_cudaPos(dense ? 0 : (size_t)(g.A - 1) * 8, 0, 0);
-        m.extent = make_cudaExtent((size_t)(g.ex + (dense ? 0 : 2)) * 8, (size_t)(g.ey + 2), (size_t)(g.ez + 2 * g.zg));
-        m.kind = cudaMemcpyHostToDevice;
-        CK(cudaMemcpy3DAsync(&m, c->stream));
-    }
-    CK(cudaMemcpyAsync(c->slot_ptr(1, 0), c->slot_ptr(0, 0), (size_t)c->nslots * g.bstride * 8,
-                       cudaMemcpyDeviceToDevice, c->stream));
-    if (!dense) {
+    if ((rc = staged_transfer(c, true, const_cast<double *>(box), origin, extent))) return rc;
+    if (c->geom.A != 0)  // inline ghost columns -> x-ghost arrays (dense rows: written by the scatter)
         CK(jac::launch_xghost_extract(sweep_args(c, 0, 0), c->stream));
-        return finish_init(c);
-    }
-    // dense rows: gather the ghost columns i = -1 / ex (interior j, k) on the host in
-    // the device layout of the x-ghost arrays (slot-major, side, xgstride) and copy
-    // them into both buffers' arrays
-    std::vector<double> stage((size_t)c->nslots * 2 * g.xgstride, 0.0);
-    const int64_t ex0 = extent[0], ex1 = extent[1];
-    for (int32_t s = 0; s < c->nslots; ++s) {
-        const jac::DevBlock &d = c->hblocks[s];
-        for (int side = 0; side < 2; ++side) {
-            double *dst = stage.data() + ((size_t)s * 2 + side) * g.xgstride;
-            const int64_t px = d.org[0] + (side ? g.ex + 1 : 0) - origin[0];
-            for (int64_t k = 0; k < g.ez; ++k) {
-                const int64_t pz = d.org[2] + g.zg + k - origin[2];
-                for (int64_t j = 0; j < g.ey; ++j) {
-                    const int64_t py = d.org[1] + 1 + j - origin[1];
-                    dst[k * g.eyp + j] = box[(pz * ex1 + py) * ex0 + px];
-                }
-            }
-        }
-    }
-    for (int buf = 0; buf < 2; ++buf)
-        CK(cudaMemcpyAsync(jac::xg_array(c->xg, g, buf, 0, 0), stage.data(), stage.size() * 8,
-                           cudaMemcpyHostToDevice, c->stream));
-    CK(cudaStreamSynchronize(c->stream));  // stage is freed on return
     return finish_init(c);
 }
 
@@ -1961,31 +2050,16 @@ int jac_get_block(jac_ctx *c, int32_t ix, int32_t iy, int32_t iz, double *out)
 
 int jac_get_field_box(jac_ctx *c, double *box, const int64_t *origin, const int64_t *extent)
 {
+    NvtxRange range("jac_get_field_box");
     if (!c) return fail(JAC_EINVAL, "ctx is NULL");
     int rc;
     if ((rc = check_box(c, box, origin, extent))) return rc;
-    if (c->group) {
+    if (c->group) {  // the devices' regions are disjoint: read them back concurrently
         DeviceGuard guard;
-        for (jac_ctx *sc : c->subs)
-            if ((rc = jac_get_field_box(sc, box, origin, extent))) return rc;
-        return JAC_OK;
+        return for_each_sub(c, [&](jac_ctx *sc) { return jac_get_field_box(sc, box, origin, extent); });
     }
     CK(cudaSetDevice(c->device));
-    const jac::Geom &g = c->geom;
-    for (int32_t s = 0; s < c->nslots; ++s) {
-        const jac::DevBlock &d = c->hblocks[s];
-        cudaMemcpy3DParms m{};
-        m.srcPtr = make_cudaPitchedPtr(c->slot_ptr((int)(c->iters & 1), s), (size_t)g.P * 8, (size_t)g.P, (size_t)(g.ey + 2));
-        m.srcPos = make_cudaPos((size_t)g.A * 8, 1, (size_t)g.zg);
-        m.dstPtr = make_cudaPitchedPtr(box, (size_t)extent[0] * 8, (size_t)extent[0], (size_t)extent[1]);
-        m.dstPos = make_cudaPos((size_t)(d.org[0] + 1 - origin[0]) * 8, (size_t)(d.org[1] + 1 - origin[1]),
-                                (size_t)(d.org[2] + g.zg - origin[2]));
-        m.extent = make_cudaExtent((size_t)g.ex * 8, (size_t)g.ey, (size_t)g.ez);
-        m.kind = cudaMemcpyDeviceToHost;
-        CK(cudaMemcpy3DAsync(&m, c->stream));
-    }
-    CK(cudaStreamSynchronize(c->stream));
-    return JAC_OK;
+    return staged_transfer(c, false, box, origin, extent);
 }
 
 int jac_get_field(jac_ctx *c, double *padded)
@@ -2166,6 +2240,10 @@ int jac_destroy(jac_ctx *c)
     if (c->nccl_comm) {
         if (const NcclApi *N = nccl_api()) N->commDestroy((ncclComm_t)c->nccl_comm);
     }
+    if (c->cstream) { cudaStreamSynchronize(c->cstream); cudaStreamDestroy(c->cstream); }
+    for (cudaEvent_t e : c->sev) if (e) cudaEventDestroy(e);
+    if (c->stage[0]) cudaFree(c->stage[0]);
+    if (c->dlist) cudaFree(c->dlist);
     if (c->ev0) cudaEventDestroy(c->ev0);
     if (c->ev1) cudaEventDestroy(c->ev1);
     if (c->stream) cudaStreamDestroy(c->stream);

@@ -20,7 +20,8 @@
 //  barrier_kernel     cross-rank neighbour barrier on device flags (st.release.sys /
 //                     ld.acquire.sys over NVLink), replacing the paper's IPC event
 //                     pool.
-//  xghost_extract_kernel / hash_init_kernel  cold-path init helpers.
+//  xghost_extract_kernel / hash_init_kernel / stage_scatter_kernel / stage_gather_kernel
+//                     cold-path init and host-transfer helpers.
 //
 // The update (PAPER.md:281 Jacobi, 3-D lift R1; readings R2-R4 in DESIGN.md):
 //     u' = ((((((c + x-) + x+) + y-) + y+) + z-) + z+) * fl(1/7)
@@ -1147,6 +1148,72 @@ __global__ void hash_init_kernel(const SweepArgs a, int64_t nx, int64_t ny, uint
     }
 }
 
+// ------------------------------------------------------------------ staged host transfers
+// The intersection of a block's cell range [lo0, lo0 + n) (block-relative, per dim) with
+// the stage box, as block-relative [lo, hi).
+__device__ __forceinline__ bool stage_clip(const DevBlock &blk, const StageBox &sb, const int64_t lo0[3],
+                                           const int64_t n[3], int64_t lo[3], int64_t hi[3])
+{
+    bool any = true;
+    for (int k = 0; k < 3; ++k) {
+        lo[k] = max(lo0[k], sb.o[k] - blk.org[k]);
+        hi[k] = min(lo0[k] + n[k], sb.o[k] + sb.n[k] - blk.org[k]);
+        any &= lo[k] < hi[k];
+    }
+    return any;
+}
+
+__global__ void stage_scatter_kernel(const SweepArgs a, const int32_t *list, int32_t nlist, const double *st,
+                                     const StageBox sb)
+{
+    const Geom &g = a.g;
+    const int64_t lo0[3] = {0, 0, 0}, n[3] = {g.ex + 2, g.ey + 2, g.ez + 2 * g.zg};  // ghost-inclusive
+    for (int32_t li = blockIdx.y; li < nlist; li += gridDim.y) {
+        const DevBlock &blk = a.blocks[list[li]];
+        int64_t lo[3], hi[3];
+        if (!stage_clip(blk, sb, lo0, n, lo, hi)) continue;
+        const int64_t nx = hi[0] - lo[0], ny = hi[1] - lo[1], nc = nx * ny * (hi[2] - lo[2]);
+        double *b0 = a.arena + (int64_t)blk.slot * g.bstride;
+        double *b1 = a.arena + (int64_t)(g.nslots + blk.slot) * g.bstride;
+        for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nc; e += (int64_t)gridDim.x * blockDim.x) {
+            const int64_t ii = lo[0] + e % nx, jj = lo[1] + (e / nx) % ny, kk = lo[2] + e / (nx * ny);
+            const double v = st[((blk.org[2] + kk - sb.o[2]) * sb.n[1] + (blk.org[1] + jj - sb.o[1])) * sb.n[0] +
+                                (blk.org[0] + ii - sb.o[0])];
+            if (g.A == 0 && (ii == 0 || ii == n[0] - 1)) {  // dense rows: x ghosts -> x-ghost arrays
+                if (jj >= 1 && jj <= g.ey && kk >= g.zg && kk < g.ez + g.zg) {
+                    const int64_t xi = (kk - g.zg) * g.eyp + (jj - 1);
+                    ST8(a, xg_array(a.xg, g, 0, blk.slot, ii ? 1 : 0) + xi, v);
+                    ST8(a, xg_array(a.xg, g, 1, blk.slot, ii ? 1 : 0) + xi, v);
+                }
+                continue;
+            }
+            const int64_t off = kk * g.Q + jj * g.P + (g.A - 1) + ii;
+            ST8(a, b0 + off, v);
+            ST8(a, b1 + off, v);
+        }
+    }
+}
+
+__global__ void stage_gather_kernel(const SweepArgs a, const int32_t *list, int32_t nlist, double *st,
+                                    const StageBox sb, int buf)
+{
+    const Geom &g = a.g;
+    const int64_t lo0[3] = {1, 1, g.zg}, n[3] = {g.ex, g.ey, g.ez};  // interior
+    for (int32_t li = blockIdx.y; li < nlist; li += gridDim.y) {
+        const DevBlock &blk = a.blocks[list[li]];
+        int64_t lo[3], hi[3];
+        if (!stage_clip(blk, sb, lo0, n, lo, hi)) continue;
+        const int64_t nx = hi[0] - lo[0], ny = hi[1] - lo[1], nc = nx * ny * (hi[2] - lo[2]);
+        const double *src = a.arena + (int64_t)(buf * g.nslots + blk.slot) * g.bstride;
+        for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nc; e += (int64_t)gridDim.x * blockDim.x) {
+            const int64_t ii = lo[0] + e % nx, jj = lo[1] + (e / nx) % ny, kk = lo[2] + e / (nx * ny);
+            ST8(a, st + ((blk.org[2] + kk - sb.o[2]) * sb.n[1] + (blk.org[1] + jj - sb.o[1])) * sb.n[0] +
+                       (blk.org[0] + ii - sb.o[0]),
+                src[kk * g.Q + jj * g.P + (g.A - 1) + ii]);
+        }
+    }
+}
+
 // ------------------------------------------------------------------ host launchers
 template <int BX, int BY, int W, int NT, int NS>
 static int resident_tma_t()
@@ -1333,6 +1400,28 @@ cudaError_t launch_face_copy(const FaceCopy *list, int n, int64_t maxcount, cuda
 cudaError_t launch_hash_init(const SweepArgs &a, int64_t nx, int64_t ny, uint64_t seed, cudaStream_t s)
 {
     hash_init_kernel<<<dim3(64, (unsigned)a.g.nslots), 256, 0, s>>>(a, nx, ny, seed);
+    return cudaGetLastError();
+}
+
+static dim3 stage_grid(int32_t nlist, int64_t cells)
+{
+    const int64_t gx = std::min<int64_t>(64, std::max<int64_t>(1, (cells + 1023) / 1024));
+    return dim3((unsigned)gx, (unsigned)std::max(1, std::min(nlist, 65535)));
+}
+
+cudaError_t launch_stage_scatter(const SweepArgs &a, const int32_t *list, int32_t nlist, int64_t cells,
+                                 const double *st, const StageBox &sb, cudaStream_t s)
+{
+    if (nlist <= 0) return cudaSuccess;
+    stage_scatter_kernel<<<stage_grid(nlist, cells), 256, 0, s>>>(a, list, nlist, st, sb);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_stage_gather(const SweepArgs &a, const int32_t *list, int32_t nlist, int64_t cells, double *st,
+                                const StageBox &sb, int buf, cudaStream_t s)
+{
+    if (nlist <= 0) return cudaSuccess;
+    stage_gather_kernel<<<stage_grid(nlist, cells), 256, 0, s>>>(a, list, nlist, st, sb, buf);
     return cudaGetLastError();
 }
 

@@ -41,5 +41,19 @@ cudaError_t launch_pack_face(const SweepArgs &a, int slot, int f, int buf, int p
 cudaError_t launch_unpack_face(const SweepArgs &a, int slot, int nslot, int f, int buf, int par, cudaStream_t s);
 cudaError_t launch_xghost_extract(const SweepArgs &a, cudaStream_t s);
 cudaError_t launch_hash_init(const SweepArgs &a, int64_t nx, int64_t ny, uint64_t seed, cudaStream_t s);
+// Staged host transfers (jac_set_init_box / jac_get_field_box): one slab of the local
+// box sits in device staging memory, x fastest; the kernels move it into / out of the
+// blocks listed in list[0..nlist) (indices into a.blocks).
+struct StageBox {
+    int64_t o[3];  // padded global coordinates of the first staged cell
+    int64_t n[3];  // staged extents (x, y, z)
+};
+// every ghost-inclusive cell of a listed block inside the stage box -> both buffers
+// (dense rows: x ghosts -> both x-ghost arrays), as hash_init does with hash values
+cudaError_t launch_stage_scatter(const SweepArgs &a, const int32_t *list, int32_t nlist, int64_t cells,
+                                 const double *st, const StageBox &sb, cudaStream_t s);
+// every interior cell of a listed block inside the stage box, buffer `buf` -> staging
+cudaError_t launch_stage_gather(const SweepArgs &a, const int32_t *list, int32_t nlist, int64_t cells, double *st,
+                                const StageBox &sb, int buf, cudaStream_t s);
 
 }  // namespace jac

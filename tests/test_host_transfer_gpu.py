@@ -1,0 +1,85 @@
+"""Host transfers through the device staging slabs (engine.cu staged_transfer):
+jac_set_init_box scatters slabs of whole planes (3-D) or rows (2-D) into both buffers
+and the x-ghost arrays; jac_get_field_box gathers the interiors back.  Forced tiny slabs
+(JAC_STAGE_BYTES=1: one plane / row per slab, i.e. slabs that cut blocks and their ghost
+layers) must give the oracle's bits in both row layouts, leave every cell outside the
+local interiors untouched, and work from pinned memory."""
+import numpy as np
+import pytest
+
+import jac_inputs as JI
+import oracle
+import paper_2605_12734_b200 as jb
+
+pytestmark = pytest.mark.gpu
+
+
+def _bits(a, b):
+    bad = np.flatnonzero(a.view(np.uint64) != b.view(np.uint64))
+    assert bad.size == 0, f"{bad.size} mismatches, first at {np.unravel_index(bad[0], a.shape)}"
+
+
+@pytest.mark.parametrize("slab", ["1", "20000", None])
+@pytest.mark.parametrize("dense", [True, False])
+@pytest.mark.parametrize("dims,blocks", [((64, 48, 40), (2, 3, 5)), ((32, 32, 32), (4, 4, 4)), ((40, 24, 9), (1, 1, 1))])
+def test_staged_init_and_readback_3d(monkeypatch, slab, dense, dims, blocks):
+    if slab or not dense:
+        monkeypatch.setenv("JAC_EXPERIMENT", "1")
+    if slab:
+        monkeypatch.setenv("JAC_STAGE_BYTES", slab)
+    if not dense:
+        monkeypatch.setenv("JAC_NO_DENSE", "1")
+    u0 = JI.hash_field(*dims, seed=7)
+    with jb.Jacobi3D(dims, blocks) as s:
+        s.set_init(u0)
+        _bits(s.field(u0), u0)  # round trip before any sweep
+        s.step(1)  # every ghost cell the scatter wrote is read once
+        _bits(s.field(u0), oracle.jacobi3d(u0, 1))
+        s.step(4)
+        _bits(s.field(u0), oracle.jacobi3d(u0, 5))
+
+
+def test_field_box_leaves_the_shell_untouched(monkeypatch):
+    monkeypatch.setenv("JAC_EXPERIMENT", "1")
+    monkeypatch.setenv("JAC_STAGE_BYTES", "1")
+    dims = (48, 32, 16)
+    u0 = JI.hash_field(*dims, seed=8)
+    with jb.Jacobi3D(dims, (2, 2, 2)) as s:
+        s.set_init(u0)
+        s.step(3)
+        box = np.full_like(u0, np.nan)
+        s.field_box(box, (0, 0, 0))
+    want = oracle.jacobi3d(u0, 3)
+    _bits(box[1:-1, 1:-1, 1:-1], want[1:-1, 1:-1, 1:-1])
+    shell = np.ones(box.shape, bool)
+    shell[1:-1, 1:-1, 1:-1] = False
+    assert np.isnan(box[shell]).all()
+
+
+@pytest.mark.parametrize("slab", ["1", None])
+@pytest.mark.parametrize("dims,blocks", [((200, 90), (2, 3)), ((64, 64), (1, 1)), ((70, 33), (5, 3))])
+def test_staged_init_and_readback_2d(monkeypatch, slab, dims, blocks):
+    if slab:
+        monkeypatch.setenv("JAC_EXPERIMENT", "1")
+        monkeypatch.setenv("JAC_STAGE_BYTES", slab)
+    u0 = JI.hash_field2d(*dims, seed=9)
+    with jb.Jacobi2D(dims, blocks) as s:
+        s.set_init(u0)
+        _bits(s.field(u0), u0)
+        s.step(6)
+        _bits(s.field(u0), oracle.jacobi2d_omp(u0, 6)[0])
+
+
+def test_pinned_host_buffers():
+    torch = pytest.importorskip("torch")
+    dims = (64, 64, 64)
+    u0 = JI.hash_field(*dims, seed=10)
+    hin = torch.empty(u0.shape, dtype=torch.float64, pin_memory=True).numpy()
+    hin[...] = u0
+    hout = torch.empty(u0.shape, dtype=torch.float64, pin_memory=True).numpy()
+    hout[...] = 0.0
+    with jb.Jacobi3D(dims, (2, 2, 2)) as s:
+        s.set_init_box(hin, (0, 0, 0))
+        s.step(2)
+        s.field_box(hout, (0, 0, 0))
+    _bits(hout[1:-1, 1:-1, 1:-1], oracle.jacobi3d(u0, 2)[1:-1, 1:-1, 1:-1])
