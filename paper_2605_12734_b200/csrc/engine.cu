@@ -544,6 +544,133 @@ void configure_tiles(jac_ctx *c)
 
 int build_item_map(jac_ctx *c);
 
+// Host <-> device transfers of the local box through two device staging slabs.  A slab
+// is a run of whole planes (3-D) or rows (2-D) of the region, moved over PCIe by one
+// pitched copy whose rows span the region's full width, then scattered into (gathered
+// from) the blocks by a kernel; the copy of one slab overlaps the kernel of the other
+// (copy stream + events).  One pitched copy per block instead ran the link at a quarter
+// of its rate for 32^3 blocks (256-byte rows), and the dense rows' x ghosts needed a
+// strided gather on the host.
+constexpr int64_t kStageSlabBytes = 64ll << 20;
+
+int ensure_staging(jac_ctx *c)
+{
+    if (c->stage[0]) return JAC_OK;
+    int64_t lo[3], ex[3];
+    jac_local_box(c, lo, ex);
+    const int64_t unit = (ex[2] > 1 ? ex[0] * ex[1] : ex[0]) * 8;  // one plane / row of the init region
+    const int64_t total = ex[0] * ex[1] * ex[2] * 8;
+    int64_t slab = kStageSlabBytes;
+    if (const char *v = knob(c, "JAC_STAGE_BYTES")) slab = std::max<int64_t>(1, atoll(v));  // tests: many slabs
+    const size_t bytes = (size_t)round_up(std::max(unit, std::min(slab, total)), 256);
+    void *p = nullptr;
+    if (cudaMalloc(&p, 2 * bytes) != cudaSuccess)
+        return fail(JAC_ENOMEM, "cudaMalloc(%zu bytes) for the host-transfer staging slabs", 2 * bytes);
+    c->stage[0] = static_cast<double *>(p);
+    c->stage[1] = c->stage[0] + bytes / 8;
+    c->stage_bytes = bytes;
+    CK(cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking));
+    for (cudaEvent_t &e : c->sev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    // block lists: a block meets at most ceil(extent / slab) + 1 slabs of the init region
+    const jac::Geom &g = c->geom;
+    const int64_t bext = ex[2] > 1 ? g.ez + 2 * g.zg : g.ey + 2;
+    const int64_t per = std::max<int64_t>(1, (int64_t)bytes / unit);
+    c->dlist_cap = (size_t)c->nslots * (size_t)((bext + per - 1) / per + 1);
+    CK(cudaMalloc(&c->dlist, c->dlist_cap * sizeof(int32_t)));
+    c->ranges.push_back({(unsigned long long)(uintptr_t)p, (unsigned long long)(uintptr_t)p + 2 * bytes});
+    return upload_ranges(c);
+}
+
+// to_device: the ghost-inclusive local box of `hbox` -> both buffers of every local
+// block (jac_set_init_box); else the interiors of the current buffer -> `hbox`
+// (jac_get_field_box).  hbox covers the region (check_box).  Returns with the transfer
+// queued on c->stream (to_device) or complete (else).
+int staged_transfer(jac_ctx *c, bool to_device, double *hbox, const int64_t *origin, const int64_t *extent)
+{
+    const jac::Geom &g = c->geom;
+    int rc;
+    if ((rc = ensure_staging(c))) return rc;
+    int64_t lo[3], ex[3];
+    jac_local_box(c, lo, ex);
+    if (!to_device)
+        for (int k = 0; k < 3; ++k) {
+            const int gh = k == 2 ? g.zg : 1;
+            lo[k] += gh;
+            ex[k] -= 2 * gh;
+        }
+    const int od = ex[2] > 1 ? 2 : 1;  // slab dimension: z (3-D), y (2-D or one interior plane)
+    const int64_t unit = (od == 2 ? ex[0] * ex[1] : ex[0]) * 8;
+    const int64_t per = std::max<int64_t>(1, (int64_t)c->stage_bytes / unit);
+    const int64_t nslab = (ex[od] + per - 1) / per;
+    // the blocks whose ghost-inclusive range meets each slab (indices into the table)
+    const int64_t bext[3] = {g.ex + 2, g.ey + 2, g.ez + 2 * g.zg};
+    std::vector<int32_t> list;
+    std::vector<int64_t> first((size_t)nslab + 1, 0);
+    for (int64_t i = 0; i < nslab; ++i) {
+        first[i] = (int64_t)list.size();
+        const int64_t s0 = lo[od] + i * per, s1 = std::min(s0 + per, lo[od] + ex[od]);
+        for (int32_t t = 0; t < c->nslots; ++t) {
+            const int64_t b0 = c->hblocks[t].org[od];
+            if (b0 < s1 && s0 < b0 + bext[od]) list.push_back(t);
+        }
+    }
+    first[nslab] = (int64_t)list.size();
+    if (list.size() > c->dlist_cap) {
+        if (c->dlist) CK(cudaFree(c->dlist));
+        c->dlist = nullptr;
+        CK(cudaMalloc(&c->dlist, list.size() * sizeof(int32_t)));
+        c->dlist_cap = list.size();
+    }
+    if (!list.empty()) CK(cudaMemcpy(c->dlist, list.data(), list.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    const jac::SweepArgs a = sweep_args(c, 0, 0);
+    cudaEvent_t *filled = c->sev, *drained = c->sev + 2;
+    // both slabs start free, after everything already queued on the main stream
+    CK(cudaEventRecord(drained[0], c->stream));
+    CK(cudaEventRecord(drained[1], c->stream));
+    const int cur = (int)(c->iters & 1);
+    const cudaPitchedPtr hp = make_cudaPitchedPtr(hbox, (size_t)extent[0] * 8, (size_t)extent[0], (size_t)extent[1]);
+    for (int64_t i = 0; i < nslab; ++i) {
+        const int b = (int)(i & 1);
+        jac::StageBox sb;
+        for (int k = 0; k < 3; ++k) { sb.o[k] = lo[k]; sb.n[k] = ex[k]; }
+        sb.o[od] = lo[od] + i * per;
+        sb.n[od] = std::min(per, lo[od] + ex[od] - sb.o[od]);
+        const int64_t rows = std::min(bext[1], sb.n[1]) * std::min(bext[2], sb.n[2]);  // per block, at most
+        const int32_t *L = c->dlist + first[i];
+        const int32_t nl = (int32_t)(first[i + 1] - first[i]);
+        cudaMemcpy3DParms m{};
+        const cudaPitchedPtr dp = make_cudaPitchedPtr(c->stage[b], (size_t)sb.n[0] * 8, (size_t)sb.n[0], (size_t)sb.n[1]);
+        const cudaPos hpos = make_cudaPos((size_t)(sb.o[0] - origin[0]) * 8, (size_t)(sb.o[1] - origin[1]),
+                                          (size_t)(sb.o[2] - origin[2]));
+        m.extent = make_cudaExtent((size_t)sb.n[0] * 8, (size_t)sb.n[1], (size_t)sb.n[2]);
+        if (to_device) {
+            CK(cudaStreamWaitEvent(c->cstream, drained[b], 0));
+            m.srcPtr = hp;
+            m.srcPos = hpos;
+            m.dstPtr = dp;
+            m.kind = cudaMemcpyHostToDevice;
+            CK(cudaMemcpy3DAsync(&m, c->cstream));
+            CK(cudaEventRecord(filled[b], c->cstream));
+            CK(cudaStreamWaitEvent(c->stream, filled[b], 0));
+            CK(jac::launch_stage_scatter(a, L, nl, rows, c->stage[b], sb, c->stream));
+            CK(cudaEventRecord(drained[b], c->stream));
+        } else {
+            CK(cudaStreamWaitEvent(c->stream, drained[b], 0));
+            CK(jac::launch_stage_gather(a, L, nl, rows, c->stage[b], sb, cur, c->stream));
+            CK(cudaEventRecord(filled[b], c->stream));
+            CK(cudaStreamWaitEvent(c->cstream, filled[b], 0));
+            m.srcPtr = dp;
+            m.dstPtr = hp;
+            m.dstPos = hpos;
+            m.kind = cudaMemcpyDeviceToHost;
+            CK(cudaMemcpy3DAsync(&m, c->cstream));
+            CK(cudaEventRecord(drained[b], c->cstream));
+        }
+    }
+    if (!to_device) CK(cudaStreamSynchronize(c->cstream));
+    return JAC_OK;
+}
+
 // Autotune of the wide tile's TMA ring depth (6 stages at 3 CTAs / SM vs 4 stages at
 // 4 CTAs / SM) on the context's own decomposition, GPU and data: 1 + 8 sweeps each,
 // exchange off, the faster wins (ties within 0.5%: 6 stages).  Measured with the lean
@@ -1012,6 +1139,7 @@ int create_common(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, in
     for (int k = 0; k < 4; ++k) c->status_h[k] = 0;
     c->ranges.push_back({(unsigned long long)(uintptr_t)c->alloc, (unsigned long long)(uintptr_t)c->alloc + c->alloc_bytes});
     if ((rc = upload_ranges(c))) return bail(rc);
+    if ((rc = ensure_staging(c))) return bail(rc);  // host-transfer slabs (adds its store range)
     // per-partition sync table: own control words; neighbours' flag slots are local
     // for virtual partitions, filled when the peers are connected for a rank context
     c->hsync.assign(c->parts.size(), jac::PartSync{});
@@ -1667,127 +1795,6 @@ int region_copy(jac_ctx *c, const int64_t *lo, const int64_t *ext, double *out, 
         CK(cudaMemcpy3DAsync(&m, c->stream));
     }
     CK(cudaStreamSynchronize(c->stream));
-    return JAC_OK;
-}
-// Host <-> device transfers of the local box through two device staging slabs.  A slab
-// is a run of whole planes (3-D) or rows (2-D) of the region, moved over PCIe by one
-// pitched copy whose rows span the region's full width, then scattered into (gathered
-// from) the blocks by a kernel; the copy of one slab overlaps the kernel of the other
-// (copy stream + events).  One pitched copy per block instead ran the link at a quarter
-// of its rate for 32^3 blocks (256-byte rows), and the dense rows' x ghosts needed a
-// strided gather on the host.
-constexpr int64_t kStageSlabBytes = 64ll << 20;
-
-int ensure_staging(jac_ctx *c)
-{
-    if (c->stage[0]) return JAC_OK;
-    int64_t lo[3], ex[3];
-    jac_local_box(c, lo, ex);
-    const int64_t unit = (ex[2] > 1 ? ex[0] * ex[1] : ex[0]) * 8;  // one plane / row of the init region
-    const int64_t total = ex[0] * ex[1] * ex[2] * 8;
-    int64_t slab = kStageSlabBytes;
-    if (const char *v = knob(c, "JAC_STAGE_BYTES")) slab = std::max<int64_t>(1, atoll(v));  // tests: many slabs
-    const size_t bytes = (size_t)round_up(std::max(unit, std::min(slab, total)), 256);
-    void *p = nullptr;
-    if (cudaMalloc(&p, 2 * bytes) != cudaSuccess)
-        return fail(JAC_ENOMEM, "cudaMalloc(%zu bytes) for the host-transfer staging slabs", 2 * bytes);
-    c->stage[0] = static_cast<double *>(p);
-    c->stage[1] = c->stage[0] + bytes / 8;
-    c->stage_bytes = bytes;
-    CK(cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking));
-    for (cudaEvent_t &e : c->sev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    c->ranges.push_back({(unsigned long long)(uintptr_t)p, (unsigned long long)(uintptr_t)p + 2 * bytes});
-    return upload_ranges(c);
-}
-
-// to_device: the ghost-inclusive local box of `hbox` -> both buffers of every local
-// block (jac_set_init_box); else the interiors of the current buffer -> `hbox`
-// (jac_get_field_box).  hbox covers the region (check_box).  Returns with the transfer
-// queued on c->stream (to_device) or complete (else).
-int staged_transfer(jac_ctx *c, bool to_device, double *hbox, const int64_t *origin, const int64_t *extent)
-{
-    const jac::Geom &g = c->geom;
-    int rc;
-    if ((rc = ensure_staging(c))) return rc;
-    int64_t lo[3], ex[3];
-    jac_local_box(c, lo, ex);
-    if (!to_device)
-        for (int k = 0; k < 3; ++k) {
-            const int gh = k == 2 ? g.zg : 1;
-            lo[k] += gh;
-            ex[k] -= 2 * gh;
-        }
-    const int od = ex[2] > 1 ? 2 : 1;  // slab dimension: z (3-D), y (2-D or one interior plane)
-    const int64_t unit = (od == 2 ? ex[0] * ex[1] : ex[0]) * 8;
-    const int64_t per = std::max<int64_t>(1, (int64_t)c->stage_bytes / unit);
-    const int64_t nslab = (ex[od] + per - 1) / per;
-    // the blocks whose ghost-inclusive range meets each slab (indices into the table)
-    const int64_t bext[3] = {g.ex + 2, g.ey + 2, g.ez + 2 * g.zg};
-    std::vector<int32_t> list;
-    std::vector<int64_t> first((size_t)nslab + 1, 0);
-    for (int64_t i = 0; i < nslab; ++i) {
-        first[i] = (int64_t)list.size();
-        const int64_t s0 = lo[od] + i * per, s1 = std::min(s0 + per, lo[od] + ex[od]);
-        for (int32_t t = 0; t < c->nslots; ++t) {
-            const int64_t b0 = c->hblocks[t].org[od];
-            if (b0 < s1 && s0 < b0 + bext[od]) list.push_back(t);
-        }
-    }
-    first[nslab] = (int64_t)list.size();
-    if (list.size() > c->dlist_cap) {
-        if (c->dlist) CK(cudaFree(c->dlist));
-        c->dlist = nullptr;
-        CK(cudaMalloc(&c->dlist, list.size() * sizeof(int32_t)));
-        c->dlist_cap = list.size();
-    }
-    if (!list.empty()) CK(cudaMemcpy(c->dlist, list.data(), list.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
-    const jac::SweepArgs a = sweep_args(c, 0, 0);
-    cudaEvent_t *filled = c->sev, *drained = c->sev + 2;
-    // both slabs start free, after everything already queued on the main stream
-    CK(cudaEventRecord(drained[0], c->stream));
-    CK(cudaEventRecord(drained[1], c->stream));
-    const int cur = (int)(c->iters & 1);
-    const cudaPitchedPtr hp = make_cudaPitchedPtr(hbox, (size_t)extent[0] * 8, (size_t)extent[0], (size_t)extent[1]);
-    for (int64_t i = 0; i < nslab; ++i) {
-        const int b = (int)(i & 1);
-        jac::StageBox sb;
-        for (int k = 0; k < 3; ++k) { sb.o[k] = lo[k]; sb.n[k] = ex[k]; }
-        sb.o[od] = lo[od] + i * per;
-        sb.n[od] = std::min(per, lo[od] + ex[od] - sb.o[od]);
-        int64_t cells = 1;  // upper bound on one block's cells inside the slab
-        for (int k = 0; k < 3; ++k) cells *= std::min(bext[k], sb.n[k]);
-        const int32_t *L = c->dlist + first[i];
-        const int32_t nl = (int32_t)(first[i + 1] - first[i]);
-        cudaMemcpy3DParms m{};
-        const cudaPitchedPtr dp = make_cudaPitchedPtr(c->stage[b], (size_t)sb.n[0] * 8, (size_t)sb.n[0], (size_t)sb.n[1]);
-        const cudaPos hpos = make_cudaPos((size_t)(sb.o[0] - origin[0]) * 8, (size_t)(sb.o[1] - origin[1]),
-                                          (size_t)(sb.o[2] - origin[2]));
-        m.extent = make_cudaExtent((size_t)sb.n[0] * 8, (size_t)sb.n[1], (size_t)sb.n[2]);
-        if (to_device) {
-            CK(cudaStreamWaitEvent(c->cstream, drained[b], 0));
-            m.srcPtr = hp;
-            m.srcPos = hpos;
-            m.dstPtr = dp;
-            m.kind = cudaMemcpyHostToDevice;
-            CK(cudaMemcpy3DAsync(&m, c->cstream));
-            CK(cudaEventRecord(filled[b], c->cstream));
-            CK(cudaStreamWaitEvent(c->stream, filled[b], 0));
-            CK(jac::launch_stage_scatter(a, L, nl, cells, c->stage[b], sb, c->stream));
-            CK(cudaEventRecord(drained[b], c->stream));
-        } else {
-            CK(cudaStreamWaitEvent(c->stream, drained[b], 0));
-            CK(jac::launch_stage_gather(a, L, nl, cells, c->stage[b], sb, cur, c->stream));
-            CK(cudaEventRecord(filled[b], c->stream));
-            CK(cudaStreamWaitEvent(c->cstream, filled[b], 0));
-            m.srcPtr = dp;
-            m.dstPtr = hp;
-            m.dstPos = hpos;
-            m.kind = cudaMemcpyDeviceToHost;
-            CK(cudaMemcpy3DAsync(&m, c->cstream));
-            CK(cudaEventRecord(drained[b], c->cstream));
-        }
-    }
-    if (!to_device) CK(cudaStreamSynchronize(c->cstream));
     return JAC_OK;
 }
 }  // namespace

@@ -20,7 +20,7 @@
 //  barrier_kernel     cross-rank neighbour barrier on device flags (st.release.sys /
 //                     ld.acquire.sys over NVLink), replacing the paper's IPC event
 //                     pool.
-//  xghost_extract_kernel / hash_init_kernel / stage_scatter_kernel / stage_gather_kernel
+//  xghost_extract_kernel / hash_init_kernel / stage_kernel<scatter|gather>
 //                     cold-path init and host-transfer helpers.
 //
 // The update (PAPER.md:281 Jacobi, 3-D lift R1; readings R2-R4 in DESIGN.md):
@@ -1163,53 +1163,52 @@ __device__ __forceinline__ bool stage_clip(const DevBlock &blk, const StageBox &
     return any;
 }
 
-__global__ void stage_scatter_kernel(const SweepArgs a, const int32_t *list, int32_t nlist, const double *st,
-                                     const StageBox sb)
+// One warp per row of the clipped range (x along the lanes, rows spread over the grid):
+// coalesced on both sides, one division per row.  SCATTER: staging -> every
+// ghost-inclusive cell of the block in both buffers (dense rows: x ghosts -> both
+// x-ghost arrays, as hash_init_kernel); else interior cells of buffer `buf` -> staging.
+template <bool SCATTER>
+__global__ void __launch_bounds__(256) stage_kernel(const SweepArgs a, const int32_t *__restrict__ list, int32_t nlist,
+                                                   double *__restrict__ st, const StageBox sb, int buf)
 {
     const Geom &g = a.g;
-    const int64_t lo0[3] = {0, 0, 0}, n[3] = {g.ex + 2, g.ey + 2, g.ez + 2 * g.zg};  // ghost-inclusive
+    const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    const int64_t lo0[3] = {SCATTER ? 0 : 1, SCATTER ? 0 : 1, SCATTER ? 0 : g.zg};
+    const int64_t n[3] = {SCATTER ? g.ex + 2 : g.ex, SCATTER ? g.ey + 2 : g.ey,
+                          SCATTER ? g.ez + 2 * g.zg : g.ez};
     for (int32_t li = blockIdx.y; li < nlist; li += gridDim.y) {
         const DevBlock &blk = a.blocks[list[li]];
         int64_t lo[3], hi[3];
         if (!stage_clip(blk, sb, lo0, n, lo, hi)) continue;
-        const int64_t nx = hi[0] - lo[0], ny = hi[1] - lo[1], nc = nx * ny * (hi[2] - lo[2]);
-        double *b0 = a.arena + (int64_t)blk.slot * g.bstride;
+        const int ny = (int)(hi[1] - lo[1]), nrows = ny * (int)(hi[2] - lo[2]);
+        const int i0 = (int)lo[0], i1 = (int)hi[0];
+        double *b0 = a.arena + (int64_t)((SCATTER ? 0 : buf) * g.nslots + blk.slot) * g.bstride;
         double *b1 = a.arena + (int64_t)(g.nslots + blk.slot) * g.bstride;
-        for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nc; e += (int64_t)gridDim.x * blockDim.x) {
-            const int64_t ii = lo[0] + e % nx, jj = lo[1] + (e / nx) % ny, kk = lo[2] + e / (nx * ny);
-            const double v = st[((blk.org[2] + kk - sb.o[2]) * sb.n[1] + (blk.org[1] + jj - sb.o[1])) * sb.n[0] +
-                                (blk.org[0] + ii - sb.o[0])];
-            if (g.A == 0 && (ii == 0 || ii == n[0] - 1)) {  // dense rows: x ghosts -> x-ghost arrays
-                if (jj >= 1 && jj <= g.ey && kk >= g.zg && kk < g.ez + g.zg) {
-                    const int64_t xi = (kk - g.zg) * g.eyp + (jj - 1);
-                    ST8(a, xg_array(a.xg, g, 0, blk.slot, ii ? 1 : 0) + xi, v);
-                    ST8(a, xg_array(a.xg, g, 1, blk.slot, ii ? 1 : 0) + xi, v);
+        for (int r = blockIdx.x * nw + (threadIdx.x >> 5); r < nrows; r += gridDim.x * nw) {
+            const int64_t jj = lo[1] + r % ny, kk = lo[2] + r / ny;
+            double *srow = st + ((blk.org[2] + kk - sb.o[2]) * sb.n[1] + (blk.org[1] + jj - sb.o[1])) * sb.n[0] +
+                           (blk.org[0] - sb.o[0]);  // element ii of the block row
+            const int64_t roff = kk * g.Q + jj * g.P + (g.A - 1);
+            if (SCATTER) {
+                const bool xgrow = g.A == 0 && jj >= 1 && jj <= g.ey && kk >= g.zg && kk < g.ez + g.zg;
+#pragma unroll 4
+                for (int ii = i0 + lane; ii < i1; ii += 32) {
+                    const double v = srow[ii];
+                    if (g.A == 0 && (ii == 0 || ii == n[0] - 1)) {  // dense rows: x ghosts
+                        if (xgrow) {
+                            const int64_t xi = (kk - g.zg) * g.eyp + (jj - 1);
+                            ST8(a, xg_array(a.xg, g, 0, blk.slot, ii ? 1 : 0) + xi, v);
+                            ST8(a, xg_array(a.xg, g, 1, blk.slot, ii ? 1 : 0) + xi, v);
+                        }
+                        continue;
+                    }
+                    ST8(a, b0 + roff + ii, v);
+                    ST8(a, b1 + roff + ii, v);
                 }
-                continue;
+            } else {
+#pragma unroll 4
+                for (int ii = i0 + lane; ii < i1; ii += 32) ST8(a, srow + ii, b0[roff + ii]);
             }
-            const int64_t off = kk * g.Q + jj * g.P + (g.A - 1) + ii;
-            ST8(a, b0 + off, v);
-            ST8(a, b1 + off, v);
-        }
-    }
-}
-
-__global__ void stage_gather_kernel(const SweepArgs a, const int32_t *list, int32_t nlist, double *st,
-                                    const StageBox sb, int buf)
-{
-    const Geom &g = a.g;
-    const int64_t lo0[3] = {1, 1, g.zg}, n[3] = {g.ex, g.ey, g.ez};  // interior
-    for (int32_t li = blockIdx.y; li < nlist; li += gridDim.y) {
-        const DevBlock &blk = a.blocks[list[li]];
-        int64_t lo[3], hi[3];
-        if (!stage_clip(blk, sb, lo0, n, lo, hi)) continue;
-        const int64_t nx = hi[0] - lo[0], ny = hi[1] - lo[1], nc = nx * ny * (hi[2] - lo[2]);
-        const double *src = a.arena + (int64_t)(buf * g.nslots + blk.slot) * g.bstride;
-        for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nc; e += (int64_t)gridDim.x * blockDim.x) {
-            const int64_t ii = lo[0] + e % nx, jj = lo[1] + (e / nx) % ny, kk = lo[2] + e / (nx * ny);
-            ST8(a, st + ((blk.org[2] + kk - sb.o[2]) * sb.n[1] + (blk.org[1] + jj - sb.o[1])) * sb.n[0] +
-                       (blk.org[0] + ii - sb.o[0]),
-                src[kk * g.Q + jj * g.P + (g.A - 1) + ii]);
         }
     }
 }
@@ -1403,25 +1402,27 @@ cudaError_t launch_hash_init(const SweepArgs &a, int64_t nx, int64_t ny, uint64_
     return cudaGetLastError();
 }
 
-static dim3 stage_grid(int32_t nlist, int64_t cells)
+// rows: an upper bound on one listed block's rows inside the slab (8 rows per CTA)
+static dim3 stage_grid(int32_t nlist, int64_t rows)
 {
-    const int64_t gx = std::min<int64_t>(64, std::max<int64_t>(1, (cells + 1023) / 1024));
+    const int64_t gx = std::min<int64_t>(std::max<int64_t>(1, 4096 / std::max(1, nlist)),
+                                         std::max<int64_t>(1, (rows + 7) / 8));
     return dim3((unsigned)gx, (unsigned)std::max(1, std::min(nlist, 65535)));
 }
 
-cudaError_t launch_stage_scatter(const SweepArgs &a, const int32_t *list, int32_t nlist, int64_t cells,
+cudaError_t launch_stage_scatter(const SweepArgs &a, const int32_t *list, int32_t nlist, int64_t rows,
                                  const double *st, const StageBox &sb, cudaStream_t s)
 {
     if (nlist <= 0) return cudaSuccess;
-    stage_scatter_kernel<<<stage_grid(nlist, cells), 256, 0, s>>>(a, list, nlist, st, sb);
+    stage_kernel<true><<<stage_grid(nlist, rows), 256, 0, s>>>(a, list, nlist, const_cast<double *>(st), sb, 0);
     return cudaGetLastError();
 }
 
-cudaError_t launch_stage_gather(const SweepArgs &a, const int32_t *list, int32_t nlist, int64_t cells, double *st,
+cudaError_t launch_stage_gather(const SweepArgs &a, const int32_t *list, int32_t nlist, int64_t rows, double *st,
                                 const StageBox &sb, int buf, cudaStream_t s)
 {
     if (nlist <= 0) return cudaSuccess;
-    stage_gather_kernel<<<stage_grid(nlist, cells), 256, 0, s>>>(a, list, nlist, st, sb, buf);
+    stage_kernel<false><<<stage_grid(nlist, rows), 256, 0, s>>>(a, list, nlist, st, sb, buf);
     return cudaGetLastError();
 }
 

@@ -50,10 +50,10 @@ struct StageBox {
 };
 // every ghost-inclusive cell of a listed block inside the stage box -> both buffers
 // (dense rows: x ghosts -> both x-ghost arrays), as hash_init does with hash values
-cudaError_t launch_stage_scatter(const SweepArgs &a, const int32_t *list, int32_t nlist, int64_t cells,
+cudaError_t launch_stage_scatter(const SweepArgs &a, const int32_t *list, int32_t nlist, int64_t rows,
                                  const double *st, const StageBox &sb, cudaStream_t s);
 // every interior cell of a listed block inside the stage box, buffer `buf` -> staging
-cudaError_t launch_stage_gather(const SweepArgs &a, const int32_t *list, int32_t nlist, int64_t cells, double *st,
+cudaError_t launch_stage_gather(const SweepArgs &a, const int32_t *list, int32_t nlist, int64_t rows, double *st,
                                 const StageBox &sb, int buf, cudaStream_t s);
 
 }  // namespace jac
