@@ -203,6 +203,7 @@ struct jac_ctx {
     // the first transfer
     double *stage[2] = {nullptr, nullptr};
     size_t stage_bytes = 0;
+    bool stage_pitched = false;  // JAC_STAGE_PITCHED=1 (tests): pitched copies even for contiguous slabs
     cudaStream_t cstream = nullptr;
     cudaEvent_t sev[4] = {nullptr, nullptr, nullptr, nullptr};
     int32_t *dlist = nullptr;
@@ -270,7 +271,8 @@ const char *const kKnobs[] = {"JAC_L2PROMO", "JAC_ZC",     "JAC_ZCHUNK", "JAC_GC
                               "JAC_AUTOTUNE", "JAC_A",      "JAC_PALIGN", "JAC_NO_DENSE", "JAC_UNROLL",
                               "JAC_PDL",     "JAC_NO_FUSED_SYNC", "JAC_ORDER_EXP", "JAC_DROP_REMOTE",
                               "JAC_HOLD_SIGNAL", "JAC_REMOTE_SPREAD", "JAC_CHECK_SELFTEST", "JAC_YCHUNK",
-                              "JAC_NO_CTA_SYSFENCE", "JAC_REMOTE_COLMAJOR", "JAC_XBAND", "JAC_STAGE_BYTES"};
+                              "JAC_NO_CTA_SYSFENCE", "JAC_REMOTE_COLMAJOR", "JAC_XBAND", "JAC_STAGE_BYTES",
+                              "JAC_STAGE_PITCHED"};
 
 const char *knob(jac_ctx *c, const char *name)
 {
@@ -558,10 +560,11 @@ int ensure_staging(jac_ctx *c)
     if (c->stage[0]) return JAC_OK;
     int64_t lo[3], ex[3];
     jac_local_box(c, lo, ex);
-    const int64_t unit = (ex[2] > 1 ? ex[0] * ex[1] : ex[0]) * 8;  // one plane / row of the init region
+    const int64_t unit = (ex[2] > 1 ? round_up(ex[0], 32) * ex[1] : round_up(ex[0], 32)) * 8;  // one plane / row
     const int64_t total = ex[0] * ex[1] * ex[2] * 8;
     int64_t slab = kStageSlabBytes;
     if (const char *v = knob(c, "JAC_STAGE_BYTES")) slab = std::max<int64_t>(1, atoll(v));  // tests: many slabs
+    c->stage_pitched = knob(c, "JAC_STAGE_PITCHED") != nullptr;
     const size_t bytes = (size_t)round_up(std::max(unit, std::min(slab, total)), 256);
     void *p = nullptr;
     if (cudaMalloc(&p, 2 * bytes) != cudaSuccess)
@@ -599,7 +602,12 @@ int staged_transfer(jac_ctx *c, bool to_device, double *hbox, const int64_t *ori
             ex[k] -= 2 * gh;
         }
     const int od = ex[2] > 1 ? 2 : 1;  // slab dimension: z (3-D), y (2-D or one interior plane)
-    const int64_t unit = (od == 2 ? ex[0] * ex[1] : ex[0]) * 8;
+    // A region whose rows (and planes) are the host box's is one contiguous run per slab:
+    // one linear copy.  Otherwise a pitched copy into 256-byte aligned staging rows (a
+    // host-to-device copy into unaligned 4112-byte rows ran at 60% of the link rate).
+    const bool contiguous = ex[0] == extent[0] && (od == 1 || ex[1] == extent[1]) && !c->stage_pitched;
+    const int64_t pitch = contiguous ? ex[0] : round_up(ex[0], 32);
+    const int64_t unit = (od == 2 ? pitch * ex[1] : pitch) * 8;
     const int64_t per = std::max<int64_t>(1, (int64_t)c->stage_bytes / unit);
     const int64_t nslab = (ex[od] + per - 1) / per;
     // the blocks whose ghost-inclusive range meets each slab (indices into the table)
@@ -633,23 +641,27 @@ int staged_transfer(jac_ctx *c, bool to_device, double *hbox, const int64_t *ori
         const int b = (int)(i & 1);
         jac::StageBox sb;
         for (int k = 0; k < 3; ++k) { sb.o[k] = lo[k]; sb.n[k] = ex[k]; }
+        sb.pitch = pitch;
         sb.o[od] = lo[od] + i * per;
         sb.n[od] = std::min(per, lo[od] + ex[od] - sb.o[od]);
         const int64_t rows = std::min(bext[1], sb.n[1]) * std::min(bext[2], sb.n[2]);  // per block, at most
         const int32_t *L = c->dlist + first[i];
         const int32_t nl = (int32_t)(first[i + 1] - first[i]);
         cudaMemcpy3DParms m{};
-        const cudaPitchedPtr dp = make_cudaPitchedPtr(c->stage[b], (size_t)sb.n[0] * 8, (size_t)sb.n[0], (size_t)sb.n[1]);
+        const cudaPitchedPtr dp = make_cudaPitchedPtr(c->stage[b], (size_t)pitch * 8, (size_t)sb.n[0], (size_t)sb.n[1]);
         const cudaPos hpos = make_cudaPos((size_t)(sb.o[0] - origin[0]) * 8, (size_t)(sb.o[1] - origin[1]),
                                           (size_t)(sb.o[2] - origin[2]));
         m.extent = make_cudaExtent((size_t)sb.n[0] * 8, (size_t)sb.n[1], (size_t)sb.n[2]);
+        double *hrun = hbox + ((sb.o[2] - origin[2]) * extent[1] + (sb.o[1] - origin[1])) * extent[0] + (sb.o[0] - origin[0]);
+        const size_t run = (size_t)(sb.n[0] * sb.n[1] * sb.n[2]) * 8;  // contiguous: the slab's bytes
         if (to_device) {
             CK(cudaStreamWaitEvent(c->cstream, drained[b], 0));
             m.srcPtr = hp;
             m.srcPos = hpos;
             m.dstPtr = dp;
             m.kind = cudaMemcpyHostToDevice;
-            CK(cudaMemcpy3DAsync(&m, c->cstream));
+            if (contiguous) CK(cudaMemcpyAsync(c->stage[b], hrun, run, cudaMemcpyHostToDevice, c->cstream));
+            else CK(cudaMemcpy3DAsync(&m, c->cstream));
             CK(cudaEventRecord(filled[b], c->cstream));
             CK(cudaStreamWaitEvent(c->stream, filled[b], 0));
             CK(jac::launch_stage_scatter(a, L, nl, rows, c->stage[b], sb, c->stream));
@@ -663,7 +675,8 @@ int staged_transfer(jac_ctx *c, bool to_device, double *hbox, const int64_t *ori
             m.dstPtr = hp;
             m.dstPos = hpos;
             m.kind = cudaMemcpyDeviceToHost;
-            CK(cudaMemcpy3DAsync(&m, c->cstream));
+            if (contiguous) CK(cudaMemcpyAsync(hrun, c->stage[b], run, cudaMemcpyDeviceToHost, c->cstream));
+            else CK(cudaMemcpy3DAsync(&m, c->cstream));
             CK(cudaEventRecord(drained[b], c->cstream));
         }
     }

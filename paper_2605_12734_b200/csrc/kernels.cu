@@ -1186,7 +1186,7 @@ __global__ void __launch_bounds__(256) stage_kernel(const SweepArgs a, const int
         double *b1 = a.arena + (int64_t)(g.nslots + blk.slot) * g.bstride;
         for (int r = blockIdx.x * nw + (threadIdx.x >> 5); r < nrows; r += gridDim.x * nw) {
             const int64_t jj = lo[1] + r % ny, kk = lo[2] + r / ny;
-            double *srow = st + ((blk.org[2] + kk - sb.o[2]) * sb.n[1] + (blk.org[1] + jj - sb.o[1])) * sb.n[0] +
+            double *srow = st + ((blk.org[2] + kk - sb.o[2]) * sb.n[1] + (blk.org[1] + jj - sb.o[1])) * sb.pitch +
                            (blk.org[0] - sb.o[0]);  // element ii of the block row
             const int64_t roff = kk * g.Q + jj * g.P + (g.A - 1);
             if (SCATTER) {

@@ -47,6 +47,7 @@ cudaError_t launch_hash_init(const SweepArgs &a, int64_t nx, int64_t ny, uint64_
 struct StageBox {
     int64_t o[3];  // padded global coordinates of the first staged cell
     int64_t n[3];  // staged extents (x, y, z)
+    int64_t pitch; // doubles per staged row (>= n[0])
 };
 // every ghost-inclusive cell of a listed block inside the stage box -> both buffers
 // (dense rows: x ghosts -> both x-ghost arrays), as hash_init does with hash values

@@ -19,12 +19,14 @@ def _bits(a, b):
     assert bad.size == 0, f"{bad.size} mismatches, first at {np.unravel_index(bad[0], a.shape)}"
 
 
+@pytest.mark.parametrize("pitched", [False, True])
 @pytest.mark.parametrize("slab", ["1", "20000", None])
 @pytest.mark.parametrize("dense", [True, False])
 @pytest.mark.parametrize("dims,blocks", [((64, 48, 40), (2, 3, 5)), ((32, 32, 32), (4, 4, 4)), ((40, 24, 9), (1, 1, 1))])
-def test_staged_init_and_readback_3d(monkeypatch, slab, dense, dims, blocks):
-    if slab or not dense:
-        monkeypatch.setenv("JAC_EXPERIMENT", "1")
+def test_staged_init_and_readback_3d(monkeypatch, pitched, slab, dense, dims, blocks):
+    monkeypatch.setenv("JAC_EXPERIMENT", "1")
+    if pitched:  # the sub-box path (multi-GPU partitions) on one GPU
+        monkeypatch.setenv("JAC_STAGE_PITCHED", "1")
     if slab:
         monkeypatch.setenv("JAC_STAGE_BYTES", slab)
     if not dense:
@@ -56,11 +58,14 @@ def test_field_box_leaves_the_shell_untouched(monkeypatch):
     assert np.isnan(box[shell]).all()
 
 
+@pytest.mark.parametrize("pitched", [False, True])
 @pytest.mark.parametrize("slab", ["1", None])
 @pytest.mark.parametrize("dims,blocks", [((200, 90), (2, 3)), ((64, 64), (1, 1)), ((70, 33), (5, 3))])
-def test_staged_init_and_readback_2d(monkeypatch, slab, dims, blocks):
+def test_staged_init_and_readback_2d(monkeypatch, pitched, slab, dims, blocks):
+    monkeypatch.setenv("JAC_EXPERIMENT", "1")
+    if pitched:
+        monkeypatch.setenv("JAC_STAGE_PITCHED", "1")
     if slab:
-        monkeypatch.setenv("JAC_EXPERIMENT", "1")
         monkeypatch.setenv("JAC_STAGE_BYTES", slab)
     u0 = JI.hash_field2d(*dims, seed=9)
     with jb.Jacobi2D(dims, blocks) as s:

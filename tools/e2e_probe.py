@@ -1,4 +1,4 @@
-"""Breakdown of the e2e job (bench.py run_e2e): jac_set_init_box, jac_step(K),
+"""(JAC_EXPERIMENT=1 JAC_STAGE_PITCHED=1: the pitched staging path.)  Breakdown of the e2e job (bench.py run_e2e): jac_set_init_box, jac_step(K),
 jac_get_field_box with pinned host buffers, each timed on the host, next to plain
 linear pinned H2D / D2H copies of the same byte counts (torch)."""
 import os, sys, time
