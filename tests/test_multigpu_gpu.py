@@ -74,6 +74,8 @@ SP_CASES = [
     # (n_gpus, dims, blocks, grid, iters, flags, hash)
     (2, (64, 48, 80), (2, 2, 4), None, 21, 0, False),         # 1x1x2, ODF 8
     (2, (128, 40, 36), (2, 1, 1), (2, 1, 1), 9, 0, True),     # x split: remote x-ghost arrays
+    (2, (96, 40, 36), (2, 1, 1), (2, 1, 1), 7, 0, False),     # x split, host init: pitched staging rows
+    (2, (48, 64, 40), (1, 2, 1), (1, 2, 1), 5, 0, False),     # y split, host init: one run per plane
     (2, (48, 48, 48), (2, 2, 2), None, 11, 1 << 4, False),    # unfused pack + barrier + pull
     (2, (48, 48, 48), (2, 2, 2), None, 5, 1 << 1, False),     # no graph (interleaved launches)
     (2, (64, 64, 64), (2, 2, 2), None, 6, 1 << 5, False),     # plain-load sweep + barrier
