@@ -148,7 +148,8 @@ int jac_plan_face(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, in
  * JAC_F_NCCL / JAC_F_PER_BLOCK with n_gpus > 1 (rank contexts only).  Under
  * JAC_F_VIRTUAL_GPUS every partition lives on device 0 (test mode, see the flag).
  * Allocates everything (two ghosted arrays per block, descriptor table, control
- * words, streams, events); nothing is allocated inside jac_step (PAPER.md:190-194
+ * words, streams, events, two host-transfer staging slabs of up to 64 MiB); nothing
+ * is allocated inside jac_step (PAPER.md:190-194
  * "persistent Views ... preallocated buffers"). *out receives the context. */
 int jac_create(int64_t nx, int64_t ny, int64_t nz, int32_t bx, int32_t by, int32_t bz,
                int32_t n_gpus, const int32_t *gpu_grid, uint32_t flags, jac_ctx **out);
@@ -184,8 +185,10 @@ int jac_nccl_init(jac_ctx *c, const void *id);
 /* Copies the padded initial field (host, see conventions) into BOTH ghosted
  * buffers of every local block, ghosts included, so the shell is Dirichlet data in
  * both ("outer halo = initial boundary values") and the first sweep's
- * ghosts are the neighbours' initial values.  Resets iterations_done to 0.  A
- * pinned host array is copied by DMA; a pageable one is staged by the driver. */
+ * ghosts are the neighbours' initial values.  Resets iterations_done to 0.  The
+ * data moves through device staging slabs (whole planes / rows per slab, a kernel
+ * scatters each into the blocks); a pinned host array is read by DMA at the link
+ * rate, a pageable one is staged again by the driver. */
 int jac_set_init(jac_ctx *c, const double *padded);
 /* Same as jac_set_init for a sub-box of the padded global array: `box` holds
  * extent[2] x extent[1] x extent[0] doubles (x fastest) whose element (0,0,0) is
