@@ -230,7 +230,9 @@ int jac_get_block_padded(jac_ctx *c, int32_t ix, int32_t iy, int32_t iz, double 
  * non-local blocks untouched). */
 int jac_get_field(jac_ctx *c, double *padded);
 /* Interiors of all local blocks written into a padded sub-box laid out as for
- * jac_set_init_box (cells outside local interiors untouched). */
+ * jac_set_init_box (cells outside local interiors untouched).  The box must cover the
+ * local interiors (not necessarily their ghost layer): a box of exactly the interiors
+ * is read back with one linear copy per staging slab. */
 int jac_get_field_box(jac_ctx *c, double *box, const int64_t *origin, const int64_t *extent);
 
 /* Interior sub-box [lo, lo+ext) (0-based interior coordinates, x fastest) into

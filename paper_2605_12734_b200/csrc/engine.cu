@@ -1778,12 +1778,20 @@ int jac_local_box(const jac_ctx *c, int64_t *origin, int64_t *extent)
 }
 
 namespace {
-int check_box(const jac_ctx *c, const void *box, const int64_t *origin, const int64_t *extent)
+// The host box must cover the context's ghost-inclusive local box (init), or only its
+// local interiors (interior = true: read-back).
+int check_box(const jac_ctx *c, const void *box, const int64_t *origin, const int64_t *extent, bool interior = false)
 {
     if (!box || !origin || !extent) return fail(JAC_EINVAL, "box/origin/extent is NULL");
     int64_t lo[3], ex[3];
     jac_local_box(c, lo, ex);
     const int zg = c->group ? c->subs[0]->geom.zg : c->geom.zg;
+    if (interior)
+        for (int k = 0; k < 3; ++k) {
+            const int gh = k == 2 ? zg : 1;
+            lo[k] += gh;
+            ex[k] -= 2 * gh;
+        }
     for (int k = 0; k < 3; ++k)
         if (origin[k] < 0 || extent[k] < 1 || origin[k] > lo[k] || origin[k] + extent[k] < lo[k] + ex[k] ||
             origin[k] + extent[k] > c->plan.n[k] + (k == 2 ? 2 * zg : 2))
@@ -2084,7 +2092,7 @@ int jac_get_field_box(jac_ctx *c, double *box, const int64_t *origin, const int6
     NvtxRange range("jac_get_field_box");
     if (!c) return fail(JAC_EINVAL, "ctx is NULL");
     int rc;
-    if ((rc = check_box(c, box, origin, extent))) return rc;
+    if ((rc = check_box(c, box, origin, extent, true))) return rc;
     if (c->group) {  // the devices' regions are disjoint: read them back concurrently
         DeviceGuard guard;
         return for_each_sub(c, [&](jac_ctx *sc) { return jac_get_field_box(sc, box, origin, extent); });

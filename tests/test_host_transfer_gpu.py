@@ -88,3 +88,24 @@ def test_pinned_host_buffers():
         s.step(2)
         s.field_box(hout, (0, 0, 0))
     _bits(hout[1:-1, 1:-1, 1:-1], oracle.jacobi3d(u0, 2)[1:-1, 1:-1, 1:-1])
+
+
+@pytest.mark.parametrize("pitched", [False, True])
+def test_interior_box_readback(monkeypatch, pitched):
+    """jac_get_field_box into a box of exactly the interiors (the linear read-back) and
+    into a box one cell short of them (JAC_EINVAL)."""
+    monkeypatch.setenv("JAC_EXPERIMENT", "1")
+    monkeypatch.setenv("JAC_STAGE_BYTES", "1")
+    if pitched:
+        monkeypatch.setenv("JAC_STAGE_PITCHED", "1")
+    dims = (40, 24, 16)
+    u0 = JI.hash_field(*dims, seed=11)
+    with jb.Jacobi3D(dims, (2, 1, 2)) as s:
+        s.set_init(u0)
+        s.step(3)
+        inner = np.full((dims[2], dims[1], dims[0]), np.nan)
+        s.field_box(inner, (1, 1, 1))
+        _bits(inner, oracle.jacobi3d(u0, 3)[1:-1, 1:-1, 1:-1])
+        short = np.zeros((dims[2] - 1, dims[1], dims[0]))
+        with pytest.raises(jb.jacobi3d.JacError):
+            s.field_box(short, (1, 1, 1))
