@@ -208,6 +208,7 @@ struct jac_ctx {
     cudaEvent_t sev[4] = {nullptr, nullptr, nullptr, nullptr};
     int32_t *dlist = nullptr;
     size_t dlist_cap = 0;
+    std::vector<int32_t> by_origin[3];  // table indices sorted by block origin along x / y / z
     // JAC_F_PER_BLOCK (paper-style): one stream per block, events per block and parity
     std::vector<cudaStream_t> bstreams;
     std::vector<cudaEvent_t> bevents;  // [slot * 2 + parity]
@@ -614,17 +615,25 @@ int staged_transfer(jac_ctx *c, bool to_device, double *hbox, const int64_t *ori
     const int64_t unit = (od == 2 ? pitch * ex[1] : pitch) * 8;
     const int64_t per = std::max<int64_t>(1, (int64_t)c->stage_bytes / unit);
     const int64_t nslab = (ex[od] + per - 1) / per;
-    // the blocks whose ghost-inclusive range meets each slab (indices into the table)
+    // the blocks whose ghost-inclusive range meets each slab (indices into the table),
+    // from the table sorted by origin along the slab dimension
     const int64_t bext[3] = {g.ex + 2, g.ey + 2, g.ez + 2 * g.zg};
+    std::vector<int32_t> &order = c->by_origin[od];
+    if (order.size() != (size_t)c->nslots) {
+        order.resize(c->nslots);
+        for (int32_t t = 0; t < c->nslots; ++t) order[t] = t;
+        std::stable_sort(order.begin(), order.end(),
+                         [&](int32_t x, int32_t y) { return c->hblocks[x].org[od] < c->hblocks[y].org[od]; });
+    }
     std::vector<int32_t> list;
     std::vector<int64_t> first((size_t)nslab + 1, 0);
     for (int64_t i = 0; i < nslab; ++i) {
         first[i] = (int64_t)list.size();
         const int64_t s0 = lo[od] + i * per, s1 = std::min(s0 + per, lo[od] + ex[od]);
-        for (int32_t t = 0; t < c->nslots; ++t) {
-            const int64_t b0 = c->hblocks[t].org[od];
-            if (b0 < s1 && s0 < b0 + bext[od]) list.push_back(t);
-        }
+        // origins in (s0 - bext, s1)
+        auto it = std::lower_bound(order.begin(), order.end(), s0 - bext[od] + 1,
+                                   [&](int32_t t, int64_t v) { return c->hblocks[t].org[od] < v; });
+        for (; it != order.end() && c->hblocks[*it].org[od] < s1; ++it) list.push_back(*it);
     }
     first[nslab] = (int64_t)list.size();
     if (list.size() > c->dlist_cap) {
