@@ -204,6 +204,7 @@ struct jac_ctx {
     double *stage[2] = {nullptr, nullptr};
     size_t stage_bytes = 0;
     bool stage_pitched = false;  // JAC_STAGE_PITCHED=1 (tests): pitched copies even for contiguous slabs
+    bool stage_direct = false;   // JAC_DIRECT=1 (experiment): kernels read / write a mapped pinned host box
     cudaStream_t cstream = nullptr;
     cudaEvent_t sev[4] = {nullptr, nullptr, nullptr, nullptr};
     int32_t *dlist = nullptr;
@@ -273,7 +274,7 @@ const char *const kKnobs[] = {"JAC_L2PROMO", "JAC_ZC",     "JAC_ZCHUNK", "JAC_GC
                               "JAC_PDL",     "JAC_NO_FUSED_SYNC", "JAC_ORDER_EXP", "JAC_DROP_REMOTE",
                               "JAC_HOLD_SIGNAL", "JAC_REMOTE_SPREAD", "JAC_CHECK_SELFTEST", "JAC_YCHUNK",
                               "JAC_NO_CTA_SYSFENCE", "JAC_REMOTE_COLMAJOR", "JAC_XBAND", "JAC_STAGE_BYTES",
-                              "JAC_STAGE_PITCHED"};
+                              "JAC_STAGE_PITCHED", "JAC_DIRECT"};
 
 const char *knob(jac_ctx *c, const char *name)
 {
@@ -566,6 +567,7 @@ int ensure_staging(jac_ctx *c)
     int64_t slab = kStageSlabBytes;
     if (const char *v = knob(c, "JAC_STAGE_BYTES")) slab = std::max<int64_t>(1, atoll(v));  // tests: many slabs
     c->stage_pitched = knob(c, "JAC_STAGE_PITCHED") != nullptr;
+    c->stage_direct = knob(c, "JAC_DIRECT") != nullptr;
     const size_t bytes = (size_t)round_up(std::max(unit, std::min(slab, total)), 256);
     void *p = nullptr;
     if (cudaMalloc(&p, 2 * bytes) != cudaSuccess)
@@ -613,6 +615,29 @@ int staged_transfer(jac_ctx *c, bool to_device, double *hbox, const int64_t *ori
     const bool contiguous = full_rows && (od == 1 || ex[1] == extent[1]);
     const int64_t pitch = full_rows ? ex[0] : round_up(ex[0], 32);
     const int64_t unit = (od == 2 ? pitch * ex[1] : pitch) * 8;
+#ifndef JAC_CHECKED
+    // JAC_DIRECT=1 (experiment): a pinned, mapped host box is read / written by the
+    // kernel itself over PCIe, one launch, no staging
+    cudaPointerAttributes pa{};
+    if (c->stage_direct && cudaPointerGetAttributes(&pa, hbox) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
+        pa.devicePointer) {
+        std::vector<int32_t> all(c->nslots);
+        for (int32_t t = 0; t < c->nslots; ++t) all[t] = t;
+        CK(cudaMemcpy(c->dlist, all.data(), all.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+        jac::StageBox sb;
+        for (int k = 0; k < 3; ++k) { sb.o[k] = origin[k]; sb.n[k] = extent[k]; }
+        sb.pitch = extent[0];
+        const int64_t rows = (int64_t)(g.ey + 2) * (g.ez + 2 * g.zg);
+        double *dev_view = static_cast<double *>(pa.devicePointer);
+        const jac::SweepArgs a = sweep_args(c, 0, 0);
+        if (to_device) CK(jac::launch_stage_scatter(a, c->dlist, c->nslots, rows, dev_view, sb, c->stream));
+        else {
+            CK(jac::launch_stage_gather(a, c->dlist, c->nslots, rows, dev_view, sb, (int)(c->iters & 1), c->stream));
+            CK(cudaStreamSynchronize(c->stream));
+        }
+        return JAC_OK;
+    }
+#endif
     const int64_t per = std::max<int64_t>(1, (int64_t)c->stage_bytes / unit);
     const int64_t nslab = (ex[od] + per - 1) / per;
     // the blocks whose ghost-inclusive range meets each slab (indices into the table),
