@@ -75,7 +75,14 @@ def test_staged_init_and_readback_2d(monkeypatch, pitched, slab, dims, blocks):
         _bits(s.field(u0), oracle.jacobi2d_omp(u0, 6)[0])
 
 
-def test_pinned_host_buffers():
+@pytest.mark.parametrize("mode", [None, "JAC_STAGE_PITCHED", "JAC_DIRECT"])
+def test_pinned_host_buffers(monkeypatch, mode):
+    """Pinned boxes: staged slabs (default), the kernel reading the host rows itself
+    (partial rows, here forced by JAC_STAGE_PITCHED) and the zero-copy path both ways
+    (JAC_DIRECT)."""
+    if mode:
+        monkeypatch.setenv("JAC_EXPERIMENT", "1")
+        monkeypatch.setenv(mode, "1")
     torch = pytest.importorskip("torch")
     dims = (64, 64, 64)
     u0 = JI.hash_field(*dims, seed=10)
