@@ -607,18 +607,33 @@ __global__ void __launch_bounds__(NT, min_ctas_per_sm(NT, NS, BX, BY))
         auto has = [&](int f) { return has_target(a, blk, dst, f); };
         const bool edge = (t.x0 == 0) || (t.x0 + BX >= g.ex) ||
                           (exch && ((t.y0 == 0 && has(YM)) || (t.y0 + BY >= g.ey && has(YP))));
-        double *xf = nullptr;  // x-face target of this lane (row 0 of the thread, plane q)
-        int64_t xs = 0;
-        if (exch && (ilo || ihi1)) {
-            const int f = ilo ? XM : XP;
+        // x faces: the face lanes (first / last lane of every row group) put their values
+        // in shared memory; after the plane's barrier the first BY threads store each
+        // side's BY rows, two per thread, as one contiguous run per instruction (full
+        // 32-byte sectors: over NVLink a partly written sector travels as its own
+        // transfer -- the face lanes storing their own rows sent 1.75x the face bytes).
+        auto xtarget = [&](int f, int64_t &stride) -> double * {
+            double *p = nullptr;
+            stride = 0;
             if (a.mode == MODE_FUSED) {
-                xf = blk.nb[f][dst];
-                xs = g.eyp;
+                p = blk.nb[f][dst];
+                stride = g.eyp;
             } else if (blk.nb[f][0]) {
-                xf = a.outbox + (int64_t)slot * g.ostride + g.ooff[f];
-                xs = g.ey;
+                p = a.outbox + (int64_t)slot * g.ostride + g.ooff[f];
+                stride = g.ey;
             }
-            if (xf) xf += t.y0 + jl0 + (int64_t)(t.zs - 1 + q) * xs;
+            return p;
+        };
+        int64_t xs = 0;
+        const bool xput = exch && (ilo || ihi1) && xtarget(ilo ? XM : XP, xs) != nullptr;  // holds face values
+        const int xside = ilo ? 0 : 1;
+        double *xf = nullptr;  // this thread's store target (threads < BY): rows 2l, 2l+1 of one side
+        if (exch && (int)threadIdx.x < BY) {
+            const int side = (int)threadIdx.x / (BY / 2);
+            if (side == 0 ? t.x0 == 0 : t.x0 + BX >= g.ex) {
+                xf = xtarget(side ? XP : XM, xs);
+                if (xf) xf += t.y0 + 2 * ((int)threadIdx.x % (BY / 2)) + (int64_t)(t.zs - 1 + q) * xs;
+            }
         }
         // y-face target of this thread (row 0 if yf_lo, else row RY-1; a full tile has
         // ey >= BY, so no thread holds both): the neighbour's ghost row (plane stride
@@ -648,6 +663,7 @@ __global__ void __launch_bounds__(NT, min_ctas_per_sm(NT, NS, BX, BY))
         }
         const bool yv = (ys & 1) == 0;  // y-face rows 16-byte aligned (ghost rows; packed, even ex)
         const bool xv2 = (xs & 1) == 0;  // x-face row pairs 16-byte aligned (pitch eyp; outbox: even ey)
+        __shared__ __align__(16) double xface[2][2][BY];  // [plane parity][side][row]
         double *op = own + (int64_t)(t.zs + q) * g.Q + (int64_t)(t.y0 + jl0 + 1) * g.P + g.A + i;
         const int64_t P = g.P, Qs = g.Q;
         int sn = (q + 1) % NSL;               // ring slot of plane q+1
@@ -659,7 +675,6 @@ __global__ void __launch_bounds__(NT, min_ctas_per_sm(NT, NS, BX, BY))
             const double *Sb = Sc + sb;
 #pragma unroll
             for (int r = 0; r < RY; ++r) C[r] = *reinterpret_cast<const double2 *>(Sn + sb + r * W);
-            double xprev = 0.0;  // x-face value of the previous row (pairs of rows: one store)
 #pragma unroll
             for (int r = 0; r < RY; ++r) {
                 double xm = Sb[r * W - 1], xp1 = Sb[r * W + 2];
@@ -673,18 +688,7 @@ __global__ void __launch_bounds__(NT, min_ctas_per_sm(NT, NS, BX, BY))
                 v.x = stencil7(B[r].x, xm, B[r].y, ym.x, yp.x, A[r].x, C[r].x);
                 v.y = stencil7(B[r].y, B[r].x, xp1, ym.y, yp.y, A[r].y, C[r].y);
                 ST16(a, op + r * P, v);
-                // x face: rows r-1 and r of this lane are adjacent in the neighbour's x-ghost
-                // array, so an even row count stores them as one 16-byte pair (half the
-                // transactions; over NVLink a lone 8-byte store travels as its own transfer)
-                if (XE && xf) {
-                    const double xv = ilo ? v.x : v.y;
-                    if (RY % 2 == 0 && xv2) {
-                        if (r & 1) ST16(a, xf + r - 1, make_double2(xprev, xv));
-                        else xprev = xv;
-                    } else {
-                        ST8(a, xf + r, xv);
-                    }
-                }
+                if (XE && xput) xface[q & 1][xside][jl0 + r] = ilo ? v.x : v.y;
                 if (XE && yf && ((r == 0 && yf_lo) || (r == RY - 1 && !yf_lo))) {
                     // one 16-byte store (NVLink sends a half-written 32-byte sector as its own
                     // transfer); packed rows of odd width ex are only 8-byte aligned
@@ -693,9 +697,15 @@ __global__ void __launch_bounds__(NT, min_ctas_per_sm(NT, NS, BX, BY))
                 }
             }
             op += Qs;
-            if (XE && xf) xf += xs;
             if (XE && yf) yf += ys;
-            refill(q);  // centre plane done
+            refill(q);  // centre plane done; its x-face values are in shared memory
+            if (XE && xf) {
+                const double2 pv = *reinterpret_cast<const double2 *>(
+                    &xface[q & 1][(int)threadIdx.x / (BY / 2)][2 * ((int)threadIdx.x % (BY / 2))]);
+                if (xv2) ST16(a, xf, pv);
+                else { ST8(a, xf, pv.x); ST8(a, xf + 1, pv.y); }
+                xf += xs;
+            }
             ++q;
             Sc = Sn;
             if (++sn == NSL) { sn = 0; pn ^= 1u; }
