@@ -826,12 +826,24 @@ __global__ void __launch_bounds__(NT, 4) sweep2d_tma_kernel(const __grid_constan
     const int jl0 = rg * RY;
     const int sb = (jl0 + 1) * W + col;
     const int xg = L::XG_OFF + jl0;
-    double *xf = nullptr;  // x-face target, element j at xf + j (plane k = 0)
-    if (xfull && exch && (ilo || ihi1)) {
-        const int f = ilo ? XM : XP;
-        if (a.mode == MODE_FUSED) xf = blk.nb[f][dst];
-        else if (blk.nb[f][0]) xf = a.outbox + (int64_t)slot * g.ostride + g.ooff[f];
+    // x faces as in the 3-D sweep: the face lanes put their values in shared memory, and
+    // after the tile's barrier the first BY threads store each side's rows, two per
+    // thread, as one contiguous run per instruction.
+    auto xtarget = [&](int f) -> double * {  // element j at p + j (plane k = 0)
+        if (a.mode == MODE_FUSED) return blk.nb[f][dst];
+        return blk.nb[f][0] ? a.outbox + (int64_t)slot * g.ostride + g.ooff[f] : nullptr;
+    };
+    const bool xput = xfull && exch && (ilo || ihi1) && xtarget(ilo ? XM : XP) != nullptr;
+    const int xside = ilo ? 0 : 1;
+    double *xst = nullptr;  // threads < BY: rows 2l, 2l+1 of one side
+    if (xfull && exch && (int)threadIdx.x < BY) {
+        const int side = (int)threadIdx.x / (BY / 2);
+        if (side == 0 ? xlo : xhi) {
+            xst = xtarget(side ? XP : XM);
+            if (xst) xst += 2 * ((int)threadIdx.x % (BY / 2));
+        }
     }
+    __shared__ __align__(16) double xface[2][2][BY];  // [tile parity][side][row]
     // general y tile: every store through emit_pair
     auto tile_general = [&](int q) {
         mbar_wait(&bars[q % NS], (q / NS) & 1);
@@ -869,7 +881,7 @@ __global__ void __launch_bounds__(NT, 4) sweep2d_tma_kernel(const __grid_constan
         int sl = q % NS;                    // ring slot of tile q
         uint32_t ph = (q / NS) & 1u;        // its mbarrier parity
         double *op = own + (int64_t)((ty0 + q) * BY + jl0 + 1) * g.P + g.A + i;
-        double *xfp = xf ? xf + (ty0 + q) * BY + jl0 : nullptr;
+        double *xfp = xst ? xst + (int64_t)(ty0 + q) * BY : nullptr;
         const int64_t P = g.P, TP = (int64_t)BY * g.P;
         auto run = [&](const bool XE) {
             for (; q < qend; ++q) {
@@ -879,7 +891,6 @@ __global__ void __launch_bounds__(NT, 4) sweep2d_tma_kernel(const __grid_constan
                 double2 rw[RY + 2];  // rows jl0-1 .. jl0+RY
 #pragma unroll
                 for (int r = 0; r < RY + 2; ++r) rw[r] = *reinterpret_cast<const double2 *>(Sb + (r - 1) * W);
-                double xprev = 0.0;  // x-face value of the previous row (see the 3-D sweep)
 #pragma unroll
                 for (int r = 0; r < RY; ++r) {
                     double xm = Sb[r * W - 1], xp1 = Sb[r * W + 2];
@@ -892,20 +903,16 @@ __global__ void __launch_bounds__(NT, 4) sweep2d_tma_kernel(const __grid_constan
                     v.x = stencil5(c.x, xm, c.y, rw[r].x, rw[r + 2].x);
                     v.y = stencil5(c.y, c.x, xp1, rw[r].y, rw[r + 2].y);
                     ST16(a, op + r * P, v);
-                    if (XE && xfp) {  // row pairs: one 16-byte store (the x-ghost pitch eyp is even)
-                        const double xv = ilo ? v.x : v.y;
-                        if (RY % 2 == 0) {
-                            if (r & 1) ST16(a, xfp + r - 1, make_double2(xprev, xv));
-                            else xprev = xv;
-                        } else {
-                            ST8(a, xfp + r, xv);
-                        }
-                    }
+                    if (XE && xput) xface[q & 1][xside][jl0 + r] = ilo ? v.x : v.y;
                 }
                 op += TP;
-                if (XE && xfp) xfp += BY;
                 __syncthreads();
                 if (threadIdx.x == 0 && q + NS < nq) issue(q + NS);
+                if (XE && xfp) {  // row pairs of the x-ghost array (element j at xfp + j; even offsets)
+                    ST16(a, xfp, *reinterpret_cast<const double2 *>(
+                                     &xface[q & 1][(int)threadIdx.x / (BY / 2)][2 * ((int)threadIdx.x % (BY / 2))]));
+                    xfp += BY;
+                }
                 if (++sl == NS) { sl = 0; ph ^= 1u; }
             }
         };
