@@ -26,8 +26,7 @@ void run(torch::Tensor s, torch::Tensor d, int rows) {
 m = load_inline("pitch_copy_probe", cpp_sources="void run(torch::Tensor s, torch::Tensor d, int rows);",
                 cuda_sources=src, functions=["run"], extra_cuda_cflags=["-O3", "-gencode", "arch=compute_100a,code=sm_100a"],
                 verbose=False)
-total = 1 << 29  # doubles per array (4 GiB)
-for rows in (16, 128):
+for total, rows in ((1 << 29, 16), (1 << 29, 128), (1 << 27, 16), (1 << 27, 128)):  # doubles per array: 4 GiB, 1 GiB
     res = {}
     for width in (32768, 131072, 32768, 131072):
         s = torch.rand((total // width, width), dtype=torch.float64, device="cuda")
@@ -41,5 +40,5 @@ for rows in (16, 128):
         ms = e0.elapsed_time(e1) / 10
         res.setdefault(width, []).append(ms)
         del s, d
-    print(f"tile rows {rows}: " + "  ".join(f"width {w}: {min(v):.3f} ms ({2 * total * 8 / (min(v) * 1e-3) / 1e12:.2f} TB/s)"
+    print(f"{total * 8 >> 30} GiB arrays, tile rows {rows}: " + "  ".join(f"width {w}: {min(v):.3f} ms ({2 * total * 8 / (min(v) * 1e-3) / 1e12:.2f} TB/s)"
                                            for w, v in res.items()), flush=True)
