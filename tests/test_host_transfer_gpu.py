@@ -116,3 +116,30 @@ def test_interior_box_readback(monkeypatch, pitched):
         short = np.zeros((dims[2] - 1, dims[1], dims[0]))
         with pytest.raises(jb.jacobi3d.JacError):
             s.field_box(short, (1, 1, 1))
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_staged_transfer_fuzz(monkeypatch, seed):
+    """Random shapes, block grids, slab sizes and copy paths (linear, pitched, zero-copy
+    from pinned memory): init + read-back round trip and one sweep against the oracle."""
+    rng = np.random.default_rng(1000 + seed)
+    monkeypatch.setenv("JAC_EXPERIMENT", "1")
+    monkeypatch.setenv("JAC_STAGE_BYTES", str(int(rng.integers(1, 200000))))
+    if rng.random() < 0.5:
+        monkeypatch.setenv("JAC_STAGE_PITCHED", "1")
+    blocks = tuple(int(b) for b in rng.integers(1, 4, size=3))
+    dims = tuple(int(b * e) for b, e in zip(blocks, rng.integers(2, 12, size=3) * 2))
+    u0 = JI.hash_field(*dims, seed=20 + seed)
+    pinned = rng.random() < 0.5
+    if pinned:
+        torch = pytest.importorskip("torch")
+        h = torch.empty(u0.shape, dtype=torch.float64, pin_memory=True).numpy()
+        h[...] = u0
+        u_in = h
+    else:
+        u_in = u0
+    with jb.Jacobi3D(dims, blocks) as s:
+        s.set_init_box(u_in, (0, 0, 0))
+        _bits(s.field(u0), u0)
+        s.step(1)
+        _bits(s.field(u0), oracle.jacobi3d(u0, 1))
