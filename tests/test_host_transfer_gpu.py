@@ -143,3 +143,20 @@ def test_staged_transfer_fuzz(monkeypatch, seed):
         _bits(s.field(u0), u0)
         s.step(1)
         _bits(s.field(u0), oracle.jacobi3d(u0, 1))
+
+
+def test_pinned_x_split_group(monkeypatch):
+    """One process, two GPUs split in x: each device's partial-row sub-box of one pinned
+    host array takes the zero-copy init (the array was pinned by device 0's context)."""
+    torch = pytest.importorskip("torch")
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    dims = (96, 40, 36)
+    u0 = JI.hash_field(*dims, seed=31)
+    h = torch.empty(u0.shape, dtype=torch.float64, pin_memory=True).numpy()
+    h[...] = u0
+    with jb.Jacobi3D(dims, (2, 1, 1), n_gpus=2, gpu_grid=(2, 1, 1)) as s:
+        s.set_init_box(h, (0, 0, 0))
+        _bits(s.field(u0), u0)
+        s.step(3)
+        _bits(s.field(u0), oracle.jacobi3d(u0, 3))
